@@ -1,0 +1,175 @@
+"""Python driver for the CPU oracle (oracle/twofold_oracle.c).
+
+TEST INFRASTRUCTURE ONLY.  Imported by tests/, __graft_entry__.smoke() and the
+cpu_baseline / --impl reference legs of bench.py -- never by the product
+package.  It evaluates the reference algorithm (pkg/src/twofold/explog.py:265-467)
+op for op on the CPU:
+
+  binary64: one C pass, libm = glibc (the library CPython's math calls);
+  binary32: replay passes, libm = numpy float32 ufuncs (the reference's
+            _Libm32, _fp.py:221-245), evaluated vectorised between passes.
+
+Parity pinning: tests/test_oracle_golden.py checks this oracle bit-for-bit
+against outputs of the reference package itself (tests/golden/*.npz, produced
+by tests/golden/gen_golden.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "build", "libtforacle.so")
+
+FNS = {"texp": 0, "texpm1": 1, "tlog": 2, "tlog1p": 3}
+_LIBM32 = {0: np.exp, 1: np.expm1, 2: np.log, 3: np.log1p}
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with its Makefile (gcc, -ffp-contract=off)."""
+    src = os.path.join(HERE, "twofold_oracle.c")
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", HERE], check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = ctypes.CDLL(LIB_PATH)
+        i64, i32, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+        L.tfo_eval_f64.argtypes = [i32, i32, vp, vp, vp, vp, i64, i32]
+        L.tfo_eval_f64.restype = i32
+        L.tfo_eval_f32_pass.argtypes = [i32, i32, vp, vp, vp, vp, i64, vp, i32, vp, vp, i32]
+        L.tfo_eval_f32_pass.restype = i64
+        L.tfo_maxcalls.restype = i32
+        for name in ("tfo_pexp0_raw64", "tfo_pexpm10_raw64", "tfo_taylor_exp64",
+                     "tfo_taylor_expm1_64"):
+            getattr(L, name).argtypes = [i32, ctypes.c_double, vp]
+        for name in ("tfo_pexp0_raw32", "tfo_pexpm10_raw32"):
+            getattr(L, name).argtypes = [i32, ctypes.c_float, vp]
+        L.tfo_decompose_exp64.argtypes = [ctypes.c_double, vp, vp]
+        L.tfo_decompose_expm1_64.argtypes = [ctypes.c_double, vp, vp]
+        L.tfo_decompose_exp32.argtypes = [ctypes.c_float, vp, vp]
+        L.tfo_decompose_expm1_32.argtypes = [ctypes.c_float, vp, vp]
+        L.tfo_eft64.argtypes = [i32, i32, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def default_threads() -> int:
+    return max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count() or 1)
+
+
+def evaluate(fn: str, width: int, x0, x1, backend: str = "dv", nthreads: int | None = None):
+    """Reference result (z0, z1) for arrays x0, x1 of the lane's dtype."""
+    L = lib()
+    code = FNS[fn]
+    dv = 1 if backend == "dv" else 0
+    if backend not in ("dv", "fma"):
+        raise ValueError(f"unknown backend {backend!r}")
+    nt = nthreads or default_threads()
+    if width == 64:
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        x1 = np.ascontiguousarray(x1, dtype=np.float64)
+        n = x0.size
+        z0 = np.empty(n, np.float64)
+        z1 = np.empty(n, np.float64)
+        rc = L.tfo_eval_f64(code, dv, _ptr(x0), _ptr(x1), _ptr(z0), _ptr(z1), n, nt)
+        if rc != 0:
+            raise RuntimeError("oracle rejected arguments")
+        return z0, z1
+    if width != 32:
+        raise ValueError(f"unsupported width {width!r}")
+    x0 = np.ascontiguousarray(x0, dtype=np.float32)
+    x1 = np.ascontiguousarray(x1, dtype=np.float32)
+    n = x0.size
+    mc = L.tfo_maxcalls()
+    z0 = np.full(n, np.nan, np.float32)
+    z1 = np.full(n, np.nan, np.float32)
+    ans = np.zeros((n, mc), np.float32)
+    req_arg = np.zeros(n, np.float32)
+    req_fn = np.full(n, -1, np.int8)
+    for k in range(mc + 1):
+        pending = L.tfo_eval_f32_pass(code, dv, _ptr(x0), _ptr(x1), _ptr(z0), _ptr(z1), n,
+                                      _ptr(ans), k, _ptr(req_arg), _ptr(req_fn), nt)
+        if pending < 0:
+            raise RuntimeError("oracle rejected arguments")
+        if pending == 0:
+            return z0, z1
+        if k == mc:
+            break
+        with np.errstate(all="ignore"):
+            for f, ufunc in _LIBM32.items():
+                sel = req_fn == f
+                if sel.any():
+                    ans[sel, k] = ufunc(req_arg[sel])
+    raise RuntimeError("binary32 oracle did not converge (more libm calls than expected)")
+
+
+# ---- building blocks (known-answer tests) -----------------------------------
+
+def pexp0_raw(x: float, width: int = 64, backend: str = "fma"):
+    out = np.zeros(2, np.float64 if width == 64 else np.float32)
+    f = lib().tfo_pexp0_raw64 if width == 64 else lib().tfo_pexp0_raw32
+    f(1 if backend == "dv" else 0, x, _ptr(out))
+    return float(out[0]), float(out[1])
+
+
+def pexpm10_raw(x: float, width: int = 64, backend: str = "fma"):
+    out = np.zeros(2, np.float64 if width == 64 else np.float32)
+    f = lib().tfo_pexpm10_raw64 if width == 64 else lib().tfo_pexpm10_raw32
+    f(1 if backend == "dv" else 0, x, _ptr(out))
+    return float(out[0]), float(out[1])
+
+
+def taylor_exp(y: float, backend: str = "fma"):
+    out = np.zeros(2, np.float64)
+    lib().tfo_taylor_exp64(1 if backend == "dv" else 0, y, _ptr(out))
+    return float(out[0]), float(out[1])
+
+
+def taylor_expm1(y: float, backend: str = "fma"):
+    out = np.zeros(2, np.float64)
+    lib().tfo_taylor_expm1_64(1 if backend == "dv" else 0, y, _ptr(out))
+    return float(out[0]), float(out[1])
+
+
+def decompose_exp(x: float, width: int = 64):
+    mn = np.zeros(2, np.int64)
+    y = np.zeros(1, np.float64 if width == 64 else np.float32)
+    f = lib().tfo_decompose_exp64 if width == 64 else lib().tfo_decompose_exp32
+    f(x, _ptr(mn), _ptr(y))
+    return int(mn[0]), int(mn[1]), float(y[0])
+
+
+def decompose_expm1(x: float, width: int = 64):
+    n = np.zeros(1, np.int64)
+    y = np.zeros(1, np.float64 if width == 64 else np.float32)
+    f = lib().tfo_decompose_expm1_64 if width == 64 else lib().tfo_decompose_expm1_32
+    f(x, _ptr(n), _ptr(y))
+    return 0, int(n[0]), float(y[0])
+
+
+_EFT_OPS = {"two_sum": 0, "fast_two_sum": 1, "renorm": 2, "t_add": 3, "t_add_d": 4,
+            "t_mul": 5, "t_mul_d": 6, "two_prod": 7}
+
+
+def eft64(op: str, *args: float, backend: str = "fma"):
+    a = np.zeros(4, np.float64)
+    a[: len(args)] = args
+    out = np.zeros(2, np.float64)
+    lib().tfo_eft64(_EFT_OPS[op], 1 if backend == "dv" else 0, _ptr(a), _ptr(out))
+    return float(out[0]), float(out[1])

@@ -1,0 +1,846 @@
+/*
+ * twofold_oracle.c -- CPU restatement of the reference twofold texp/texpm1/
+ * tlog/tlog1p path, op for op.  TEST INFRASTRUCTURE ONLY: it is the parity
+ * checker for the CUDA kernels and the CPU baseline arm of bench.py; nothing
+ * in the product package links or calls it.
+ *
+ * Every function below restates one function of the reference Python package
+ * (/root/reference/pkg/src/twofold, cited file:line) in C with the SAME
+ * sequence of IEEE operations.  Compile with -ffp-contract=off -fno-builtin
+ * and without -ffast-math: each + - * is one correctly rounded IEEE op, and
+ * fma()/fmaf() is used exactly where the reference calls its fused residual.
+ *
+ * Exact-residual backends (eft.py:254-264, eft32.py:180-190):
+ *   dv  = Dekker-Veltkamp split (what the reference runs in this image: no
+ *         gmpy2, no math.fma -> _fp.default_backend_name() == "dv");
+ *   fma = single-rounding fused multiply-add.
+ *
+ * Platform libm (_fp.py:191-245):
+ *   binary64 -> glibc exp/expm1/log/log1p, the same entry points CPython's
+ *               math module calls (linked directly, -fno-builtin);
+ *   binary32 -> numpy float32 ufuncs.  C cannot call numpy, so the binary32
+ *               lane runs in "replay" passes: call k of an element returns the
+ *               k-th answer supplied by the Python driver (oracle/oracle.py),
+ *               or records its (function, argument) request and poisons the
+ *               rest of the element.  The driver evaluates requests with numpy
+ *               and re-runs until no element is pending (<= 4 passes).
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "../paper_1502_05216_b200/csrc/tf_tables.h"
+
+#define EXPORT __attribute__((visibility("default")))
+
+enum { FN_TEXP = 0, FN_TEXPM1 = 1, FN_TLOG = 2, FN_TLOG1P = 3 };
+enum { LM_EXP = 0, LM_EXPM1 = 1, LM_LOG = 2, LM_LOG1P = 3, LM_NONE = -1 };
+#define MAXCALLS 4
+
+/* ======================================================================== */
+/* binary64 lane                                                             */
+/* ======================================================================== */
+
+typedef struct { double v, e; } tf64;
+
+static inline tf64 mk64(double v, double e) { tf64 t = {v, e}; return t; }
+
+/* _special (eft.py:65-74): NaN value -> (v, v); NaN operand -> (v, NaN). */
+static inline tf64 special64(double v, int any_nan) {
+    if (isnan(v)) return mk64(v, v);
+    if (any_nan) return mk64(v, NAN);
+    return mk64(v, v);
+}
+#define N2(a, b) (isnan(a) || isnan(b))
+#define N3(a, b, c) (isnan(a) || isnan(b) || isnan(c))
+#define N4(a, b, c, d) (isnan(a) || isnan(b) || isnan(c) || isnan(d))
+
+/* fast_two_sum (eft.py:77-82) */
+static tf64 fast_two_sum64(double a, double b) {
+    double s = a + b;
+    if (isfinite(s)) return mk64(s, b - (s - a));
+    return special64(s, N2(a, b));
+}
+
+/* two_sum (eft.py:85-92) */
+static tf64 two_sum64(double a, double b) {
+    double s = a + b;
+    if (isfinite(s)) {
+        double bp = s - a;
+        double ap = s - bp;
+        return mk64(s, (a - ap) + (b - bp));
+    }
+    return special64(s, N2(a, b));
+}
+
+/* renorm (eft.py:168-171) */
+static tf64 renorm64(tf64 x) {
+    tf64 t = two_sum64(x.v, x.e);
+    return fast_two_sum64(t.v, t.e);
+}
+
+/* split (eft.py:107-128) */
+static void split64(double x, double* hi, double* lo) {
+    const double S = 134217729.0;
+    if (fabs(x) > 0x1p996) {
+        double xs = x * 0x1p-28;
+        double a = S * xs;
+        double b = a - xs;
+        double h = a - b;
+        if (fabs(h) == 0x1p996) h = copysign(0x1p996 - 0x1p970, h);
+        *hi = h * 0x1p28;
+        *lo = (xs - h) * 0x1p28;
+        return;
+    }
+    double a = S * x;
+    double b = a - x;
+    double h = a - b;
+    *hi = h;
+    *lo = x - h;
+}
+
+/* _prod_err_fma / _prod_err_dv (eft.py:254-264) */
+static double prod_err64(int dv, double x, double y, double v) {
+    if (!dv) return fma(x, y, -v);
+    double xh, xl, yh, yl;
+    split64(x, &xh, &xl);
+    split64(y, &yh, &yl);
+    double e0 = v - xh * yh;
+    double e1 = e0 - xh * yl;
+    double e2 = e1 - xl * yh;
+    return xl * yl - e2;
+}
+
+/* t_add (eft.py:182-189) */
+static tf64 t_add64(tf64 x, tf64 y) {
+    double s = x.v + y.v;
+    if (!isfinite(s)) return special64(s, N4(x.v, x.e, y.v, y.e));
+    double bp = s - x.v;
+    double ap = s - bp;
+    double e = (x.v - ap) + (y.v - bp);
+    return mk64(s, e + (x.e + y.e));
+}
+
+/* t_add_d (eft.py:192-199) */
+static tf64 t_add_d64(tf64 x, double b) {
+    double s = x.v + b;
+    if (!isfinite(s)) return special64(s, N3(x.v, x.e, b));
+    double bp = s - x.v;
+    double ap = s - bp;
+    double e = (x.v - ap) + (b - bp);
+    return mk64(s, e + x.e);
+}
+
+/* t_mul (eft.py:207-212) */
+static tf64 t_mul64(int dv, tf64 x, tf64 y) {
+    double v = x.v * y.v;
+    if (!isfinite(v)) return special64(v, N4(x.v, x.e, y.v, y.e));
+    double e = prod_err64(dv, x.v, y.v, v);
+    return mk64(v, e + (x.v * y.e + x.e * y.v));
+}
+
+/* t_mul_d (eft.py:214-219) */
+static tf64 t_mul_d64(int dv, tf64 x, double b) {
+    double v = x.v * b;
+    if (!isfinite(v)) return special64(v, N3(x.v, x.e, b));
+    double e = prod_err64(dv, x.v, b, v);
+    return mk64(v, x.e * b + e);
+}
+
+/* params.py:276-293 */
+#define LO64 (-0x1.74385446d71c4p+9)
+#define HI64 (0x1.62e42fefa39f0p+9)
+static const tf64 LN2_64 = {TF64_LN2_V, TF64_LN2_E};
+static const tf64 INVF_64 = {TF64_INVFACT_V, TF64_INVFACT_E};
+
+static inline tf64 tab64(const double* t, int lo, int64_t i) {
+    return mk64(t[2 * (i - lo)], t[2 * (i - lo) + 1]);
+}
+
+/* decompose_exp (expcore.py:35-50): x = 4m + n/32 + y exactly. */
+static void decompose_exp64(double x, int64_t* m, int64_t* n, double* y) {
+    double M = nearbyint(x * 32.0);      /* Python round(): ties-to-even */
+    *y = x - M / 32.0;
+    int64_t Mi = (int64_t)M;
+    int64_t a = Mi < 0 ? -Mi : Mi;
+    if (Mi >= 0) { *m = a / 128; *n = a % 128; }
+    else { *m = -(a / 128); *n = -(a % 128); }
+}
+
+/* decompose_expm1 (expcore.py:53-58) */
+static void decompose_expm1_64(double x, int64_t* n, double* y) {
+    double M = nearbyint(x * 128.0);
+    *y = x - M / 128.0;
+    *n = (int64_t)M;
+}
+
+/* _seed + taylor_exp (expcore.py:82-105): coeffs 12!/k!, 3 dotted steps. */
+static tf64 taylor_exp64(int dv, double y) {
+    static const double c[13] = {1.0, 12.0, 132.0, 1320.0, 11880.0, 95040.0,
+                                 665280.0, 3991680.0, 19958400.0, 79833600.0,
+                                 239500800.0, 479001600.0, 479001600.0};
+    double s = y + c[1];
+    s = s * y + c[2];
+    s = s * y + c[3];
+    tf64 t = mk64(s, 0.0);
+    for (int k = 4; k <= 12; ++k) t = t_add_d64(t_mul_d64(dv, t, y), c[k]);
+    return t;
+}
+
+/* taylor_expm1 (expcore.py:107-116): coeffs 10!/k! k=10..1, times 1/10!. */
+static tf64 taylor_expm1_64(int dv, double y) {
+    static const double c[10] = {1.0, 10.0, 90.0, 720.0, 5040.0, 30240.0,
+                                 151200.0, 604800.0, 1814400.0, 3628800.0};
+    double s = y + c[1];
+    s = s * y + c[2];
+    s = s * y + c[3];
+    tf64 t = mk64(s, 0.0);
+    for (int k = 4; k <= 9; ++k) t = t_add_d64(t_mul_d64(dv, t, y), c[k]);
+    t = t_mul_d64(dv, t, y);
+    return t_mul64(dv, t, INVF_64);
+}
+
+/* pexp0_raw (expcore.py:120-133) */
+static tf64 pexp0_raw64(int dv, double x) {
+    if (isnan(x)) return mk64(NAN, NAN);
+    if (x < LO64) return mk64(0.0, 0.0);
+    if (x > HI64) return mk64(INFINITY, INFINITY);
+    int64_t m, n;
+    double y;
+    decompose_exp64(x, &m, &n, &y);
+    tf64 e = tab64(TF64_E, TF64_E_LO, m);
+    tf64 c = tab64(TF64_C, TF64_C_LO, n);
+    tf64 t = taylor_exp64(dv, y);
+    return t_mul64(dv, e, t_mul64(dv, c, t));
+}
+
+/* pexpm10_raw (expcore.py:138-147) */
+static tf64 pexpm10_raw64(int dv, double x) {
+    if (isnan(x)) return mk64(NAN, NAN);
+    if (fabs(x) <= LN2_64.v) {
+        int64_t n;
+        double y;
+        decompose_expm1_64(x, &n, &y);
+        tf64 c = tab64(TF64_CM1, TF64_CM1_LO, n);
+        tf64 t = taylor_expm1_64(dv, y);
+        return t_add64(t_mul64(dv, c, t), t_add64(c, t));
+    }
+    return t_add_d64(pexp0_raw64(dv, x), -1.0);
+}
+
+/* glibc libm behind CPython math, with _Libm64's exception mapping
+ * (_fp.py:191-218): the C entry points already return inf/-inf/NaN there. */
+static double lm64(int f, double x) {
+    switch (f) {
+        case LM_EXP: return exp(x);
+        case LM_EXPM1: return expm1(x);
+        case LM_LOG: return log(x);
+        default: return log1p(x);
+    }
+}
+
+/* ExpLog.texp (explog.py:265-275) */
+static tf64 texp64(int dv, double x0, double x1) {
+    tf64 v = pexp0_raw64(dv, x0);
+    double z0 = lm64(LM_EXP, x0);
+    if (z0 == v.v && isinf(z0)) return mk64(z0, z0);
+    double t1 = lm64(LM_EXPM1, x1);
+    return mk64(z0, (z0 * t1) + (v.e + (v.v - z0)));
+}
+
+/* ExpLog.texpm1 (explog.py:299-310) */
+static tf64 texpm1_64(int dv, double x0, double x1) {
+    tf64 w = pexpm10_raw64(dv, x0);
+    double z0 = lm64(LM_EXPM1, x0);
+    if (z0 == w.v && isinf(z0)) return mk64(z0, z0);
+    double t1 = lm64(LM_EXPM1, x1);
+    double tail = w.e + (w.v - z0);
+    return mk64(z0, ((z0 + 1.0) * t1) + tail);
+}
+
+#define NEWTON_TOL 0x1p-20 /* explog.py:205 */
+
+/* _newton_log_z (explog.py:320-336) */
+static double newton_log_z64(int dv, double z0, double z1, double r0) {
+    tf64 s = pexpm10_raw64(dv, -r0);
+    double zm1 = z0 - 1.0;
+    tf64 u;
+    if (z1 == 0.0) {
+        u = t_add_d64(t_mul_d64(dv, s, z0), zm1);
+    } else {
+        tf64 w = fast_two_sum64(zm1, z1);
+        u = t_add64(t_mul64(dv, mk64(z0, z1), s), w);
+    }
+    return u.v + u.e;
+}
+
+/* _log_core (explog.py:338-358) */
+static tf64 log_core64(int dv, double y0, double y1) {
+    double z0, z1;
+    int n = 0;
+    if (y0 < 0.5 || y0 > 2.0) {
+        if (isfinite(y0) && y0 != 0.0) z0 = frexp(y0, &n);
+        else z0 = y0; /* Python math.frexp(inf/nan/0) -> (x, 0) */
+        z1 = (y1 != 0.0) ? ldexp(y1, -n) : 0.0;
+    } else {
+        z0 = y0;
+        z1 = y1;
+    }
+    double r0 = (y1 == 0.0 && z1 == 0.0) ? lm64(LM_LOG, z0)
+                                          : lm64(LM_LOG1P, (z0 - 1.0) + z1);
+    double r1 = newton_log_z64(dv, z0, z1, r0);
+    if (fabs(r1) > NEWTON_TOL * fabs(r0) + NEWTON_TOL) {
+        r0 = r0 + r1;
+        r1 = newton_log_z64(dv, z0, z1, r0);
+    }
+    if (n == 0) return mk64(r0, r1);
+    tf64 nl = t_mul_d64(dv, LN2_64, (double)n);
+    return t_add64(mk64(r0, r1), nl);
+}
+
+/* _correct (explog.py:366-373) */
+static tf64 correct64(tf64 core, double lib0) {
+    if (isinf(lib0) && core.v == lib0) return mk64(lib0, lib0);
+    return mk64(lib0, core.e + (core.v - lib0));
+}
+
+/* ExpLog.tlog (explog.py:394-399) */
+static tf64 tlog64(int dv, double y0, double y1) {
+    tf64 v = renorm64(mk64(y0, y1));
+    tf64 core = log_core64(dv, v.v, v.e);
+    return correct64(core, lm64(LM_LOG, y0));
+}
+
+/* ExpLog.tlogp (explog.py:389-392) */
+static tf64 tlogp64(int dv, tf64 y) {
+    tf64 core = log_core64(dv, y.v, y.e);
+    return correct64(core, lm64(LM_LOG, y.v));
+}
+
+/* _newton_log1p_in_band (explog.py:410-424) */
+static double newton_log1p64(int dv, double y0, double y1, double x0) {
+    tf64 s = pexpm10_raw64(dv, -x0);
+    tf64 u;
+    if (y1 == 0.0) {
+        tf64 w = fast_two_sum64(1.0, y0);
+        u = t_add_d64(t_mul64(dv, w, s), y0);
+    } else {
+        tf64 ys = t_mul64(dv, mk64(y0, y1), s);
+        u = t_add64(t_add64(ys, mk64(y0, y1)), s);
+    }
+    return u.v + u.e;
+}
+
+/* _log1p_core (explog.py:426-432) */
+static tf64 log1p_core64(int dv, double y0, double y1) {
+    double x0 = lm64(LM_LOG1P, y0);
+    double x1 = newton_log1p64(dv, y0, y1, x0);
+    if (fabs(x1) > NEWTON_TOL * fabs(x0) + NEWTON_TOL) {
+        x0 = x0 + x1;
+        x1 = newton_log1p64(dv, y0, y1, x0);
+    }
+    return mk64(x0, x1);
+}
+
+/* _plog1p_raw (explog.py:440-444) */
+static tf64 plog1p_raw64(int dv, tf64 y) {
+    if (y.v < -0.5 || y.v > 1.0) {
+        tf64 w = renorm64(t_add_d64(y, 1.0));
+        return tlogp64(dv, w);
+    }
+    return log1p_core64(dv, y.v, y.e);
+}
+
+/* ExpLog.tlog1p (explog.py:464-467) */
+static tf64 tlog1p64(int dv, double y0, double y1) {
+    tf64 v = renorm64(mk64(y0, y1));
+    tf64 core = plog1p_raw64(dv, v);
+    return correct64(core, lm64(LM_LOG1P, y0));
+}
+
+static tf64 eval64(int fn, int dv, double x0, double x1) {
+    switch (fn) {
+        case FN_TEXP: return texp64(dv, x0, x1);
+        case FN_TEXPM1: return texpm1_64(dv, x0, x1);
+        case FN_TLOG: return tlog64(dv, x0, x1);
+        default: return tlog1p64(dv, x0, x1);
+    }
+}
+
+/* ======================================================================== */
+/* binary32 lane (eft32.py, expcore.py with rnd=r32, explog.py width=32)     */
+/* Native float arithmetic == r32-narrowed double arithmetic (_fp.py:1-8).   */
+/* ======================================================================== */
+
+typedef struct { float v, e; } tf32;
+static inline tf32 mk32(float v, float e) { tf32 t = {v, e}; return t; }
+
+static inline tf32 special32(float v, int any_nan) {
+    if (isnan(v)) return mk32(v, v);
+    if (any_nan) return mk32(v, NAN);
+    return mk32(v, v);
+}
+
+/* eft32.py:36-40 */
+static tf32 fast_two_sum32(float a, float b) {
+    float s = a + b;
+    if (isfinite(s)) return mk32(s, b - (s - a));
+    return special32(s, N2(a, b));
+}
+
+/* eft32.py:43-49 */
+static tf32 two_sum32(float a, float b) {
+    float s = a + b;
+    if (isfinite(s)) {
+        float bp = s - a;
+        float ap = s - bp;
+        return mk32(s, (a - ap) + (b - bp));
+    }
+    return special32(s, N2(a, b));
+}
+
+/* eft32.py:117-119 */
+static tf32 renorm32(tf32 x) {
+    tf32 t = two_sum32(x.v, x.e);
+    return fast_two_sum32(t.v, t.e);
+}
+
+/* eft32.py:63-82 */
+static void split32(float x, float* hi, float* lo) {
+    const float S = 4097.0f;
+    if (fabsf(x) > 0x1p115f) {
+        float xs = x * 0x1p-13f;
+        float a = S * xs;
+        float b = a - xs;
+        float h = a - b;
+        if (fabsf(h) == 0x1p115f) h = copysignf(0x1p115f - 0x1p103f, h);
+        *hi = h * 0x1p13f;
+        *lo = (xs - h) * 0x1p13f;
+        return;
+    }
+    float a = S * x;
+    float b = a - x;
+    float h = a - b;
+    *hi = h;
+    *lo = x - h;
+}
+
+/* eft32.py:180-190; fma32 (_fp.py:112-127) is a correctly rounded fmaf */
+static float prod_err32(int dv, float x, float y, float v) {
+    if (!dv) return fmaf(x, y, -v);
+    float xh, xl, yh, yl;
+    split32(x, &xh, &xl);
+    split32(y, &yh, &yl);
+    float e0 = v - xh * yh;
+    float e1 = e0 - xh * yl;
+    float e2 = e1 - xl * yh;
+    return xl * yl - e2;
+}
+
+/* eft32.py:122-129 */
+static tf32 t_add32(tf32 x, tf32 y) {
+    float s = x.v + y.v;
+    if (!isfinite(s)) return special32(s, N4(x.v, x.e, y.v, y.e));
+    float bp = s - x.v;
+    float ap = s - bp;
+    float e = (x.v - ap) + (y.v - bp);
+    return mk32(s, e + (x.e + y.e));
+}
+
+/* eft32.py:132-139 */
+static tf32 t_add_d32(tf32 x, float b) {
+    float s = x.v + b;
+    if (!isfinite(s)) return special32(s, N3(x.v, x.e, b));
+    float bp = s - x.v;
+    float ap = s - bp;
+    float e = (x.v - ap) + (b - bp);
+    return mk32(s, e + x.e);
+}
+
+/* eft32.py:147-152 */
+static tf32 t_mul32(int dv, tf32 x, tf32 y) {
+    float v = x.v * y.v;
+    if (!isfinite(v)) return special32(v, N4(x.v, x.e, y.v, y.e));
+    float e = prod_err32(dv, x.v, y.v, v);
+    return mk32(v, e + ((x.v * y.e) + (x.e * y.v)));
+}
+
+/* eft32.py:154-159 */
+static tf32 t_mul_d32(int dv, tf32 x, float b) {
+    float v = x.v * b;
+    if (!isfinite(v)) return special32(v, N3(x.v, x.e, b));
+    float e = prod_err32(dv, x.v, b, v);
+    return mk32(v, (x.e * b) + e);
+}
+
+/* params.py:295-312 */
+#define LO32 (-0x1.9d1da0p+6f)
+#define HI32 (0x1.62e430p+6f)
+static const tf32 LN2_32 = {TF32_LN2_V, TF32_LN2_E};
+static const tf32 INVF_32 = {TF32_INVFACT_V, TF32_INVFACT_E};
+
+static inline tf32 tab32(const float* t, int lo, int64_t i) {
+    return mk32(t[2 * (i - lo)], t[2 * (i - lo) + 1]);
+}
+
+/* decompose_exp (expcore.py:35-50) with L=1, K=5: the double-precision
+ * scaling and subtraction are exact, so y is an exact binary32. */
+static void decompose_exp32(float x, int64_t* m, int64_t* n, float* y) {
+    double xd = x;
+    double M = nearbyint(xd * 32.0);
+    *y = (float)(xd - M / 32.0);
+    int64_t Mi = (int64_t)M;
+    int64_t a = Mi < 0 ? -Mi : Mi;
+    if (Mi >= 0) { *m = a / 64; *n = a % 64; }
+    else { *m = -(a / 64); *n = -(a % 64); }
+}
+
+static void decompose_expm1_32(float x, int64_t* n, float* y) {
+    double xd = x;
+    double M = nearbyint(xd * 128.0);
+    *y = (float)(xd - M / 128.0);
+    *n = (int64_t)M;
+}
+
+/* taylor_exp, N=6, 2 dotted steps (expcore.py:82-105) */
+static tf32 taylor_exp32(int dv, float y) {
+    static const float c[7] = {1.f, 6.f, 30.f, 120.f, 360.f, 720.f, 720.f};
+    float s = y + c[1];
+    s = (s * y) + c[2];
+    tf32 t = mk32(s, 0.0f);
+    for (int k = 3; k <= 6; ++k) t = t_add_d32(t_mul_d32(dv, t, y), c[k]);
+    return t;
+}
+
+/* taylor_expm1, N_m1=5 (expcore.py:107-116) */
+static tf32 taylor_expm1_32(int dv, float y) {
+    static const float c[5] = {1.f, 5.f, 20.f, 60.f, 120.f};
+    float s = y + c[1];
+    s = (s * y) + c[2];
+    tf32 t = mk32(s, 0.0f);
+    for (int k = 3; k <= 4; ++k) t = t_add_d32(t_mul_d32(dv, t, y), c[k]);
+    t = t_mul_d32(dv, t, y);
+    return t_mul32(dv, t, INVF_32);
+}
+
+static tf32 pexp0_raw32(int dv, float x) {
+    if (isnan(x)) return mk32(NAN, NAN);
+    if (x < LO32) return mk32(0.0f, 0.0f);
+    if (x > HI32) return mk32(INFINITY, INFINITY);
+    int64_t m, n;
+    float y;
+    decompose_exp32(x, &m, &n, &y);
+    tf32 e = tab32(TF32_E, TF32_E_LO, m);
+    tf32 c = tab32(TF32_C, TF32_C_LO, n);
+    tf32 t = taylor_exp32(dv, y);
+    return t_mul32(dv, e, t_mul32(dv, c, t));
+}
+
+static tf32 pexpm10_raw32(int dv, float x) {
+    if (isnan(x)) return mk32(NAN, NAN);
+    if (fabsf(x) <= LN2_32.v) {
+        int64_t n;
+        float y;
+        decompose_expm1_32(x, &n, &y);
+        tf32 c = tab32(TF32_CM1, TF32_CM1_LO, n);
+        tf32 t = taylor_expm1_32(dv, y);
+        return t_add32(t_mul32(dv, c, t), t_add32(c, t));
+    }
+    return t_add_d32(pexp0_raw32(dv, x), -1.0f);
+}
+
+/* replayed numpy-float32 libm (see header comment) */
+typedef struct {
+    const float* ans; /* MAXCALLS answers of this element */
+    int n_known;
+    int k;
+    float* req_arg;
+    int8_t* req_fn;
+} L32;
+
+static float lm32(L32* L, int f, float x) {
+    int k = L->k++;
+    if (k < L->n_known) return L->ans[k];
+    if (k == L->n_known) {
+        *L->req_arg = x;
+        *L->req_fn = (int8_t)f;
+    }
+    return NAN;
+}
+
+static tf32 texp32(int dv, L32* L, float x0, float x1) {
+    tf32 v = pexp0_raw32(dv, x0);
+    float z0 = lm32(L, LM_EXP, x0);
+    if (z0 == v.v && isinf(z0)) return mk32(z0, z0);
+    float t1 = lm32(L, LM_EXPM1, x1);
+    return mk32(z0, (z0 * t1) + (v.e + (v.v - z0)));
+}
+
+static tf32 texpm1_32(int dv, L32* L, float x0, float x1) {
+    tf32 w = pexpm10_raw32(dv, x0);
+    float z0 = lm32(L, LM_EXPM1, x0);
+    if (z0 == w.v && isinf(z0)) return mk32(z0, z0);
+    float t1 = lm32(L, LM_EXPM1, x1);
+    float tail = w.e + (w.v - z0);
+    return mk32(z0, ((z0 + 1.0f) * t1) + tail);
+}
+
+static float newton_log_z32(int dv, float z0, float z1, float r0) {
+    tf32 s = pexpm10_raw32(dv, -r0);
+    float zm1 = z0 - 1.0f;
+    tf32 u;
+    if (z1 == 0.0f) {
+        u = t_add_d32(t_mul_d32(dv, s, z0), zm1);
+    } else {
+        tf32 w = fast_two_sum32(zm1, z1);
+        u = t_add32(t_mul32(dv, mk32(z0, z1), s), w);
+    }
+    return u.v + u.e;
+}
+
+/* the Newton-tolerance test runs in binary64 in the reference (plain Python
+ * float arithmetic, explog.py:351 and 429) */
+static inline int newton_again32(float r1, float r0) {
+    return fabs((double)r1) > NEWTON_TOL * fabs((double)r0) + NEWTON_TOL;
+}
+
+static tf32 log_core32(int dv, L32* L, float y0, float y1) {
+    float z0, z1;
+    int n = 0;
+    if (y0 < 0.5f || y0 > 2.0f) {
+        if (isfinite(y0) && y0 != 0.0f) z0 = (float)frexp((double)y0, &n);
+        else z0 = y0;
+        z1 = (y1 != 0.0f) ? (float)ldexp((double)y1, -n) : 0.0f;
+    } else {
+        z0 = y0;
+        z1 = y1;
+    }
+    float r0 = (y1 == 0.0f && z1 == 0.0f) ? lm32(L, LM_LOG, z0)
+                                            : lm32(L, LM_LOG1P, (z0 - 1.0f) + z1);
+    float r1 = newton_log_z32(dv, z0, z1, r0);
+    if (newton_again32(r1, r0)) {
+        r0 = r0 + r1;
+        r1 = newton_log_z32(dv, z0, z1, r0);
+    }
+    if (n == 0) return mk32(r0, r1);
+    tf32 nl = t_mul_d32(dv, LN2_32, (float)n);
+    return t_add32(mk32(r0, r1), nl);
+}
+
+static tf32 correct32(tf32 core, float lib0) {
+    if (isinf(lib0) && core.v == lib0) return mk32(lib0, lib0);
+    return mk32(lib0, core.e + (core.v - lib0));
+}
+
+static tf32 tlog32(int dv, L32* L, float y0, float y1) {
+    tf32 v = renorm32(mk32(y0, y1));
+    tf32 core = log_core32(dv, L, v.v, v.e);
+    return correct32(core, lm32(L, LM_LOG, y0));
+}
+
+static tf32 tlogp32(int dv, L32* L, tf32 y) {
+    tf32 core = log_core32(dv, L, y.v, y.e);
+    return correct32(core, lm32(L, LM_LOG, y.v));
+}
+
+static float newton_log1p32(int dv, float y0, float y1, float x0) {
+    tf32 s = pexpm10_raw32(dv, -x0);
+    tf32 u;
+    if (y1 == 0.0f) {
+        tf32 w = fast_two_sum32(1.0f, y0);
+        u = t_add_d32(t_mul32(dv, w, s), y0);
+    } else {
+        tf32 ys = t_mul32(dv, mk32(y0, y1), s);
+        u = t_add32(t_add32(ys, mk32(y0, y1)), s);
+    }
+    return u.v + u.e;
+}
+
+static tf32 log1p_core32(int dv, L32* L, float y0, float y1) {
+    float x0 = lm32(L, LM_LOG1P, y0);
+    float x1 = newton_log1p32(dv, y0, y1, x0);
+    if (newton_again32(x1, x0)) {
+        x0 = x0 + x1;
+        x1 = newton_log1p32(dv, y0, y1, x0);
+    }
+    return mk32(x0, x1);
+}
+
+static tf32 plog1p_raw32(int dv, L32* L, tf32 y) {
+    if (y.v < -0.5f || y.v > 1.0f) {
+        tf32 w = renorm32(t_add_d32(y, 1.0f));
+        return tlogp32(dv, L, w);
+    }
+    return log1p_core32(dv, L, y.v, y.e);
+}
+
+static tf32 tlog1p32(int dv, L32* L, float y0, float y1) {
+    tf32 v = renorm32(mk32(y0, y1));
+    tf32 core = plog1p_raw32(dv, L, v);
+    return correct32(core, lm32(L, LM_LOG1P, y0));
+}
+
+static tf32 eval32(int fn, int dv, L32* L, float x0, float x1) {
+    switch (fn) {
+        case FN_TEXP: return texp32(dv, L, x0, x1);
+        case FN_TEXPM1: return texpm1_32(dv, L, x0, x1);
+        case FN_TLOG: return tlog32(dv, L, x0, x1);
+        default: return tlog1p32(dv, L, x0, x1);
+    }
+}
+
+/* ======================================================================== */
+/* exported batch entry points                                               */
+/* ======================================================================== */
+
+/* tiny pthread parallel-for: [0, n) split into nthreads contiguous chunks */
+typedef struct {
+    void (*body)(void* ctx, int64_t lo, int64_t hi, int64_t* acc);
+    void* ctx;
+    int64_t lo, hi, acc;
+} chunk_t;
+
+static void* chunk_main(void* p) {
+    chunk_t* c = (chunk_t*)p;
+    c->body(c->ctx, c->lo, c->hi, &c->acc);
+    return NULL;
+}
+
+static int64_t parallel_for(int64_t n, int nthreads,
+                            void (*body)(void*, int64_t, int64_t, int64_t*), void* ctx) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    if ((int64_t)nthreads > n) nthreads = n > 0 ? (int)n : 1;
+    chunk_t ch[256];
+    pthread_t th[256];
+    int64_t acc = 0;
+    for (int t = 0; t < nthreads; ++t) {
+        ch[t].body = body;
+        ch[t].ctx = ctx;
+        ch[t].lo = n * t / nthreads;
+        ch[t].hi = n * (t + 1) / nthreads;
+        ch[t].acc = 0;
+    }
+    int started = 0;
+    for (int t = 1; t < nthreads; ++t)
+        if (pthread_create(&th[t], NULL, chunk_main, &ch[t]) == 0) started = t;
+        else { chunk_main(&ch[t]); }
+    chunk_main(&ch[0]);
+    for (int t = 1; t <= started; ++t) pthread_join(th[t], NULL);
+    for (int t = 0; t < nthreads; ++t) acc += ch[t].acc;
+    return acc;
+}
+
+typedef struct {
+    int fn, dv;
+    const double *x0, *x1;
+    double *z0, *z1;
+} job64_t;
+
+static void body64(void* p, int64_t lo, int64_t hi, int64_t* acc) {
+    job64_t* j = (job64_t*)p;
+    (void)acc;
+    for (int64_t i = lo; i < hi; ++i) {
+        tf64 r = eval64(j->fn, j->dv, j->x0[i], j->x1[i]);
+        j->z0[i] = r.v;
+        j->z1[i] = r.e;
+    }
+}
+
+EXPORT int tfo_eval_f64(int fn, int dv, const double* x0, const double* x1,
+                        double* z0, double* z1, int64_t n, int nthreads) {
+    if (fn < 0 || fn > 3 || n < 0) return -1;
+    job64_t j = {fn, dv, x0, x1, z0, z1};
+    parallel_for(n, nthreads, body64, &j);
+    return 0;
+}
+
+typedef struct {
+    int fn, dv, n_known;
+    const float *x0, *x1, *ans;
+    float *z0, *z1, *req_arg;
+    int8_t* req_fn;
+} job32_t;
+
+static void body32(void* p, int64_t lo, int64_t hi, int64_t* acc) {
+    job32_t* j = (job32_t*)p;
+    for (int64_t i = lo; i < hi; ++i) {
+        L32 L = {j->ans + (size_t)i * MAXCALLS, j->n_known, 0, j->req_arg + i, j->req_fn + i};
+        j->req_fn[i] = LM_NONE;
+        tf32 r = eval32(j->fn, j->dv, &L, j->x0[i], j->x1[i]);
+        if (j->req_fn[i] != LM_NONE) {
+            ++*acc;
+        } else {
+            j->z0[i] = r.v;
+            j->z1[i] = r.e;
+        }
+    }
+}
+
+/* One replay pass; returns the number of elements still waiting for libm
+ * answers (their req_fn/req_arg name call number n_known). */
+EXPORT int64_t tfo_eval_f32_pass(int fn, int dv, const float* x0, const float* x1,
+                                 float* z0, float* z1, int64_t n, const float* ans,
+                                 int n_known, float* req_arg, int8_t* req_fn,
+                                 int nthreads) {
+    if (fn < 0 || fn > 3 || n < 0 || n_known < 0 || n_known > MAXCALLS) return -1;
+    job32_t j = {fn, dv, n_known, x0, x1, ans, z0, z1, req_arg, req_fn};
+    return parallel_for(n, nthreads, body32, &j);
+}
+
+EXPORT int tfo_maxcalls(void) { return MAXCALLS; }
+
+/* ---- building blocks, for the known-answer tests of tests/test_oracle_kat.py */
+
+EXPORT void tfo_pexp0_raw64(int dv, double x, double* out) {
+    tf64 r = pexp0_raw64(dv, x); out[0] = r.v; out[1] = r.e;
+}
+EXPORT void tfo_pexpm10_raw64(int dv, double x, double* out) {
+    tf64 r = pexpm10_raw64(dv, x); out[0] = r.v; out[1] = r.e;
+}
+EXPORT void tfo_taylor_exp64(int dv, double y, double* out) {
+    tf64 r = taylor_exp64(dv, y); out[0] = r.v; out[1] = r.e;
+}
+EXPORT void tfo_taylor_expm1_64(int dv, double y, double* out) {
+    tf64 r = taylor_expm1_64(dv, y); out[0] = r.v; out[1] = r.e;
+}
+EXPORT void tfo_decompose_exp64(double x, int64_t* mn, double* y) {
+    decompose_exp64(x, &mn[0], &mn[1], y);
+}
+EXPORT void tfo_decompose_expm1_64(double x, int64_t* n, double* y) {
+    decompose_expm1_64(x, n, y);
+}
+EXPORT void tfo_pexp0_raw32(int dv, float x, float* out) {
+    tf32 r = pexp0_raw32(dv, x); out[0] = r.v; out[1] = r.e;
+}
+EXPORT void tfo_pexpm10_raw32(int dv, float x, float* out) {
+    tf32 r = pexpm10_raw32(dv, x); out[0] = r.v; out[1] = r.e;
+}
+EXPORT void tfo_decompose_exp32(float x, int64_t* mn, float* y) {
+    decompose_exp32(x, &mn[0], &mn[1], y);
+}
+EXPORT void tfo_decompose_expm1_32(float x, int64_t* n, float* y) {
+    decompose_expm1_32(x, n, y);
+}
+/* op = 0 two_sum, 1 fast_two_sum, 2 renorm, 3 t_add, 4 t_add_d, 5 t_mul,
+ * 6 t_mul_d, 7 two_prod (t_mul_d of (a,0) by b is NOT two_prod; see eft.py:131) */
+EXPORT void tfo_eft64(int op, int dv, const double* a, double* out) {
+    tf64 r;
+    switch (op) {
+        case 0: r = two_sum64(a[0], a[1]); break;
+        case 1: r = fast_two_sum64(a[0], a[1]); break;
+        case 2: r = renorm64(mk64(a[0], a[1])); break;
+        case 3: r = t_add64(mk64(a[0], a[1]), mk64(a[2], a[3])); break;
+        case 4: r = t_add_d64(mk64(a[0], a[1]), a[2]); break;
+        case 5: r = t_mul64(dv, mk64(a[0], a[1]), mk64(a[2], a[3])); break;
+        case 6: r = t_mul_d64(dv, mk64(a[0], a[1]), a[2]); break;
+        default: {
+            double v = a[0] * a[1];
+            r = isfinite(v) ? mk64(v, prod_err64(dv, a[0], a[1], v))
+                            : special64(v, N2(a[0], a[1]));
+        }
+    }
+    out[0] = r.v;
+    out[1] = r.e;
+}
