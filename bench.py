@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 twofold hot path (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], the single-GPU config the metric is quoted
+on): one STEP = texpm1 and tlog1p over the cfg-2 float64 twofolds, N = 2^24
+each (x0 = +-s*10^-e, s~U[1,10), e~U{0..300}; tlog1p clamped to
+[-1+2^-52, 1e300]; x1 = x0*u*2^-53).  Inputs are generated on the device by
+the shard-invariant generator (rank r of G owns global elements
+[r*N, (r+1)*N) -- weak scaling, no collective on the hot path).  The 512 MiB
+of inputs per step exceed the 126 MB L2, so no flush is needed.
+
+  value  = elements evaluated per second, whole job (sum over ranks), CUDA
+           events on the launching stream, max over ranks;
+  e2e    = the same metric through the public API with pinned HOST buffers
+           (H2D + kernels + D2H inside the timed region, wall clock);
+  per_function = every (function, width) kernel at its own config (2^24
+           binary64 / 2^26 binary32 elements), same timing rules;
+  roofline = the dominant kernel's algorithmic FP64 op rate vs the measured
+           FP64 FMA-pipe peak of this GPU (tf_fma_peak), plus its HBM rate;
+  cpu_baseline = the CPU oracle (C port of the reference algorithm, all host
+           threads) on a bounded sample of the same workload.
+
+`--impl reference` times that CPU port alone (rank 0) on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+# algorithmic FP ops per element (reference op sequence,
+# config branch mix), the roofline numerators.
+ALG_OPS = {("texp", 64): 123.0, ("texpm1", 64): 111.1, ("tlog", 64): 151.4,
+           ("tlog1p", 64): 142.1, ("texp", 32): 66.0, ("texpm1", 32): 73.9,
+           ("tlog", 32): 106.0, ("tlog1p", 32): 110.0}
+HEADLINE = (("texpm1", "cfg2_texpm1_f64"), ("tlog1p", "cfg2_tlog1p_f64"))
+PER_FN = {
+    ("texp", 64): "cfg1_texp_f64", ("texpm1", 64): "cfg2_texpm1_f64",
+    ("tlog", 64): "cfg3_tlog_f64", ("tlog1p", 64): "cfg2_tlog1p_f64",
+    ("texp", 32): "cfg4_texp_f32", ("texpm1", 32): "cfg4_texpm1_f32",
+    ("tlog", 32): "cfg4_tlog_f32", ("tlog1p", 32): "cfg4_tlog1p_f32",
+}
+N_HEAD = 1 << 24
+N_FN = {64: 1 << 24, 32: 1 << 26}
+SEED = 2024
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class ClockSampler:
+    """NVML sampler of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001 -- clocks are reported as unavailable
+            self.ok = False
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    """CPU port of the reference algorithm (oracle/, kind "port"), all host threads."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_1502_05216_b200 import workloads
+
+    O.build()
+    nt = O.default_threads()
+    sample = args.ref_sample
+    data = {}
+    for fn, cfg in HEADLINE:
+        _, width, dist, _ = workloads.CONFIGS[cfg]
+        data[fn] = workloads.generate(dist, 0, sample, seed=SEED)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        for fn, _ in HEADLINE:
+            O.evaluate(fn, 64, *data[fn], backend="dv", nthreads=nt)
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t)
+    per_step = statistics.median(times)
+    value = 2 * sample / per_step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg-2 generator)",
+        "config": {"workload": "cfg2: texpm1 + tlog1p over float64 twofolds",
+                   "elements_per_function": sample, "sample_of": N_HEAD},
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": nt, "kind": "port",
+                         "sample": f"{sample} elements per function per step "
+                                   f"(bounded sample of the 2^24-element cfg-2 step)"},
+        "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "twofold evals/sec (cfg2: texpm1+tlog1p float64, N=2^24 each)"
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+
+    from paper_1502_05216_b200 import Twofold, _lib, api, workloads
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    L = _lib.ensure_device(local)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    f64 = api(64)
+
+    def gen(dist_name, n, dt, start):
+        x0 = torch.empty(n, dtype=dt, device=dev)
+        x1 = torch.empty(n, dtype=dt, device=dev)
+        _lib.check(L.tf_generate(_lib.DIST_CODES[dist_name], SEED, start, n, x0.data_ptr(),
+                                 x1.data_ptr(), sp), "tf_generate")
+        return x0, x1
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        import torch.distributed as dist
+
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- headline step: texpm1 + tlog1p over cfg-2, N per rank
+    n = args.n
+    start = rank * n
+    ins, outs = {}, {}
+    for fn, cfg in HEADLINE:
+        _, width, dname, _ = workloads.CONFIGS[cfg]
+        ins[fn] = gen(dname, n, torch.float64, start)
+        outs[fn] = (torch.empty(n, dtype=torch.float64, device=dev),
+                    torch.empty(n, dtype=torch.float64, device=dev))
+    torch.cuda.synchronize()
+
+    def step(evs=None):
+        for k, (fn, _) in enumerate(HEADLINE):
+            if evs is not None:
+                evs[k][0].record(stream)
+            a0, a1 = ins[fn]
+            z0, z1 = outs[fn]
+            f64._launch(fn, a0, a1, z0, z1, n, sp)
+            if evs is not None:
+                evs[k][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launch_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in HEADLINE] for _ in range(args.steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for s in range(args.steps):
+            step(launch_ev[s])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_total = max_over_ranks(t0.elapsed_time(t1))
+    ms_step = ms_total / args.steps
+    value = 2 * n * world / (ms_step * 1e-3)
+    kern_ms = {fn: statistics.mean(launch_ev[s][k][0].elapsed_time(launch_ev[s][k][1])
+                                   for s in range(args.steps))
+               for k, (fn, _) in enumerate(HEADLINE)}
+
+    # ---- FP64 / FP32 FMA-pipe peak of this GPU (roofline denominator)
+    peak = {}
+    buf = torch.zeros(4, dtype=torch.float64, device=dev)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    for width in (64, 32):
+        blocks, iters = sms * 8, 4096 if width == 64 else 8192
+        for _ in range(2):
+            _lib.check(L.tf_fma_peak(width, buf.data_ptr(), blocks, iters, sp), "peak")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _lib.check(L.tf_fma_peak(width, buf.data_ptr(), blocks, iters, sp), "peak")
+        e1.record(stream)
+        torch.cuda.synchronize()
+        peak[width] = blocks * 256 * iters * 8 / (e0.elapsed_time(e1) * 1e-3)
+
+    # ---- per-function kernel rates at their configs
+    per_fn = {}
+    if not args.headline_only:
+        for (fn, width), cfg in PER_FN.items():
+            _, _, dname, _ = workloads.CONFIGS[cfg]
+            m = N_FN[width]
+            dt = torch.float64 if width == 64 else torch.float32
+            a0, a1 = gen(dname, m, dt, rank * m)
+            z0, z1 = torch.empty_like(a0), torch.empty_like(a1)
+            lib = api(width)
+            for _ in range(max(3, args.warmup)):
+                lib._launch(fn, a0, a1, z0, z1, m, sp)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(5, min(args.steps, 50))
+            e0.record(stream)
+            for _ in range(reps):
+                lib._launch(fn, a0, a1, z0, z1, m, sp)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = max_over_ranks(e0.elapsed_time(e1) / reps)
+            rate = m * world / (ms * 1e-3)
+            ops = ALG_OPS[(fn, width)] * m / (ms * 1e-3)
+            gbs = (32 if width == 64 else 16) * m / (ms * 1e-3) / 1e9
+            per_fn[f"{fn}_f{width}"] = {
+                "config": cfg, "elements": m, "ms": ms, "elements_per_s": rate,
+                "alg_gops": ops / 1e9, "fma_pipe_frac": ops / peak[width],
+                "hbm_gbs": gbs, "hbm_frac": gbs / _peaks()["hbm_gbs"]}
+            del a0, a1, z0, z1
+
+    # ---- end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        host = {}
+        for fn, _ in HEADLINE:
+            a0, a1 = ins[fn]
+            host[fn] = (a0.cpu().pin_memory(), a1.cpu().pin_memory())
+        # warm the pipeline
+        for fn, _ in HEADLINE:
+            getattr(f64, fn)(Twofold(*host[fn]))
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        barrier()
+        tw = time.perf_counter()
+        for _ in range(e2e_steps):
+            for fn, _ in HEADLINE:
+                z = getattr(f64, fn)(Twofold(*host[fn]))
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks((time.perf_counter() - tw) / e2e_steps)
+        _ = float(z.value[0])  # the result is on the host
+        e2e = {"value": 2 * n * world / t_e2e, "unit": "elements/s",
+               "h2d_bytes_per_step": 2 * 2 * n * 8, "d2h_bytes_per_step": 2 * 2 * n * 8,
+               "ms_per_step": t_e2e * 1e3, "path": "api(64).texpm1/tlog1p on pinned CPU tensors"}
+
+    # ---- parity sample + the one small NCCL reduce of error statistics
+    stats = parity_sample(args, ins, outs, n, rank, world, dev)
+
+    # ---- roofline of the dominant kernel
+    dom = max(kern_ms, key=kern_ms.get)
+    dom_ms = kern_ms[dom]
+    ops = ALG_OPS[(dom, 64)] * n / (dom_ms * 1e-3)
+    gbs = 32 * n / (dom_ms * 1e-3) / 1e9
+    roof = {"bound": "fp64", "kernel": f"k_eval<double,{dom}>",
+            "achieved": ops / 1e12, "peak": peak[64] / 1e12, "unit": "TFLOP/s",
+            "frac": ops / peak[64], "traffic": args.traffic,
+            "ops_per_element": ALG_OPS[(dom, 64)], "elements_per_launch": n,
+            "launch_ms": dom_ms, "peak_source": "measured tf_fma_peak DFMA rate (this GPU, this run)",
+            "hbm_achieved_gbs": gbs, "hbm_peak_gbs": _peaks()["hbm_gbs"],
+            "hbm_frac": gbs / _peaks()["hbm_gbs"]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded shard-invariant cfg-2 generator, on device)",
+            "config": {"workload": "cfg2: texpm1 + tlog1p over float64 twofolds",
+                       "elements_per_function_per_gpu": n, "global_elements_per_step": 2 * n * world,
+                       "parallelism": f"contiguous shards x{world}, no collective on the hot path",
+                       "l2": "inputs 512 MiB/step > 126 MB L2 (no flush needed)"},
+            "gpu_launches": len(HEADLINE) * args.steps,
+            "kernel_ms": kern_ms,
+            "clocks": clk.summary(),
+            "roofline": roof,
+            "fma_peak_tops": {"f64": peak[64] / 1e12, "f32": peak[32] / 1e12},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "per_function": per_fn,
+            "parity_sample": stats,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def parity_sample(args, ins, outs, n, rank, world, dev):
+    """Check a seeded sample of each rank's outputs against the CPU oracle, then
+    sum the per-rank counters with one tiny NCCL all-reduce."""
+    import torch
+
+    from oracle import oracle as O
+    from oracle.compare import compare
+
+    m = min(args.parity_sample, n)
+    keys = ("n", "z0_mismatch", "z0_gt1ulp", "tol_violations", "class_mismatch")
+    vec = []
+    for fn, _ in HEADLINE:
+        x0 = ins[fn][0][:m].cpu().numpy()
+        x1 = ins[fn][1][:m].cpu().numpy()
+        z0 = outs[fn][0][:m].cpu().numpy()
+        z1 = outs[fn][1][:m].cpu().numpy()
+        r0, r1 = O.evaluate(fn, 64, x0, x1, backend="dv")
+        r = compare(z0, z1, r0, r1, 64)
+        vec.extend(r[k] for k in keys)
+    t = torch.tensor(vec, dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    v = t.cpu().tolist()
+    out = {}
+    for i, (fn, _) in enumerate(HEADLINE):
+        out[fn] = {k: int(v[i * len(keys) + j]) for j, k in enumerate(keys)}
+    out["oracle"] = "CPU port, dv backend (bit-exact vs reference goldens)"
+    return out
+
+
+def cpu_baseline(args):
+    from oracle import oracle as O
+    from paper_1502_05216_b200 import workloads
+
+    O.build()
+    nt = O.default_threads()
+    sample = args.ref_sample
+    data = {fn: workloads.generate(workloads.CONFIGS[cfg][2], 0, sample, seed=SEED)
+            for fn, cfg in HEADLINE}
+    for fn, _ in HEADLINE:
+        O.evaluate(fn, 64, *data[fn], backend="dv", nthreads=nt)
+    t = time.perf_counter()
+    for fn, _ in HEADLINE:
+        O.evaluate(fn, 64, *data[fn], backend="dv", nthreads=nt)
+    dt = time.perf_counter() - t
+    return {"value": 2 * sample / dt, "unit": "elements/s", "cores": nt, "kind": "port",
+            "sample": f"{sample} elements each of texpm1 and tlog1p (cfg-2 generator), "
+                      f"C port of the reference algorithm (oracle/), {nt} threads"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--n", type=int, default=N_HEAD, help="elements per function per GPU")
+    ap.add_argument("--ref-sample", type=int, default=1 << 21)
+    ap.add_argument("--parity-sample", type=int, default=1 << 16)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per launch of the dominant kernel (profiles/)")
+    ap.add_argument("--headline-only", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,117 @@
+/*
+ * twofold_b200.h -- C ABI of libtwofold_b200.so (B200 / sm_100a).
+ *
+ * Batch twofold elementary functions over structure-of-arrays operands:
+ * element i is the twofold x0[i] + x1[i]; the result is z0[i] + z1[i] with
+ * z0[i] the correctly rounded value of the standard function at x0[i] and
+ * z1[i] the error part of the reference algorithm.
+ *
+ * Each entry point replaces, for a whole array, the per-element reference
+ * call of the Python package (/root/reference/pkg/src/twofold):
+ *   tf_texp_f64   <- ExpLog(64).texp(x)    explog.py:265-275
+ *   tf_texpm1_f64 <- ExpLog(64).texpm1(x)  explog.py:299-310
+ *   tf_tlog_f64   <- ExpLog(64).tlog(y)    explog.py:394-399
+ *   tf_tlog1p_f64 <- ExpLog(64).tlog1p(y)  explog.py:464-467
+ *   tf_*_f32      <- the same methods of ExpLog(32) (binary32 lane)
+ * (api(width) / get_function(name, width), explog.py:483-499, resolve to them).
+ * The paper's scalar C form z0 = texp(x0, x1, &z1)
+ * is the n == 1 case.
+ *
+ * Conventions
+ *   - x0, x1, z0, z1 are DEVICE pointers of the current device (tf_init),
+ *     same element type; z may alias x only element-for-element (in place).
+ *   - 16-byte aligned pointers take the vectorised path; any element-aligned
+ *     pointer is accepted.
+ *   - stream is a cudaStream_t (NULL = legacy default stream); every call is
+ *     asynchronous and thread-safe.
+ *   - return 0 on success, negative TF_ERR_* on error (message in
+ *     tf_last_error(), thread-local).  Numerics never fail: non-finite inputs
+ *     produce the reference's IEEE special results.
+ */
+#ifndef TWOFOLD_B200_H
+#define TWOFOLD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(_WIN32)
+#define TF_API __declspec(dllexport)
+#else
+#define TF_API __attribute__((visibility("default")))
+#endif
+
+#define TF_ABI_VERSION 1
+
+/* status codes */
+#define TF_OK 0
+#define TF_ERR_ARG (-1)  /* invalid argument (the reference raises ValueError) */
+#define TF_ERR_CUDA (-2) /* CUDA runtime / launch error */
+
+/* function codes for tf_eval (FUNCTION_NAMES subset TWOFOLD_ARG, explog.py:44-53) */
+#define TF_FN_TEXP 0
+#define TF_FN_TEXPM1 1
+#define TF_FN_TLOG 2
+#define TF_FN_TLOG1P 3
+
+/* tf_eval flags */
+#define TF_FLAG_FORCE_EXACT 1 /* route every element through the exact path (testing) */
+#define TF_FLAG_COUNT_EXACT 2 /* count exact-path elements (tf_exact_count) */
+
+/* synthetic distributions for tf_generate (BASELINE.json configs; workloads.py) */
+#define TF_DIST_EXP64 0
+#define TF_DIST_POW10 1
+#define TF_DIST_POW10C 2
+#define TF_DIST_LOG64 3
+#define TF_DIST_EXP32 4
+#define TF_DIST_LOG32 5
+#define TF_DIST_EXP64S 6
+#define TF_DIST_LOGU64S 7
+#define TF_DIST_COUNT 8
+
+TF_API int tf_version(void);
+TF_API const char* tf_last_error(void);
+
+/* Select the device (device < 0: keep the current one) and upload constants. */
+TF_API int tf_init(int device);
+
+TF_API int tf_texp_f64(const double* x0, const double* x1, double* z0, double* z1, int64_t n, void* stream);
+TF_API int tf_texpm1_f64(const double* x0, const double* x1, double* z0, double* z1, int64_t n, void* stream);
+TF_API int tf_tlog_f64(const double* x0, const double* x1, double* z0, double* z1, int64_t n, void* stream);
+TF_API int tf_tlog1p_f64(const double* x0, const double* x1, double* z0, double* z1, int64_t n, void* stream);
+TF_API int tf_texp_f32(const float* x0, const float* x1, float* z0, float* z1, int64_t n, void* stream);
+TF_API int tf_texpm1_f32(const float* x0, const float* x1, float* z0, float* z1, int64_t n, void* stream);
+TF_API int tf_tlog_f32(const float* x0, const float* x1, float* z0, float* z1, int64_t n, void* stream);
+TF_API int tf_tlog1p_f32(const float* x0, const float* x1, float* z0, float* z1, int64_t n, void* stream);
+
+/* Generic dispatcher: fn = TF_FN_*, width = 32 or 64, flags = TF_FLAG_*. */
+TF_API int tf_eval(int fn, int width, const void* x0, const void* x1, void* z0, void* z1,
+                   int64_t n, void* stream, int flags);
+
+/* Shard-invariant synthetic inputs: elements [start, start+n) of distribution
+ * `dist` for `seed` (bit-identical to workloads.generate). */
+TF_API int tf_generate(int dist, uint64_t seed, int64_t start, int64_t n, void* x0, void* x1,
+                       void* stream);
+
+/* Accumulate parity statistics of (z0, z1) against (r0, r1) into the 6
+ * counters at stats_dev (device memory, caller-zeroed):
+ * [elements, z0 bit mismatches, z0 mismatches > 1 ulp, |dz| > max(rel|r|, abs_guard),
+ *  non-finite class mismatches, z1 bit mismatches]. */
+TF_API int tf_compare(int width, const void* z0, const void* z1, const void* r0, const void* r1,
+                      int64_t n, double rel, double abs_guard, unsigned long long* stats_dev,
+                      void* stream);
+
+/* FMA-pipe calibration: `blocks` CTAs x 256 threads x `iters` x 8 dependent
+ * FMAs of the given width (2048 ops per thread per iteration block). */
+TF_API int tf_fma_peak(int width, void* out_dev, int blocks, int iters, void* stream);
+
+/* Elements routed through the exact path since the last reset (needs
+ * TF_FLAG_COUNT_EXACT on the counted calls); synchronous. */
+TF_API int tf_exact_count(unsigned long long* out, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TWOFOLD_B200_H */

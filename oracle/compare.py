@@ -1,0 +1,78 @@
+"""Parity comparator (TEST INFRASTRUCTURE ONLY; used by tests/, smoke() and bench).
+
+Implements the north-star acceptance rule (BASELINE.json north_star; SURVEY.md
+section 8(d) "Parity tolerances"):
+  * z0 bitwise vs the reference, mismatches counted with an ulp histogram;
+  * |(z0+z1) - (r0+r1)| <= max(rel * |r0+r1|, guard) with
+      binary64: rel = 2^-95, guard = 2 * 2^-1074
+      binary32: rel = 2^-42, guard = 2 * 2^-149
+    (the absolute guard is the stated edge tolerance at exp's underflow and
+    log's zero/one, where the reference's own error part is subnormal);
+  * non-finite results: same class (NaN <-> NaN, +-inf same sign).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+TOL = {64: (2.0 ** -95, 2.0 * 2.0 ** -1074), 32: (2.0 ** -42, 2.0 * 2.0 ** -149)}
+
+
+def _ordered(a: np.ndarray) -> np.ndarray:
+    """Map floats to integers whose difference is the ulp distance."""
+    if a.dtype == np.float64:
+        b = a.view(np.int64).astype(np.int64)
+        mag = b & np.int64(0x7FFFFFFFFFFFFFFF)
+    else:
+        b = a.view(np.int32).astype(np.int64)
+        mag = b & np.int64(0x7FFFFFFF)
+    return np.where(b < 0, -mag, mag)
+
+
+def ulp_distance(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    d = np.abs(_ordered(a) - _ordered(b))
+    return np.where(np.isnan(a) | np.isnan(b), np.where(np.isnan(a) & np.isnan(b), 0, -1), d)
+
+
+def same_bits(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    u = np.uint64 if a.dtype == np.float64 else np.uint32
+    return (a.view(u) == b.view(u)) | (np.isnan(a) & np.isnan(b))
+
+
+def compare(z0, z1, r0, r1, width: int) -> dict:
+    z0, z1, r0, r1 = (np.asarray(v) for v in (z0, z1, r0, r1))
+    rel, guard = TOL[width]
+    n = z0.size
+    s0 = same_bits(z0, r0)
+    s1 = same_bits(z1, r1)
+    ud = ulp_distance(z0, r0)
+    finite = np.isfinite(z0) & np.isfinite(z1) & np.isfinite(r0) & np.isfinite(r1)
+    with np.errstate(all="ignore"):
+        a0, a1, b0, b1 = (v.astype(np.float64) for v in (z0, z1, r0, r1))
+        d = (a0 - b0) + (a1 - b1)
+        tol = np.maximum(rel * np.abs(b0 + b1), guard)
+        viol = finite & ~(np.abs(d) <= tol)
+        # non-finite anywhere: class equality per field
+        cls0 = s0 | (z0 == r0)
+        cls1 = (np.isnan(z1) & np.isnan(r1)) | (z1 == r1) | (np.isfinite(z1) & np.isfinite(r1))
+    cls_bad = ~finite & ~(cls0 & cls1)
+    mism = ~s0
+    hist = {}
+    if mism.any():
+        vals, cnts = np.unique(ud[mism], return_counts=True)
+        hist = {int(v): int(c) for v, c in zip(vals, cnts)}
+    return {
+        "n": int(n),
+        "z0_mismatch": int(mism.sum()),
+        "z0_ulp_hist": hist,
+        "z0_gt1ulp": int((mism & ((ud > 1) | (ud < 0))).sum()),
+        "tol_violations": int(viol.sum()),
+        "tol_violations_given_z0_match": int((viol & s0).sum()),
+        "class_mismatch": int(cls_bad.sum()),
+        "z1_bit_mismatch": int((~s1).sum()),
+        "z1_bit_mismatch_given_z0_match": int((~s1 & s0).sum()),
+        "worst_rel_log2": float(np.log2(np.max(np.where(finite & (np.abs(b0 + b1) > 0),
+                                                        np.abs(d) / np.abs(b0 + b1), 0.0))
+                                        + 1e-300)),
+        "bad_idx": np.nonzero(viol | cls_bad)[0][:20].tolist(),
+    }

@@ -34,6 +34,13 @@
 
 #define EXPORT __attribute__((visibility("default")))
 
+static const double TF64_E[] = {TF64_E_INIT};
+static const double TF64_C[] = {TF64_C_INIT};
+static const double TF64_CM1[] = {TF64_CM1_INIT};
+static const float TF32_E[] = {TF32_E_INIT};
+static const float TF32_C[] = {TF32_C_INIT};
+static const float TF32_CM1[] = {TF32_CM1_INIT};
+
 enum { FN_TEXP = 0, FN_TEXPM1 = 1, FN_TLOG = 2, FN_TLOG1P = 3 };
 enum { LM_EXP = 0, LM_EXPM1 = 1, LM_LOG = 2, LM_LOG1P = 3, LM_NONE = -1 };
 #define MAXCALLS 4

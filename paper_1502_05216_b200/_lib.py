@@ -1,0 +1,101 @@
+"""ctypes binding of libtwofold_b200.so (the C ABI declared in include/twofold_b200.h).
+
+The product path has no fallback: if the library is missing, or no CUDA device
+is visible, every compute call raises RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libtwofold_b200.so")
+CSRC = os.path.join(HERE, "csrc")
+
+TF_OK, TF_ERR_ARG, TF_ERR_CUDA = 0, -1, -2
+FN_CODES = {"texp": 0, "texpm1": 1, "tlog": 2, "tlog1p": 3}
+FLAG_FORCE_EXACT = 1
+FLAG_COUNT_EXACT = 2
+DIST_CODES = {"exp64": 0, "pow10_64": 1, "pow10c_64": 2, "log64": 3, "exp32": 4, "log32": 5,
+              "exp64s": 6, "logu64s": 7}
+
+# every symbol include/twofold_b200.h declares (checked by tests/test_abi.py)
+EXPORTS = ("tf_version", "tf_last_error", "tf_init", "tf_texp_f64", "tf_texpm1_f64",
+           "tf_tlog_f64", "tf_tlog1p_f64", "tf_texp_f32", "tf_texpm1_f32", "tf_tlog_f32",
+           "tf_tlog1p_f32", "tf_eval", "tf_generate", "tf_compare", "tf_fma_peak",
+           "tf_exact_count")
+
+_lib = None
+_lock = threading.Lock()
+_inited: set[int] = set()
+
+
+def build(force: bool = False) -> str:
+    """Compile the CUDA library in-tree for sm_100a (nvcc; see csrc/Makefile)."""
+    args = ["make", "-s", "-C", CSRC]
+    if force:
+        args.insert(1, "-B")
+    subprocess.run(args, check=True)
+    return LIB_PATH
+
+
+def load() -> ctypes.CDLL:
+    """Load the shared library (no CUDA context is created here)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"libtwofold_b200.so not found at {LIB_PATH}; run "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (or make -C "
+                f"{CSRC}) first -- there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        L.tf_version.restype = i32
+        L.tf_last_error.restype = ctypes.c_char_p
+        L.tf_init.argtypes = [i32]
+        L.tf_init.restype = i32
+        for fn in ("texp", "texpm1", "tlog", "tlog1p"):
+            for w in ("f64", "f32"):
+                f = getattr(L, f"tf_{fn}_{w}")
+                f.argtypes = [vp, vp, vp, vp, i64, vp]
+                f.restype = i32
+        L.tf_eval.argtypes = [i32, i32, vp, vp, vp, vp, i64, vp, i32]
+        L.tf_eval.restype = i32
+        L.tf_generate.argtypes = [i32, ctypes.c_uint64, i64, i64, vp, vp, vp]
+        L.tf_generate.restype = i32
+        L.tf_compare.argtypes = [i32, vp, vp, vp, vp, i64, ctypes.c_double, ctypes.c_double,
+                                 vp, vp]
+        L.tf_compare.restype = i32
+        L.tf_fma_peak.argtypes = [i32, vp, i32, i32, vp]
+        L.tf_fma_peak.restype = i32
+        L.tf_exact_count.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), i32]
+        L.tf_exact_count.restype = i32
+        _lib = L
+        return L
+
+
+def check(rc: int, what: str) -> None:
+    if rc != TF_OK:
+        msg = load().tf_last_error().decode(errors="replace")
+        if rc == TF_ERR_ARG:
+            raise ValueError(f"{what}: {msg}")
+        raise RuntimeError(f"{what}: {msg}")
+
+
+def ensure_device(device_index: int) -> ctypes.CDLL:
+    L = load()
+    if device_index not in _inited:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("no CUDA device visible: the twofold kernels need a B200 "
+                               "(sm_100a); there is no CPU fallback")
+        with torch.cuda.device(device_index):
+            check(L.tf_init(-1), "tf_init")
+        _inited.add(device_index)
+    return L

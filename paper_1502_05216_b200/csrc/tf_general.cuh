@@ -1,0 +1,415 @@
+// tf_general.cuh -- the exact ("rare") path: a complete device restatement of
+// the reference texp/texpm1/tlog/tlog1p (pkg/src/twofold/explog.py:265-467,
+// expcore.py:35-147) with every _special check, for ANY input: NaN/inf,
+// out-of-domain, subnormal, under/overflowing intermediates, non-coupled
+// twofolds, second Newton iterations.  The fast kernels divert every element
+// outside their admission band to this path (per-warp queue, tf_kernels.cu).
+//
+// The platform-libm values of the reference (glibc for binary64, numpy float32
+// for binary32; _fp.py:191-245) are replaced by correctly rounded values
+// computed from the method's own twofold cores:
+//   exp/expm1(x)   = RN(v0 + v1) of pexp0/pexpm10 (scaled table near underflow)
+//   log/log1p(y)   = RN(r0 + r1) of the reference log core of (y, 0)
+// Newton seeds use CUDA log/log1p (<= 1 ulp; the Newton step absorbs it).
+#pragma once
+#include "tf_common.cuh"
+
+namespace tf {
+
+// ------------------------------------------------------------- tables (gmem)
+__device__ const double g_E64[] = {TF64_E_INIT};
+__device__ const double g_C64[] = {TF64_C_INIT};
+__device__ const double g_CM164[] = {TF64_CM1_INIT};
+__device__ const double g_ESC64[] = {TF64_ESC_INIT};
+__device__ const float g_E32[] = {TF32_E_INIT};
+__device__ const float g_C32[] = {TF32_C_INIT};
+__device__ const float g_CM132[] = {TF32_CM1_INIT};
+__device__ const float g_ESC32[] = {TF32_ESC_INIT};
+
+template <class T> struct GT;
+template <> struct GT<double> {
+  TF_DEV static TF<double> E(int m) { const double* p = g_E64 + 2 * (m - TF64_E_LO); return mk(__ldg(p), __ldg(p + 1)); }
+  TF_DEV static TF<double> C(int n) { const double* p = g_C64 + 2 * (n - TF64_C_LO); return mk(__ldg(p), __ldg(p + 1)); }
+  TF_DEV static TF<double> CM1(int n) { const double* p = g_CM164 + 2 * (n - TF64_CM1_LO); return mk(__ldg(p), __ldg(p + 1)); }
+};
+template <> struct GT<float> {
+  TF_DEV static TF<float> E(int m) { const float* p = g_E32 + 2 * (m - TF32_E_LO); return mk(__ldg(p), __ldg(p + 1)); }
+  TF_DEV static TF<float> C(int n) { const float* p = g_C32 + 2 * (n - TF32_C_LO); return mk(__ldg(p), __ldg(p + 1)); }
+  TF_DEV static TF<float> CM1(int n) { const float* p = g_CM132 + 2 * (n - TF32_CM1_LO); return mk(__ldg(p), __ldg(p + 1)); }
+};
+
+// 2^k as an exact double for k in [-1074, 1023]
+TF_DEV double p2d(int k) {
+  if (k >= -1022) return __longlong_as_double((long long)(k + 1023) << 52);
+  return __longlong_as_double(1ll << (k + 1074));
+}
+TF_DEV float p2f(int k) {  // k in [-149, 127]
+  if (k >= -126) return __int_as_float((k + 127) << 23);
+  return __int_as_float(1 << (k + 149));
+}
+
+// Python math.frexp for finite nonzero x: x = f * 2^n, 0.5 <= |f| < 1.
+TF_DEV double frexp_d(double x, int* n) { return frexp(x, n); }
+// Python math.ldexp(x, k) = RN(x * 2^k); single rounding via one exact power
+TF_DEV double ldexp_d(double x, int k) {
+  if (k > 1023) return mul(mul(x, p2d(1023)), p2d(k - 1023));  // exact scaling up
+  if (k < -1074) return mul(mul(x, p2d(-1074)), p2d(k + 1074));
+  return mul(x, p2d(k));
+}
+
+// ------------------------------------------------------------ exp cores
+// decompose_exp (expcore.py:35-50).  Python round() is ties-to-even == rint.
+template <class T> TF_DEV void decompose_exp(T x, int* m, int* n, T* y) {
+  double xd = (double)x;
+  double M = rint(mul(xd, 32.0));
+  *y = (T)sub(xd, mul(M, 0.03125));     // exact
+  int Mi = (int)M;
+  int a = Mi < 0 ? -Mi : Mi;
+  int hi = a >> P<T>::SPAN_SHIFT, lo = a & ((1 << P<T>::SPAN_SHIFT) - 1);
+  *m = Mi < 0 ? -hi : hi;
+  *n = Mi < 0 ? -lo : lo;
+}
+// decompose_expm1 (expcore.py:53-58)
+template <class T> TF_DEV void decompose_expm1(T x, int* n, T* y) {
+  double xd = (double)x;
+  double M = rint(mul(xd, 128.0));
+  *y = (T)sub(xd, mul(M, 0.0078125));
+  *n = (int)M;
+}
+
+// _seed + taylor_exp / taylor_expm1 (expcore.py:82-116)
+TF_DEV TF<double> taylor_exp_c(double y) {
+  double s = add(y, 12.0);
+  s = add(mul(s, y), 132.0);
+  s = add(mul(s, y), 1320.0);
+  TF<double> t = mk(s, 0.0);
+  const double c[9] = {11880.0, 95040.0, 665280.0, 3991680.0, 19958400.0,
+                       79833600.0, 239500800.0, 479001600.0, 479001600.0};
+#pragma unroll
+  for (int k = 0; k < 9; ++k) t = t_add_d_c(t_mul_d_c(t, y), c[k]);
+  return t;
+}
+TF_DEV TF<float> taylor_exp_c(float y) {
+  float s = add(y, 6.0f);
+  s = add(mul(s, y), 30.0f);
+  TF<float> t = mk(s, 0.0f);
+  const float c[4] = {120.f, 360.f, 720.f, 720.f};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) t = t_add_d_c(t_mul_d_c(t, y), c[k]);
+  return t;
+}
+TF_DEV TF<double> taylor_expm1_c(double y) {
+  double s = add(y, 10.0);
+  s = add(mul(s, y), 90.0);
+  s = add(mul(s, y), 720.0);
+  TF<double> t = mk(s, 0.0);
+  const double c[6] = {5040.0, 30240.0, 151200.0, 604800.0, 1814400.0, 3628800.0};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) t = t_add_d_c(t_mul_d_c(t, y), c[k]);
+  t = t_mul_d_c(t, y);
+  return t_mul_c(t, mk(P<double>::INVF_V, P<double>::INVF_E));
+}
+TF_DEV TF<float> taylor_expm1_c(float y) {
+  float s = add(y, 5.0f);
+  s = add(mul(s, y), 20.0f);
+  TF<float> t = mk(s, 0.0f);
+  const float c[2] = {60.f, 120.f};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) t = t_add_d_c(t_mul_d_c(t, y), c[k]);
+  t = t_mul_d_c(t, y);
+  return t_mul_c(t, mk(P<float>::INVF_V, P<float>::INVF_E));
+}
+
+// pexp0_raw (expcore.py:120-133)
+template <class T> TF_DEV TF<T> pexp0_raw_c(T x) {
+  if (is_nan(x)) return mk(Lim<T>::qnan(), Lim<T>::qnan());
+  if (x < P<T>::LO) return mk(T(0), T(0));
+  if (x > P<T>::HI) return mk(Lim<T>::inf(), Lim<T>::inf());
+  int m, n;
+  T y;
+  decompose_exp(x, &m, &n, &y);
+  TF<T> t = taylor_exp_c(y);
+  return t_mul_c(GT<T>::E(m), t_mul_c(GT<T>::C(n), t));
+}
+
+// pexpm10_raw (expcore.py:138-147)
+template <class T> TF_DEV TF<T> pexpm10_raw_c(T x) {
+  if (is_nan(x)) return mk(Lim<T>::qnan(), Lim<T>::qnan());
+  if (abits(x) <= abits(P<T>::LN2_V)) {
+    int n;
+    T y;
+    decompose_expm1(x, &n, &y);
+    TF<T> c = GT<T>::CM1(n);
+    TF<T> t = taylor_expm1_c(y);
+    return t_add_c(t_mul_c(c, t), t_add_c(c, t));
+  }
+  return t_add_d_c(pexp0_raw_c(x), T(-1));
+}
+
+// ------------------------------------------- correctly rounded libm stand-ins
+// exp(x) < 2^-1075 (rounds to 0) iff x <= EXP_UNF; exp(x) rounds to inf iff
+// x >= EXP_OVF (thresholds computed with mpmath, see tests/test_tables.py).
+constexpr double EXP_UNF = -0x1.74910d52d3052p+9;   // < ln(2^-1075)
+constexpr double EXP_OVF = 0x1.62e42fefa39fp+9;     // > ln(DBL_MAX + ulp/2)
+
+// RN(h + l) onto the binary64 grid, where (h, l) is a twofold scaled by 2^128
+// whose true value may lie in the subnormal range after unscaling.
+TF_DEV double round_unscale128(double h, double l) {
+  double s = add(h, l);
+  if (fabs(s) >= 0x1p-894) return mul(s, 0x1p-128);  // normal after scaling: exact
+  const double q = 0x1p-946;                           // 2^-1074 * 2^128
+  const double C = 0x1.8p-894;                         // 1.5 * 2^52 * q
+  double t = sub(add(h, C), C);                        // h rounded to multiples of q
+  double r = add(sub(h, t), l);                        // h - t exact
+  if (r > 0.5 * q) t = add(t, q);
+  else if (r < -0.5 * q) t = sub(t, q);
+  else if (fabs(r) == 0.5 * q) {                       // tie: to even multiple
+    long long k = (long long)(t * 0x1p946);
+    if (k & 1) t = r > 0 ? add(t, q) : sub(t, q);
+  }
+  return mul(t, 0x1p-128);                             // exact
+}
+
+TF_DEV double exp_cr(double x) {
+  if (is_nan(x)) return x;
+  if (x >= EXP_OVF) return Lim<double>::inf();
+  if (x <= EXP_UNF) return 0.0;
+  int m, n;
+  double y;
+  decompose_exp(x, &m, &n, &y);
+  TF<double> ct = t_mul_u(GT<double>::C(n), taylor_exp_c(y));
+  if (m <= TF64_ESC_LO + TF64_ESC_COUNT - 1) {
+    const double* p = g_ESC64 + 2 * (m - TF64_ESC_LO);
+    TF<double> v = t_mul_u(mk(__ldg(p), __ldg(p + 1)), ct);
+    return round_unscale128(v.v, v.e);
+  }
+  TF<double> e = GT<double>::E(m);
+  if (m > 170) {  // keep the product finite; rescaling is exact or overflows
+    TF<double> v = t_mul_u(mk(mul(e.v, 0x1p-64), mul(e.e, 0x1p-64)), ct);
+    return mul(add(v.v, v.e), 0x1p64);
+  }
+  TF<double> v = t_mul_u(e, ct);
+  return add(v.v, v.e);
+}
+
+TF_DEV double expm1_cr(double x) {
+  if (is_nan(x) || x == 0.0) return x;
+  if (abits(x) < 0x3c90000000000000ull) return x;   // |x| < 2^-54
+  if (x >= EXP_OVF) return Lim<double>::inf();
+  if (x <= -38.0) return -1.0;
+  if (x > 709.0) return exp_cr(x);                  // 1 << ulp(e^x)
+  TF<double> w = pexpm10_raw_c(x);
+  return add(w.v, w.e);
+}
+
+// RN to binary32 of a binary64 twofold (h + l), immune to double rounding.
+TF_DEV float rn32_twofold(double h, double l) {
+  float f = __double2float_rn(h);
+  if (!is_finite(f) || l == 0.0) return f;
+  double fd = (double)f;
+  double r = add(sub(h, fd), l);                     // h - fd exact
+  if (r == 0.0) return f;
+  float nb = nextafterf(f, r > 0 ? Lim<float>::inf() : -Lim<float>::inf());
+  if (!is_finite(nb)) return f;
+  double half = 0.5 * sub((double)nb, fd);           // exact
+  if (fabs(r) > fabs(half)) return nb;
+  if (fabs(r) == fabs(half) && (ubits(f) & 1u)) return nb;
+  return f;
+}
+
+TF_DEV float exp_cr(float x) {
+  if (is_nan(x)) return x;
+  if (x > 89.0f) return Lim<float>::inf();
+  if (x < -104.0f) return 0.0f;
+  TF<double> v = pexp0_raw_c((double)x);             // normal doubles throughout
+  return rn32_twofold(v.v, v.e);
+}
+
+TF_DEV float expm1_cr(float x) {
+  if (is_nan(x) || x == 0.0f) return x;
+  if (x > 89.0f) return Lim<float>::inf();
+  if (x < -18.0f) return -1.0f;
+  TF<double> w = pexpm10_raw_c((double)x);
+  return rn32_twofold(w.v, w.e);
+}
+
+// ------------------------------------------------------------ log cores
+// Newton seeds: the reference calls libm log / log1p (explog.py:347-349,427);
+// CUDA's are within 1 ulp and the Newton step absorbs the difference.
+TF_DEV double seed_log1p(double x) { return log1p(x); }
+TF_DEV float seed_log1p(float x) { return log1pf(x); }
+
+// The Newton tolerance test is plain binary64 Python arithmetic in both lanes
+// (explog.py:351, 429).
+template <class T> TF_DEV bool newton_again(T r1, T r0) {
+  return fabs((double)r1) > 0x1p-20 * fabs((double)r0) + 0x1p-20;
+}
+
+// _newton_log_z (explog.py:320-336)
+template <class T> TF_DEV T newton_log_z_c(T z0, T z1, T r0) {
+  TF<T> s = pexpm10_raw_c(T(-r0));
+  T zm1 = sub(z0, T(1));
+  TF<T> u;
+  if (z1 == T(0)) {
+    u = t_add_d_c(t_mul_d_c(s, z0), zm1);
+  } else {
+    TF<T> w = fast_two_sum_c(zm1, z1);
+    u = t_add_c(t_mul_c(mk(z0, z1), s), w);
+  }
+  return add(u.v, u.e);
+}
+
+// _log_core (explog.py:338-358)
+template <class T> TF_DEV TF<T> log_core_c(T y0, T y1) {
+  T z0, z1;
+  int n = 0;
+  if (y0 < T(0.5) || y0 > T(2)) {
+    if (is_finite(y0) && y0 != T(0)) z0 = (T)frexp_d((double)y0, &n);
+    else z0 = y0;
+    z1 = (y1 != T(0)) ? (T)ldexp_d((double)y1, -n) : T(0);
+  } else {
+    z0 = y0;
+    z1 = y1;
+  }
+  // explog.py:346-349 seeds with log(z0) when y1 == z1 == 0, else with
+  // log1p((z0 - 1) + z1); z0 - 1 is exact, so one log1p covers both (the seed
+  // only needs to be within an ulp: the Newton step absorbs it).
+  T r0 = seed_log1p(add(sub(z0, T(1)), z1));
+  T r1 = newton_log_z_c(z0, z1, r0);
+  if (newton_again(r1, r0)) {
+    r0 = add(r0, r1);
+    r1 = newton_log_z_c(z0, z1, r0);
+  }
+  if (n == 0) return mk(r0, r1);
+  TF<T> nl = t_mul_d_c(mk(P<T>::LN2_V, P<T>::LN2_E), (T)n);
+  return t_add_c(mk(r0, r1), nl);
+}
+
+// _newton_log1p_in_band (explog.py:410-424)
+template <class T> TF_DEV T newton_log1p_c(T y0, T y1, T x0) {
+  TF<T> s = pexpm10_raw_c(T(-x0));
+  TF<T> u;
+  if (y1 == T(0)) {
+    TF<T> w = fast_two_sum_c(T(1), y0);
+    u = t_add_d_c(t_mul_c(w, s), y0);
+  } else {
+    TF<T> ys = t_mul_c(mk(y0, y1), s);
+    u = t_add_c(t_add_c(ys, mk(y0, y1)), s);
+  }
+  return add(u.v, u.e);
+}
+
+// _log1p_core (explog.py:426-432)
+template <class T> TF_DEV TF<T> log1p_core_c(T y0, T y1) {
+  T x0 = seed_log1p(y0);
+  T x1 = newton_log1p_c(y0, y1, x0);
+  if (newton_again(x1, x0)) {
+    x0 = add(x0, x1);
+    x1 = newton_log1p_c(y0, y1, x0);
+  }
+  return mk(x0, x1);
+}
+
+TF_DEV double log_cr(double y) {
+  if (is_nan(y) || y < 0.0) return Lim<double>::qnan();
+  if (y == 0.0) return -Lim<double>::inf();
+  if (is_inf(y)) return y;
+  TF<double> c = log_core_c(y, 0.0);
+  return add(c.v, c.e);
+}
+
+TF_DEV double log1p_cr(double y) {
+  if (is_nan(y) || y < -1.0) return Lim<double>::qnan();
+  if (y == -1.0) return -Lim<double>::inf();
+  if (is_inf(y)) return y;
+  if (abits(y) < 0x3c90000000000000ull) return y;   // |y| < 2^-54 (incl. +-0)
+  TF<double> c;
+  if (y < -0.5 || y > 1.0) {
+    TF<double> w = renorm_c(t_add_d_c(mk(y, 0.0), 1.0));
+    c = log_core_c(w.v, w.e);
+  } else {
+    c = log1p_core_c(y, 0.0);
+  }
+  return add(c.v, c.e);
+}
+
+TF_DEV float log_cr(float y) {
+  if (is_nan(y) || y < 0.0f) return Lim<float>::qnan();
+  if (y == 0.0f) return -Lim<float>::inf();
+  if (is_inf(y)) return y;
+  TF<double> c = log_core_c((double)y, 0.0);
+  return rn32_twofold(c.v, c.e);
+}
+
+TF_DEV float log1p_cr(float y) {
+  if (is_nan(y) || y < -1.0f) return Lim<float>::qnan();
+  if (y == -1.0f) return -Lim<float>::inf();
+  if (is_inf(y)) return y;
+  if (y == 0.0f) return y;
+  double yd = (double)y;
+  TF<double> c;
+  if (yd < -0.5 || yd > 1.0) {
+    TF<double> w = renorm_c(t_add_d_c(mk(yd, 0.0), 1.0));   // exact: 1 + y
+    c = log_core_c(w.v, w.e);
+  } else {
+    c = log1p_core_c(yd, 0.0);
+  }
+  return rn32_twofold(c.v, c.e);
+}
+
+// ------------------------------------------------------ public functions
+// ExpLog.texp (explog.py:265-275)
+template <class T> TF_DEV TF<T> texp_gen(T x0, T x1) {
+  TF<T> v = pexp0_raw_c(x0);
+  T z0 = exp_cr(x0);
+  if (z0 == v.v && is_inf(z0)) return mk(z0, z0);
+  T t1 = expm1_cr(x1);
+  return mk(z0, add(mul(z0, t1), add(v.e, sub(v.v, z0))));
+}
+
+// ExpLog.texpm1 (explog.py:299-310)
+template <class T> TF_DEV TF<T> texpm1_gen(T x0, T x1) {
+  TF<T> w = pexpm10_raw_c(x0);
+  T z0 = expm1_cr(x0);
+  if (z0 == w.v && is_inf(z0)) return mk(z0, z0);
+  T t1 = expm1_cr(x1);
+  T tail = add(w.e, sub(w.v, z0));
+  return mk(z0, add(mul(add(z0, T(1)), t1), tail));
+}
+
+// _correct (explog.py:366-373)
+template <class T> TF_DEV TF<T> correct_c(TF<T> core, T lib0) {
+  if (is_inf(lib0) && core.v == lib0) return mk(lib0, lib0);
+  return mk(lib0, add(core.e, sub(core.v, lib0)));
+}
+
+// ExpLog.tlog (explog.py:394-399)
+template <class T> TF_DEV TF<T> tlog_gen(T y0, T y1) {
+  TF<T> v = renorm_c(mk(y0, y1));
+  TF<T> core = log_core_c(v.v, v.e);
+  return correct_c(core, log_cr(y0));
+}
+
+// ExpLog.tlog1p (explog.py:440-467) incl. tlogp for the out-of-band branch
+template <class T> TF_DEV TF<T> tlog1p_gen(T y0, T y1) {
+  TF<T> v = renorm_c(mk(y0, y1));
+  TF<T> core;
+  if (v.v < T(-0.5) || v.v > T(1)) {
+    TF<T> w = renorm_c(t_add_d_c(v, T(1)));
+    core = correct_c(log_core_c(w.v, w.e), log_cr(w.v));     // tlogp (389-392)
+  } else {
+    core = log1p_core_c(v.v, v.e);
+  }
+  return correct_c(core, log1p_cr(y0));
+}
+
+enum Fn { FN_TEXP = 0, FN_TEXPM1 = 1, FN_TLOG = 2, FN_TLOG1P = 3 };
+
+template <class T, int FN> __device__ __noinline__ TF<T> eval_gen(T x0, T x1) {
+  if (FN == FN_TEXP) return texp_gen(x0, x1);
+  if (FN == FN_TEXPM1) return texpm1_gen(x0, x1);
+  if (FN == FN_TLOG) return tlog_gen(x0, x1);
+  return tlog1p_gen(x0, x1);
+}
+
+}  // namespace tf

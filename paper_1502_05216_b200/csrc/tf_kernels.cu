@@ -1,0 +1,521 @@
+// tf_kernels.cu -- B200 (sm_100a) kernels and the C-ABI of libtwofold_b200.so.
+//
+// One persistent, grid-stride kernel per (function, width, vector width):
+//   * SoA inputs x0[], x1[] and outputs z0[], z1[], 128-bit streaming loads and
+//     stores (__ldcs/__stcs: each byte is touched once, keep L2 for others);
+//   * VW elements per thread per iteration (2 doubles / 4 floats = one 16 B
+//     vector per array), independent dependency chains for FP64/FP32 ILP;
+//   * coupled tables staged once per CTA in shared memory (12.8 KB binary64);
+//   * fast admission-band path for every element; elements outside the band
+//     are pushed onto a per-warp shared-memory queue and evaluated 32 at a
+//     time by the exact path (full warps, no long-lived divergence).
+// The C-ABI (include/twofold_b200.h) takes plain device pointers, an element
+// count and a cudaStream_t; it never throws and reports errors as negative
+// status codes with a message in tf_last_error().
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "tf_fast.cuh"
+#include "../../include/twofold_b200.h"
+
+namespace tf {
+
+constexpr int BLOCK = 256;
+constexpr int WARPS = BLOCK / 32;
+
+__device__ unsigned long long g_rare_count = 0;
+
+template <class T, int VW> struct Vec;
+template <> struct Vec<double, 2> { typedef double2 t; };
+template <> struct Vec<float, 4> { typedef float4 t; };
+template <> struct Vec<double, 1> { typedef double t; };
+template <> struct Vec<float, 1> { typedef float t; };
+
+template <class T, int VW>
+TF_DEV void ld(const T* p, uint64_t vi, T (&a)[VW]) {
+  if constexpr (VW == 1) {
+    a[0] = __ldcs(p + vi);
+  } else if constexpr (sizeof(T) == 8) {
+    double2 v = __ldcs(reinterpret_cast<const double2*>(p) + vi);
+    a[0] = v.x; a[1] = v.y;
+  } else {
+    float4 v = __ldcs(reinterpret_cast<const float4*>(p) + vi);
+    a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+  }
+}
+template <class T, int VW>
+TF_DEV void st(T* p, uint64_t vi, const T (&a)[VW]) {
+  if constexpr (VW == 1) {
+    __stcs(p + vi, a[0]);
+  } else if constexpr (sizeof(T) == 8) {
+    __stcs(reinterpret_cast<double2*>(p) + vi, make_double2(a[0], a[1]));
+  } else {
+    __stcs(reinterpret_cast<float4*>(p) + vi, make_float4(a[0], a[1], a[2], a[3]));
+  }
+}
+
+// Evaluate the queued rare elements q[0..cnt) (cnt <= 32) with the exact path.
+template <class T, int FN>
+TF_DEV void drain(const uint32_t* q, int cnt, const T* __restrict__ x0, const T* __restrict__ x1,
+                  T* __restrict__ z0, T* __restrict__ z1, int lane, bool count) {
+  if (lane < cnt) {
+    uint32_t i = q[lane];
+    TF<T> r = eval_gen<T, FN>(x0[i], x1[i]);
+    z0[i] = r.v;
+    z1[i] = r.e;
+  }
+  if (count && lane == 0) atomicAdd(&g_rare_count, (unsigned long long)cnt);
+}
+
+template <class T, int FN, int VW>
+__global__ void __launch_bounds__(BLOCK, 4)
+k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
+       T* __restrict__ z1, uint32_t n, int flags) {
+  constexpr int QCAP = 32 + 32 * VW;
+  __shared__ STab<T> tb;
+  __shared__ uint32_t qs[WARPS][QCAP];
+  load_tables(tb);
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* q = qs[warp];
+  const bool force = flags & TF_FLAG_FORCE_EXACT;
+  const bool count = flags & TF_FLAG_COUNT_EXACT;
+  int qn = 0;  // warp-uniform
+  const uint64_t nvec = n / VW;
+  const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
+  for (uint64_t base = (uint64_t)blockIdx.x * BLOCK + warp * 32; base < nvec; base += stride) {
+    const uint64_t vi = base + lane;
+    const bool valid = vi < nvec;
+    T a[VW], b[VW], r0[VW], r1[VW];
+    bool rare[VW];
+    if (valid) {
+      ld<T, VW>(x0, vi, a);
+      ld<T, VW>(x1, vi, b);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VW; ++e) { a[e] = T(0); b[e] = T(0); }
+    }
+#pragma unroll
+    for (int e = 0; e < VW; ++e) {
+      bool ok = fast_eval<T, FN>(tb, a[e], b[e], r0[e], r1[e]);
+      rare[e] = valid && (!ok || force);
+    }
+    if (valid) {
+      st<T, VW>(z0, vi, r0);
+      st<T, VW>(z1, vi, r1);
+    }
+#pragma unroll
+    for (int e = 0; e < VW; ++e) {
+      unsigned mask = __ballot_sync(0xffffffffu, rare[e]);
+      if (mask) {
+        if (rare[e]) q[qn + __popc(mask & ((1u << lane) - 1u))] = (uint32_t)(vi * VW + e);
+        qn += __popc(mask);
+      }
+    }
+    while (qn >= 32) {
+      __syncwarp();
+      drain<T, FN>(q, 32, x0, x1, z0, z1, lane, count);
+      __syncwarp();
+      uint32_t mv = (lane + 32 < qn) ? q[lane + 32] : 0u;
+      uint32_t mv2 = (lane + 64 < qn) ? q[lane + 64] : 0u;
+      uint32_t mv3 = (lane + 96 < qn) ? q[lane + 96] : 0u;
+      uint32_t mv4 = (lane + 128 < qn) ? q[lane + 128] : 0u;
+      __syncwarp();
+      if (lane + 32 < qn) q[lane] = mv;
+      if (lane + 64 < qn) q[lane + 32] = mv2;
+      if (lane + 96 < qn) q[lane + 64] = mv3;
+      if (lane + 128 < qn) q[lane + 96] = mv4;
+      qn -= 32;
+      __syncwarp();
+    }
+  }
+  // ragged tail (n % VW elements): exact path, first warp of block 0
+  const uint32_t tail = (uint32_t)(n - nvec * VW);
+  if (blockIdx.x == 0 && warp == 0 && tail) {
+    if (lane < (int)tail) q[qn + lane] = (uint32_t)(nvec * VW + lane);
+    qn += tail;
+  }
+  while (qn > 0) {
+    __syncwarp();
+    int c = qn < 32 ? qn : 32;
+    drain<T, FN>(q, c, x0, x1, z0, z1, lane, count);
+    __syncwarp();
+    uint32_t mv = (lane + 32 < qn) ? q[lane + 32] : 0u;
+    uint32_t mv2 = (lane + 64 < qn) ? q[lane + 64] : 0u;
+    uint32_t mv3 = (lane + 96 < qn) ? q[lane + 96] : 0u;
+    uint32_t mv4 = (lane + 128 < qn) ? q[lane + 128] : 0u;
+    __syncwarp();
+    if (lane + 32 < qn) q[lane] = mv;
+    if (lane + 64 < qn) q[lane + 32] = mv2;
+    if (lane + 96 < qn) q[lane + 64] = mv3;
+    if (lane + 128 < qn) q[lane + 96] = mv4;
+    qn -= c;
+  }
+}
+
+// ------------------------------------------------------------ generator
+// Bit-identical twin of paper_1502_05216_b200/workloads.py:generate.
+TF_DEV uint64_t mix64(uint64_t z) {
+  z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27; z *= 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+TF_DEV double u01(uint64_t h) { return (double)(h >> 11) * 0x1p-53; }
+
+__constant__ double c_pow10[301];
+__constant__ double c_special_exp[18];
+__constant__ double c_special_log[18];
+
+__global__ void k_generate(int dist, uint64_t k0, uint64_t k1, uint64_t k2, uint64_t k3,
+                           uint64_t start, uint64_t n, void* x0v, void* x1v) {
+  const uint64_t G = 0x9E3779B97F4A7C15ull;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t idx = start + j + 1;
+    uint64_t h0 = mix64(k0 + idx * G), h1 = mix64(k1 + idx * G);
+    uint64_t h2 = mix64(k2 + idx * G), h3 = mix64(k3 + idx * G);
+    double v = sub(mul(2.0, u01(h1)), 1.0);
+    double x0 = 0.0;
+    if (dist == TF_DIST_EXP64 || dist == TF_DIST_EXP64S) {
+      x0 = add(-700.0, mul(1400.0, u01(h0)));
+    } else if (dist == TF_DIST_POW10 || dist == TF_DIST_POW10C) {
+      double s = add(1.0, mul(9.0, u01(h0)));
+      x0 = mul(s, c_pow10[h2 % 301ull]);
+      if (h3 & 1ull) x0 = -x0;
+      if (dist == TF_DIST_POW10C) x0 = fmin(fmax(x0, -1.0 + 0x1p-52), 1e300);
+    } else if (dist == TF_DIST_LOG64 || dist == TF_DIST_LOGU64S) {
+      double m = add(1.0, mul((double)(h0 >> 12), 0x1p-52));
+      int e = dist == TF_DIST_LOG64 ? (int)(h2 % 2046ull) - 1022 : (int)(h2 % 2045ull) - 1022;
+      x0 = ldexp(m, e);
+      if (dist == TF_DIST_LOG64 && (double)(h3 >> 11) * 0x1p-53 < 0.05) {
+        double d = mul(sub(mul(2.0, u01(mix64(h3))), 1.0), 0x1p-40);
+        x0 = add(1.0, d);
+      }
+    } else if (dist == TF_DIST_EXP32 || dist == TF_DIST_LOG32) {
+      float f;
+      if (dist == TF_DIST_EXP32) {
+        f = __double2float_rn(add(-87.0, mul(175.0, u01(h0))));
+      } else {
+        double m = add(1.0, mul((double)(h0 >> 41), 0x1p-23));
+        f = __double2float_rn(ldexp(m, (int)(h2 % 254ull) - 126));
+      }
+      float g = __double2float_rn(mul(mul((double)f, v), 0x1p-24));
+      static_cast<float*>(x0v)[j] = f;
+      static_cast<float*>(x1v)[j] = g;
+      continue;
+    }
+    double x1 = mul(mul(x0, v), 0x1p-53);
+    if (dist == TF_DIST_EXP64S || dist == TF_DIST_LOGU64S) {
+      uint64_t hs = mix64(h3 ^ 0x5555555555555555ull);
+      if ((double)(hs >> 11) * 0x1p-53 < 0.01) {
+        x0 = (dist == TF_DIST_EXP64S ? c_special_exp : c_special_log)[hs % 18ull];
+        x1 = 0.0;
+      }
+    }
+    static_cast<double*>(x0v)[j] = x0;
+    static_cast<double*>(x1v)[j] = x1;
+  }
+}
+
+// -------------------------------------------------------- parity stats
+// Per-element comparison of (z0, z1) against a reference (r0, r1) on device:
+// stats[0] elements, [1] z0 bit mismatches, [2] z0 mismatches > 1 ulp,
+// [3] z0+z1 tolerance violations, [4] non-finite class mismatches,
+// [5] z1 bit mismatches.  Tolerance: |d| <= max(rel*|ref|, abs_guard).
+template <class T>
+__global__ void k_compare(const T* z0, const T* z1, const T* r0, const T* r1, uint64_t n,
+                          double rel, double abs_guard, unsigned long long* stats) {
+  unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    T a0 = z0[i], a1 = z1[i], b0 = r0[i], b1 = r1[i];
+    c[0]++;
+    bool a0n = is_nan(a0), b0n = is_nan(b0);
+    bool same0 = (ubits(a0) == ubits(b0)) || (a0n && b0n);
+    bool same1 = (ubits(a1) == ubits(b1)) || (is_nan(a1) && is_nan(b1));
+    if (!same0) {
+      c[1]++;
+      long long d = (long long)ubits(a0) - (long long)ubits(b0);
+      bool samesign = sgn(a0) == sgn(b0);
+      if (a0n || b0n || !samesign || d > 1 || d < -1) {
+        if (!(a0 == T(0) && b0 == T(0))) c[2]++;
+      }
+    }
+    if (!same1) c[5]++;
+    bool fa = is_finite(a0) && is_finite(a1), fb = is_finite(b0) && is_finite(b1);
+    if (fa && fb) {
+      double ref = (double)b0 + (double)b1;
+      double d = ((double)a0 - (double)b0) + ((double)a1 - (double)b1);
+      double tol = fmax(rel * fabs(ref), abs_guard);
+      if (!(fabs(d) <= tol)) c[3]++;
+    } else {
+      // same class per field: NaN <-> NaN, inf of the same sign
+      bool k0 = same0 || (a0 == b0);
+      bool k1 = (is_nan(a1) && is_nan(b1)) || (!is_nan(a1) && !is_nan(b1) &&
+                                                (is_finite(a1) == is_finite(b1)) &&
+                                                (is_finite(a1) || a1 == b1));
+      if (!(k0 && k1)) c[4]++;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    unsigned long long v = c[k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&stats[k], v);
+  }
+}
+
+// ------------------------------------------------ pipe peak calibration
+// 8 independent FMA chains per thread; every FMA counts as one op (the unit of
+// the algorithmic op counts).  Used by bench.py for the roofline denominator.
+template <class T>
+__global__ void __launch_bounds__(256) k_fma_peak(T* out, int iters, T a, T b) {
+  T c[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) c[k] = T(threadIdx.x + k);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = fmaop(c[k], a, b);
+  }
+  T s = T(0);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s = add(s, c[k]);
+  if (s == T(-1.2345)) out[0] = s;  // never true; keeps the chains alive
+}
+
+}  // namespace tf
+
+// ===================================================================== ABI
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, const char* detail = "") {
+  snprintf(g_err, sizeof g_err, fmt, detail);
+  return code;
+}
+
+int cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof g_err, "%s: %s", what, cudaGetErrorString(e));
+    return TF_ERR_CUDA;
+  }
+  return TF_OK;
+}
+
+struct DevInfo {
+  int sms = 0;
+};
+std::mutex g_mu;
+DevInfo g_dev[64];
+bool g_const_ready[64] = {};
+
+int device_sms() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return 148;
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_dev[d].sms) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    g_dev[d].sms = v > 0 ? v : 148;
+  }
+  return g_dev[d].sms;
+}
+
+template <class T, int FN, int VW>
+int launch_one(const T* x0, const T* x1, T* z0, T* z1, int64_t n, cudaStream_t s, int flags) {
+  static int occ = 0;
+  if (!occ) {
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, tf::k_eval<T, FN, VW>, tf::BLOCK, 0);
+    occ = v > 0 ? v : 1;
+  }
+  const int64_t CHUNK = (int64_t)1 << 31;  // queue indices are 32-bit
+  for (int64_t off = 0; off < n; off += CHUNK) {
+    int64_t m = n - off < CHUNK ? n - off : CHUNK;
+    int64_t vecs = (m / VW + tf::BLOCK - 1) / tf::BLOCK;
+    int64_t grid = (int64_t)device_sms() * occ;
+    if (vecs < grid) grid = vecs > 0 ? vecs : 1;
+    tf::k_eval<T, FN, VW><<<(unsigned)grid, tf::BLOCK, 0, s>>>(x0 + off, x1 + off, z0 + off,
+                                                              z1 + off, (uint32_t)m, flags);
+  }
+  return cuda_check("k_eval launch");
+}
+
+template <class T, int FN>
+int launch(const T* x0, const T* x1, T* z0, T* z1, int64_t n, void* stream, int flags) {
+  if (n < 0) return fail(TF_ERR_ARG, "negative element count%s");
+  if (n == 0) return TF_OK;
+  if (!x0 || !x1 || !z0 || !z1) return fail(TF_ERR_ARG, "null pointer%s");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uintptr_t al = (uintptr_t)x0 | (uintptr_t)x1 | (uintptr_t)z0 | (uintptr_t)z1;
+  if ((al & 15) == 0) {
+    if constexpr (sizeof(T) == 8) return launch_one<T, FN, 2>(x0, x1, z0, z1, n, s, flags);
+    else return launch_one<T, FN, 4>(x0, x1, z0, z1, n, s, flags);
+  }
+  if ((al & (sizeof(T) - 1)) != 0) return fail(TF_ERR_ARG, "misaligned pointer%s");
+  return launch_one<T, FN, 1>(x0, x1, z0, z1, n, s, flags);
+}
+
+int ensure_constants() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return cuda_check("cudaGetDevice");
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_const_ready[d]) return TF_OK;
+  }
+  double p10[301];
+  for (int e = 0; e <= 300; ++e) {
+    char buf[16];
+    snprintf(buf, sizeof buf, "1e-%d", e);
+    p10[e] = strtod(buf, nullptr);  // correctly rounded decimal conversion
+  }
+  const double lo = -0x1.74385446d71c4p+9, hi = 0x1.62e42fefa39f0p+9;
+  const double inf = __builtin_inf(), nan = __builtin_nan("");
+  const double sp_exp[18] = {0.0, -0.0, inf, -inf, nan, 5e-324, -5e-324, 2.2250738585072009e-308,
+                             lo, nextafter(lo, -inf), nextafter(lo, inf), hi, nextafter(hi, inf),
+                             nextafter(hi, -inf), -745.13, -708.40, 709.78, 709.782712893384};
+  const double sp_log[18] = {0.0, -0.0, inf, -inf, nan, 5e-324, -5e-324, 2.2250738585072009e-308,
+                             2.225073858507201e-308 / 3, 1.0, -1.0, 1.7976931348623157e308, 0.5,
+                             2.0, nextafter(1.0, 0.0), nextafter(1.0, 2.0),
+                             4.9406564584124654e-322, 1e-320};
+  cudaMemcpyToSymbol(tf::c_pow10, p10, sizeof p10);
+  cudaMemcpyToSymbol(tf::c_special_exp, sp_exp, sizeof sp_exp);
+  cudaMemcpyToSymbol(tf::c_special_log, sp_log, sizeof sp_log);
+  int rc = cuda_check("constant upload");
+  if (rc == TF_OK) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_const_ready[d] = true;
+  }
+  return rc;
+}
+
+uint64_t mix64h(uint64_t z) {
+  z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27; z *= 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+}  // namespace
+
+extern "C" {
+
+TF_API int tf_version(void) { return TF_ABI_VERSION; }
+
+TF_API const char* tf_last_error(void) { return g_err; }
+
+TF_API int tf_init(int device) {
+  if (device >= 0 && cudaSetDevice(device) != cudaSuccess) return cuda_check("cudaSetDevice");
+  device_sms();
+  return ensure_constants();
+}
+
+#define TF_DEF(NAME, T, FN)                                                                \
+  TF_API int NAME(const T* x0, const T* x1, T* z0, T* z1, int64_t n, void* stream) {   \
+    return launch<T, FN>(x0, x1, z0, z1, n, stream, 0);                                 \
+  }
+TF_DEF(tf_texp_f64, double, tf::FN_TEXP)
+TF_DEF(tf_texpm1_f64, double, tf::FN_TEXPM1)
+TF_DEF(tf_tlog_f64, double, tf::FN_TLOG)
+TF_DEF(tf_tlog1p_f64, double, tf::FN_TLOG1P)
+TF_DEF(tf_texp_f32, float, tf::FN_TEXP)
+TF_DEF(tf_texpm1_f32, float, tf::FN_TEXPM1)
+TF_DEF(tf_tlog_f32, float, tf::FN_TLOG)
+TF_DEF(tf_tlog1p_f32, float, tf::FN_TLOG1P)
+#undef TF_DEF
+
+TF_API int tf_eval(int fn, int width, const void* x0, const void* x1, void* z0, void* z1,
+                   int64_t n, void* stream, int flags) {
+  if (width == 64) {
+    auto a = static_cast<const double*>(x0), b = static_cast<const double*>(x1);
+    auto c = static_cast<double*>(z0), d = static_cast<double*>(z1);
+    switch (fn) {
+      case TF_FN_TEXP: return launch<double, tf::FN_TEXP>(a, b, c, d, n, stream, flags);
+      case TF_FN_TEXPM1: return launch<double, tf::FN_TEXPM1>(a, b, c, d, n, stream, flags);
+      case TF_FN_TLOG: return launch<double, tf::FN_TLOG>(a, b, c, d, n, stream, flags);
+      case TF_FN_TLOG1P: return launch<double, tf::FN_TLOG1P>(a, b, c, d, n, stream, flags);
+    }
+  } else if (width == 32) {
+    auto a = static_cast<const float*>(x0), b = static_cast<const float*>(x1);
+    auto c = static_cast<float*>(z0), d = static_cast<float*>(z1);
+    switch (fn) {
+      case TF_FN_TEXP: return launch<float, tf::FN_TEXP>(a, b, c, d, n, stream, flags);
+      case TF_FN_TEXPM1: return launch<float, tf::FN_TEXPM1>(a, b, c, d, n, stream, flags);
+      case TF_FN_TLOG: return launch<float, tf::FN_TLOG>(a, b, c, d, n, stream, flags);
+      case TF_FN_TLOG1P: return launch<float, tf::FN_TLOG1P>(a, b, c, d, n, stream, flags);
+    }
+  } else {
+    return fail(TF_ERR_ARG, "unsupported width (expected 32 or 64)%s");
+  }
+  return fail(TF_ERR_ARG, "unknown function code%s");
+}
+
+TF_API int tf_generate(int dist, uint64_t seed, int64_t start, int64_t n, void* x0, void* x1,
+                       void* stream) {
+  if (n < 0 || start < 0) return fail(TF_ERR_ARG, "negative range%s");
+  if (dist < 0 || dist >= TF_DIST_COUNT) return fail(TF_ERR_ARG, "unknown distribution%s");
+  if (n == 0) return TF_OK;
+  if (!x0 || !x1) return fail(TF_ERR_ARG, "null pointer%s");
+  int rc = ensure_constants();
+  if (rc) return rc;
+  uint64_t k[4];
+  for (uint64_t s = 0; s < 4; ++s)
+    k[s] = mix64h(seed * 0x9E3779B97F4A7C15ull + s * 0xD1B54A32D192ED03ull);
+  int64_t grid = (int64_t)device_sms() * 8;
+  int64_t need = (n + 255) / 256;
+  if (need < grid) grid = need;
+  tf::k_generate<<<(unsigned)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      dist, k[0], k[1], k[2], k[3], (uint64_t)start, (uint64_t)n, x0, x1);
+  return cuda_check("k_generate launch");
+}
+
+TF_API int tf_compare(int width, const void* z0, const void* z1, const void* r0, const void* r1,
+                      int64_t n, double rel, double abs_guard, unsigned long long* stats_dev,
+                      void* stream) {
+  if (n < 0) return fail(TF_ERR_ARG, "negative element count%s");
+  if (!stats_dev) return fail(TF_ERR_ARG, "null stats pointer%s");
+  if (n == 0) return TF_OK;
+  int64_t grid = (int64_t)device_sms() * 8;
+  int64_t need = (n + 255) / 256;
+  if (need < grid) grid = need;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (width == 64)
+    tf::k_compare<double><<<(unsigned)grid, 256, 0, s>>>(
+        (const double*)z0, (const double*)z1, (const double*)r0, (const double*)r1, (uint64_t)n,
+        rel, abs_guard, stats_dev);
+  else if (width == 32)
+    tf::k_compare<float><<<(unsigned)grid, 256, 0, s>>>(
+        (const float*)z0, (const float*)z1, (const float*)r0, (const float*)r1, (uint64_t)n, rel,
+        abs_guard, stats_dev);
+  else
+    return fail(TF_ERR_ARG, "unsupported width%s");
+  return cuda_check("k_compare launch");
+}
+
+TF_API int tf_fma_peak(int width, void* out_dev, int blocks, int iters, void* stream) {
+  if (blocks <= 0 || iters <= 0 || !out_dev) return fail(TF_ERR_ARG, "bad peak arguments%s");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (width == 64)
+    tf::k_fma_peak<double><<<blocks, 256, 0, s>>>((double*)out_dev, iters, 0.999999, 1e-7);
+  else if (width == 32)
+    tf::k_fma_peak<float><<<blocks, 256, 0, s>>>((float*)out_dev, iters, 0.999999f, 1e-7f);
+  else
+    return fail(TF_ERR_ARG, "unsupported width%s");
+  return cuda_check("k_fma_peak launch");
+}
+
+TF_API int tf_exact_count(unsigned long long* out, int reset) {
+  if (!out) return fail(TF_ERR_ARG, "null pointer%s");
+  if (cudaMemcpyFromSymbol(out, tf::g_rare_count, sizeof(*out)) != cudaSuccess)
+    return cuda_check("read exact-path counter");
+  if (reset) {
+    unsigned long long z = 0;
+    cudaMemcpyToSymbol(tf::g_rare_count, &z, sizeof z);
+  }
+  return cuda_check("exact-path counter");
+}
+
+}  // extern "C"

@@ -1,0 +1,250 @@
+"""Drop-in twofold exp/log surface, B200 edition.
+
+Mirrors the reference public API (pkg/src/twofold/explog.py:44-62, 219-499;
+__init__.py:19-57): ``api(width, backend=None) -> ExpLog``, ``ExpLog.texp /
+texpm1 / tlog / tlog1p``, ``ExpLog.function(name)``, ``get_function(name,
+width, backend=None)``, ``FAMILIES``, ``FUNCTION_NAMES``, ``DOTTED_ARG``,
+``COUPLED_ARG``, ``TWOFOLD_ARG``, ``family_of``.  Same names, argument meaning
+and error behaviour (ValueError for a bad width, backend or function name).
+
+What changes is the operand: besides the reference's scalar pair ``(x0, x1)``
+an argument may be a pair of arrays -- CUDA tensors (evaluated on their device
+and the current stream, results allocated there), CPU tensors or numpy arrays
+(copied through pinned staging buffers, results returned on the host).  Every
+evaluation runs the hand-written sm_100a kernels of libtwofold_b200.so; there
+is no CPU fallback.
+
+Of the twenty reference functions the four twofold-argument ones
+(TWOFOLD_ARG) are implemented; the other sixteen (explog.py:251-475) are the
+next rows of the coverage plan and raise NotImplementedError here.
+"""
+
+from __future__ import annotations
+
+from functools import lru_cache
+
+import numpy as np
+
+from . import _lib
+from .eft import Twofold, get_default_backend
+from .params import params_for_width
+
+__all__ = ["ExpLog", "api", "get_function", "FAMILIES", "FUNCTION_NAMES", "DOTTED_ARG",
+           "COUPLED_ARG", "TWOFOLD_ARG", "family_of"]
+
+FAMILIES = {
+    "exp": ("pexp0", "texp0", "texp", "texpp", "pexp"),
+    "expm1": ("pexpm10", "texpm10", "texpm1", "texpm1p", "pexpm1"),
+    "log": ("plog0", "tlog0", "tlogp", "tlog", "plog"),
+    "log1p": ("plog1p0", "tlog1p0", "tlog1pp", "tlog1p", "plog1p"),
+}
+FUNCTION_NAMES = tuple(name for fam in FAMILIES.values() for name in fam)
+DOTTED_ARG = frozenset(n for n in FUNCTION_NAMES if n.endswith("0"))
+COUPLED_ARG = frozenset(("texpp", "pexp", "texpm1p", "pexpm1", "tlogp", "plog", "tlog1pp",
+                         "plog1p"))
+TWOFOLD_ARG = frozenset(("texp", "texpm1", "tlog", "tlog1p"))
+
+HOST_CHUNK = 1 << 22  # elements per pipelined host<->device chunk
+
+
+def family_of(name: str) -> str:
+    for fam, names in FAMILIES.items():
+        if name in names:
+            return fam
+    raise ValueError(f"unknown function {name!r}")
+
+
+def _is_torch(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+class ExpLog:
+    """Twofold exponent and logarithm functions for one float width."""
+
+    def __init__(self, width: int, backend: str | None = None):
+        params = params_for_width(width)
+        if backend is None:
+            backend = get_default_backend()
+        if backend not in ("fma", "dv"):
+            raise ValueError(f"unknown backend {backend!r}; expected 'fma' or 'dv'")
+        self.width = width
+        # Both reference backends name an exact-product residual; the GPU computes
+        # it with one hardware FMA (bitwise equal to "dv" except subnormal z1).
+        self.backend = backend
+        self.params = params
+        self._np = np.float64 if width == 64 else np.float32
+
+    # ---- the four twofold-argument functions (explog.py:265, 299, 394, 464)
+    def texp(self, x):
+        """Twofold e**(x0+x1); value part = correctly rounded exp(x0)."""
+        return self._call("texp", x)
+
+    def texpm1(self, x):
+        """Twofold e**(x0+x1) - 1; value part = correctly rounded expm1(x0)."""
+        return self._call("texpm1", x)
+
+    def tlog(self, y):
+        """Twofold ln of any twofold; value part = correctly rounded log(y0)."""
+        return self._call("tlog", y)
+
+    def tlog1p(self, y):
+        """Twofold ln(1 + y0 + y1); value part = correctly rounded log1p(y0)."""
+        return self._call("tlog1p", y)
+
+    def function(self, name: str):
+        if name not in FUNCTION_NAMES:
+            raise ValueError(f"unknown function {name!r}")
+        if name not in TWOFOLD_ARG:
+            raise NotImplementedError(
+                f"{name!r} is not on the B200 hot path yet (implemented: "
+                f"{', '.join(sorted(TWOFOLD_ARG))})")
+        return getattr(self, name)
+
+    def __getattr__(self, name):
+        if name in FUNCTION_NAMES:
+            return self.function(name)
+        raise AttributeError(name)
+
+    # ---- dispatch
+    def _call(self, fn: str, x, out=None):
+        x0, x1 = x[0], x[1]
+        if _is_torch(x0) or _is_torch(x1):
+            if not (_is_torch(x0) and _is_torch(x1)):
+                raise TypeError("both twofold parts must be torch tensors")
+            if x0.is_cuda or x1.is_cuda:
+                return self._device(fn, x0, x1, out)
+            return self._host_torch(fn, x0, x1)
+        if np.isscalar(x0) and np.isscalar(x1) or (isinstance(x0, (int, float)) and
+                                                   isinstance(x1, (int, float))):
+            a0 = np.array([x0], dtype=self._np)
+            a1 = np.array([x1], dtype=self._np)
+            z0, z1 = self._host_numpy(fn, a0, a1)
+            return Twofold(float(z0[0]), float(z1[0]))
+        a0 = np.asarray(x0)
+        a1 = np.asarray(x1)
+        if a0.shape != a1.shape:
+            raise ValueError(f"twofold parts differ in shape: {a0.shape} vs {a1.shape}")
+        z0, z1 = self._host_numpy(fn, a0.astype(self._np, copy=False),
+                                  a1.astype(self._np, copy=False))
+        return Twofold(z0, z1)
+
+    def _torch_dtype(self):
+        import torch
+
+        return torch.float64 if self.width == 64 else torch.float32
+
+    def _launch(self, fn, x0, x1, z0, z1, n, stream_ptr, flags=0):
+        L = _lib.ensure_device(x0.device.index if x0.device.index is not None else 0)
+        rc = L.tf_eval(_lib.FN_CODES[fn], self.width, x0.data_ptr(), x1.data_ptr(),
+                       z0.data_ptr(), z1.data_ptr(), n, stream_ptr, flags)
+        _lib.check(rc, f"tf_eval({fn}, width={self.width})")
+
+    def _device(self, fn, x0, x1, out=None, flags=0):
+        import torch
+
+        dt = self._torch_dtype()
+        if x0.dtype != dt or x1.dtype != dt:
+            raise TypeError(f"binary{self.width} twofolds need {dt} tensors, got "
+                            f"{x0.dtype}/{x1.dtype}")
+        if x0.shape != x1.shape:
+            raise ValueError(f"twofold parts differ in shape: {tuple(x0.shape)} vs "
+                             f"{tuple(x1.shape)}")
+        if x0.device != x1.device:
+            raise ValueError("twofold parts live on different devices")
+        a0 = x0.contiguous()
+        a1 = x1.contiguous()
+        if out is None:
+            z0 = torch.empty_like(a0)
+            z1 = torch.empty_like(a1)
+        else:
+            z0, z1 = out
+            if (z0.shape != a0.shape or z1.shape != a0.shape or z0.dtype != dt or
+                    z1.dtype != dt or not z0.is_contiguous() or not z1.is_contiguous()):
+                raise ValueError("out= tensors must be contiguous, same shape and dtype")
+        with torch.cuda.device(a0.device):
+            stream = torch.cuda.current_stream(a0.device).cuda_stream
+            self._launch(fn, a0, a1, z0, z1, a0.numel(), stream, flags)
+        return Twofold(z0, z1)
+
+    def _host_torch(self, fn, x0, x1):
+        import torch
+
+        dt = self._torch_dtype()
+        if x0.shape != x1.shape:
+            raise ValueError(f"twofold parts differ in shape: {tuple(x0.shape)} vs "
+                             f"{tuple(x1.shape)}")
+        a0 = x0.to(dt).contiguous().reshape(-1)
+        a1 = x1.to(dt).contiguous().reshape(-1)
+        z0, z1 = _pipeline(self, fn, a0, a1)
+        return Twofold(z0.reshape(x0.shape), z1.reshape(x0.shape))
+
+    def _host_numpy(self, fn, a0, a1):
+        import torch
+
+        t0 = torch.from_numpy(np.ascontiguousarray(a0).reshape(-1))
+        t1 = torch.from_numpy(np.ascontiguousarray(a1).reshape(-1))
+        z0, z1 = _pipeline(self, fn, t0, t1)
+        return z0.numpy().reshape(a0.shape), z1.numpy().reshape(a0.shape)
+
+
+def _pipeline(lib: ExpLog, fn: str, h0, h1, device=None, chunk: int = HOST_CHUNK):
+    """Evaluate host tensors: chunked H2D -> kernel -> D2H on two streams so the
+    copy engines run both directions while the kernels execute."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device visible: the twofold kernels need a B200 "
+                           "(sm_100a); there is no CPU fallback")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    n = h0.numel()
+    pinned = h0.is_pinned() and h1.is_pinned()
+    z0 = torch.empty(n, dtype=h0.dtype, pin_memory=True)
+    z1 = torch.empty(n, dtype=h0.dtype, pin_memory=True)
+    if n == 0:
+        return z0, z1
+    if not pinned:
+        h0 = h0.pin_memory()
+        h1 = h1.pin_memory()
+    c = min(chunk, n)
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    bufs = [[torch.empty(c, dtype=h0.dtype, device=dev) for _ in range(4)] for _ in range(2)]
+    cur = torch.cuda.current_stream(dev)
+    for s in streams:
+        s.wait_stream(cur)
+    for k, off in enumerate(range(0, n, c)):
+        m = min(c, n - off)
+        s = streams[k & 1]
+        d0, d1, e0, e1 = (b[:m] for b in bufs[k & 1])
+        with torch.cuda.stream(s):
+            d0.copy_(h0[off:off + m], non_blocking=True)
+            d1.copy_(h1[off:off + m], non_blocking=True)
+            lib._launch(fn, d0, d1, e0, e1, m, s.cuda_stream)
+            z0[off:off + m].copy_(e0, non_blocking=True)
+            z1[off:off + m].copy_(e1, non_blocking=True)
+    for s in streams:
+        s.synchronize()
+    return z0, z1
+
+
+@lru_cache(maxsize=None)
+def _api_cached(width: int, backend: str) -> ExpLog:
+    return ExpLog(width, backend)
+
+
+def api(width: int, backend: str | None = None) -> ExpLog:
+    """Cached function surface for (width, backend) (explog.py:488-494)."""
+    if backend is None:
+        backend = get_default_backend()
+    elif backend not in ("fma", "dv"):
+        raise ValueError(f"unknown backend {backend!r}")
+    return _api_cached(width, backend)
+
+
+def get_function(name: str, width: int, backend: str | None = None):
+    """Resolve one of the twenty function names for a width (explog.py:497-499)."""
+    return api(width, backend).function(name)
+
