@@ -40,6 +40,28 @@ def same_bits(a: np.ndarray, b: np.ndarray) -> np.ndarray:
 
 
 def compare(z0, z1, r0, r1, width: int) -> dict:
+    with np.errstate(all="ignore"):
+        return _compare(z0, z1, r0, r1, width)
+
+
+def bad_mask(z0, z1, r0, r1, width: int) -> np.ndarray:
+    """Elements violating the tolerance or the non-finite class rule."""
+    z0, z1, r0, r1 = (np.asarray(v) for v in (z0, z1, r0, r1))
+    rel, guard = TOL[width]
+    with np.errstate(all="ignore"):
+        finite = np.isfinite(z0) & np.isfinite(z1) & np.isfinite(r0) & np.isfinite(r1)
+        a0, a1, b0, b1 = (v.astype(np.float64) for v in (z0, z1, r0, r1))
+        d = (a0 - b0) + (a1 - b1)
+        viol = finite & ~(np.abs(d) <= np.maximum(rel * np.abs(b0 + b1), guard))
+
+        def cls(a, b):
+            return (np.isnan(a) & np.isnan(b)) | (np.isinf(a) & (a == b)) | \
+                (np.isfinite(a) & np.isfinite(b))
+
+        return viol | ~(cls(z0, r0) & cls(z1, r1))
+
+
+def _compare(z0, z1, r0, r1, width: int) -> dict:
     z0, z1, r0, r1 = (np.asarray(v) for v in (z0, z1, r0, r1))
     rel, guard = TOL[width]
     n = z0.size
@@ -52,10 +74,11 @@ def compare(z0, z1, r0, r1, width: int) -> dict:
         d = (a0 - b0) + (a1 - b1)
         tol = np.maximum(rel * np.abs(b0 + b1), guard)
         viol = finite & ~(np.abs(d) <= tol)
-        # non-finite anywhere: class equality per field
-        cls0 = s0 | (z0 == r0)
-        cls1 = (np.isnan(z1) & np.isnan(r1)) | (z1 == r1) | (np.isfinite(z1) & np.isfinite(r1))
-    cls_bad = ~finite & ~(cls0 & cls1)
+    def cls(a, b):  # same class per field: NaN <-> NaN, +-inf same sign, finite <-> finite
+        return (np.isnan(a) & np.isnan(b)) | (np.isinf(a) & (a == b)) | \
+            (np.isfinite(a) & np.isfinite(b))
+
+    cls_bad = ~(cls(z0, r0) & cls(z1, r1))
     mism = ~s0
     hist = {}
     if mism.any():

@@ -17,6 +17,7 @@ by tests/golden/gen_golden.py).
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 
@@ -27,6 +28,94 @@ LIB_PATH = os.path.join(HERE, "build", "libtforacle.so")
 
 FNS = {"texp": 0, "texpm1": 1, "tlog": 2, "tlog1p": 3}
 _LIBM32 = {0: np.exp, 1: np.expm1, 2: np.log, 3: np.log1p}
+
+
+def _cr32(ufunc):
+    """binary32 libm stand-in that is correctly rounded up to double-rounding
+    (p ~ 2^-28): evaluate in binary64, round once to binary32."""
+    def f(x):
+        return ufunc(x.astype(np.float64)).astype(np.float32)
+    return f
+
+
+_LIBM32_CR = {k: _cr32(v) for k, v in _LIBM32.items()}
+
+
+def _rn64(x) -> float:
+    """Round an mpmath number to the nearest binary64 (ties-to-even), with
+    gradual underflow and overflow to +-inf."""
+    import mpmath
+
+    if x == 0:
+        return 0.0
+    sign, man, exp, bc = x._mpf_
+    lead = exp + bc - 1
+    if lead > 1023:
+        return -math.inf if sign else math.inf
+    q = max(lead - 52, -1074)
+    shift = q - exp
+    if shift <= 0:
+        r = man << (-shift)
+    else:
+        r = man >> shift
+        rem = man - (r << shift)
+        half = 1 << (shift - 1)
+        if rem > half or (rem == half and (r & 1)):
+            r += 1
+    v = math.ldexp(float(r), q) if r < (1 << 60) else math.inf
+    del mpmath
+    return -v if sign else v
+
+
+def _cr64_scalar(f: int, x: float) -> float:
+    """Correctly rounded binary64 exp/expm1/log/log1p (mpmath, 160 bits) with
+    the reference's IEEE special results (_fp.py:191-218)."""
+    import mpmath
+
+    if math.isnan(x):
+        return x
+    if f == 0:
+        if math.isinf(x):
+            return x if x > 0 else 0.0
+        if x > 710.0:
+            return math.inf
+        if x < -746.0:
+            return 0.0
+    elif f == 1:
+        if math.isinf(x):
+            return x if x > 0 else -1.0
+        if x == 0.0:
+            return x
+        if x > 710.0:
+            return math.inf
+        if x < -50.0:
+            return -1.0
+    elif f == 2:
+        if x < 0.0:
+            return math.nan
+        if x == 0.0:
+            return -math.inf
+        if math.isinf(x):
+            return x
+    else:
+        if x < -1.0:
+            return math.nan
+        if x == -1.0:
+            return -math.inf
+        if math.isinf(x) or x == 0.0:
+            return x
+    with mpmath.workprec(160):
+        v = (mpmath.exp, mpmath.expm1, mpmath.log, mpmath.log1p)[f](mpmath.mpf(x))
+        return _rn64(v)
+
+
+def _cr64(f: int):
+    def g(x):
+        return np.array([_cr64_scalar(f, float(v)) for v in x], dtype=np.float64)
+    return g
+
+
+_LIBM64_CR = {k: _cr64(k) for k in range(4)}
 
 _lib = None
 
@@ -50,6 +139,8 @@ def lib():
         L.tfo_eval_f64.restype = i32
         L.tfo_eval_f32_pass.argtypes = [i32, i32, vp, vp, vp, vp, i64, vp, i32, vp, vp, i32]
         L.tfo_eval_f32_pass.restype = i64
+        L.tfo_eval_f64_pass.argtypes = [i32, i32, vp, vp, vp, vp, i64, vp, i32, vp, vp, i32]
+        L.tfo_eval_f64_pass.restype = i64
         L.tfo_maxcalls.restype = i32
         for name in ("tfo_pexp0_raw64", "tfo_pexpm10_raw64", "tfo_taylor_exp64",
                      "tfo_taylor_expm1_64"):
@@ -73,15 +164,22 @@ def default_threads() -> int:
     return max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count() or 1)
 
 
-def evaluate(fn: str, width: int, x0, x1, backend: str = "dv", nthreads: int | None = None):
-    """Reference result (z0, z1) for arrays x0, x1 of the lane's dtype."""
+def evaluate(fn: str, width: int, x0, x1, backend: str = "dv", nthreads: int | None = None,
+             libm32: str = "numpy", libm64: str = "glibc"):
+    """Reference result (z0, z1) for arrays x0, x1 of the lane's dtype.
+
+    libm32="numpy" is the reference's binary32 libm (_fp.py:221-245);
+    libm32="cr" swaps in correctly rounded values (the "CR-sim" oracle of
+    SURVEY.md B.6), which isolates the algorithm from numpy's libm error.
+    libm64="cr" does the same for binary64 (mpmath; slow, small samples only).
+    """
     L = lib()
     code = FNS[fn]
     dv = 1 if backend == "dv" else 0
     if backend not in ("dv", "fma"):
         raise ValueError(f"unknown backend {backend!r}")
     nt = nthreads or default_threads()
-    if width == 64:
+    if width == 64 and libm64 == "glibc":
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         x1 = np.ascontiguousarray(x1, dtype=np.float64)
         n = x0.size
@@ -91,20 +189,26 @@ def evaluate(fn: str, width: int, x0, x1, backend: str = "dv", nthreads: int | N
         if rc != 0:
             raise RuntimeError("oracle rejected arguments")
         return z0, z1
-    if width != 32:
+    if width not in (32, 64):
         raise ValueError(f"unsupported width {width!r}")
-    x0 = np.ascontiguousarray(x0, dtype=np.float32)
-    x1 = np.ascontiguousarray(x1, dtype=np.float32)
+    dt = np.float64 if width == 64 else np.float32
+    run_pass = L.tfo_eval_f64_pass if width == 64 else L.tfo_eval_f32_pass
+    x0 = np.ascontiguousarray(x0, dtype=dt)
+    x1 = np.ascontiguousarray(x1, dtype=dt)
     n = x0.size
     mc = L.tfo_maxcalls()
-    z0 = np.full(n, np.nan, np.float32)
-    z1 = np.full(n, np.nan, np.float32)
-    ans = np.zeros((n, mc), np.float32)
-    req_arg = np.zeros(n, np.float32)
+    z0 = np.full(n, np.nan, dt)
+    z1 = np.full(n, np.nan, dt)
+    ans = np.zeros((n, mc), dt)
+    req_arg = np.zeros(n, dt)
     req_fn = np.full(n, -1, np.int8)
+    if width == 64:
+        table = _LIBM64_CR
+    else:
+        table = _LIBM32 if libm32 == "numpy" else _LIBM32_CR
     for k in range(mc + 1):
-        pending = L.tfo_eval_f32_pass(code, dv, _ptr(x0), _ptr(x1), _ptr(z0), _ptr(z1), n,
-                                      _ptr(ans), k, _ptr(req_arg), _ptr(req_fn), nt)
+        pending = run_pass(code, dv, _ptr(x0), _ptr(x1), _ptr(z0), _ptr(z1), n,
+                           _ptr(ans), k, _ptr(req_arg), _ptr(req_fn), nt)
         if pending < 0:
             raise RuntimeError("oracle rejected arguments")
         if pending == 0:
@@ -112,11 +216,11 @@ def evaluate(fn: str, width: int, x0, x1, backend: str = "dv", nthreads: int | N
         if k == mc:
             break
         with np.errstate(all="ignore"):
-            for f, ufunc in _LIBM32.items():
+            for f, ufunc in table.items():
                 sel = req_fn == f
                 if sel.any():
                     ans[sel, k] = ufunc(req_arg[sel])
-    raise RuntimeError("binary32 oracle did not converge (more libm calls than expected)")
+    raise RuntimeError("replay oracle did not converge (more libm calls than expected)")
 
 
 # ---- building blocks (known-answer tests) -----------------------------------

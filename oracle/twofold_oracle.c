@@ -236,9 +236,30 @@ static tf64 pexpm10_raw64(int dv, double x) {
     return t_add_d64(pexp0_raw64(dv, x), -1.0);
 }
 
+/* replayed libm (see header comment): call k of an element returns answer k,
+ * or records the (function, argument) request and poisons the element */
+typedef struct {
+    const double* ans; /* MAXCALLS answers of this element */
+    int n_known;
+    int k;
+    double* req_arg;
+    int8_t* req_fn;
+} L64;
+
 /* glibc libm behind CPython math, with _Libm64's exception mapping
- * (_fp.py:191-218): the C entry points already return inf/-inf/NaN there. */
-static double lm64(int f, double x) {
+ * (_fp.py:191-218): the C entry points already return inf/-inf/NaN there.
+ * L != NULL: replay mode (answers from the Python driver, e.g. the
+ * correctly rounded "CR-sim" libm). */
+static double lm64(L64* L, int f, double x) {
+    if (L) {
+        int k = L->k++;
+        if (k < L->n_known) return L->ans[k];
+        if (k == L->n_known) {
+            *L->req_arg = x;
+            *L->req_fn = (int8_t)f;
+        }
+        return NAN;
+    }
     switch (f) {
         case LM_EXP: return exp(x);
         case LM_EXPM1: return expm1(x);
@@ -248,20 +269,20 @@ static double lm64(int f, double x) {
 }
 
 /* ExpLog.texp (explog.py:265-275) */
-static tf64 texp64(int dv, double x0, double x1) {
+static tf64 texp64(int dv, L64* L, double x0, double x1) {
     tf64 v = pexp0_raw64(dv, x0);
-    double z0 = lm64(LM_EXP, x0);
+    double z0 = lm64(L, LM_EXP, x0);
     if (z0 == v.v && isinf(z0)) return mk64(z0, z0);
-    double t1 = lm64(LM_EXPM1, x1);
+    double t1 = lm64(L, LM_EXPM1, x1);
     return mk64(z0, (z0 * t1) + (v.e + (v.v - z0)));
 }
 
 /* ExpLog.texpm1 (explog.py:299-310) */
-static tf64 texpm1_64(int dv, double x0, double x1) {
+static tf64 texpm1_64(int dv, L64* L, double x0, double x1) {
     tf64 w = pexpm10_raw64(dv, x0);
-    double z0 = lm64(LM_EXPM1, x0);
+    double z0 = lm64(L, LM_EXPM1, x0);
     if (z0 == w.v && isinf(z0)) return mk64(z0, z0);
-    double t1 = lm64(LM_EXPM1, x1);
+    double t1 = lm64(L, LM_EXPM1, x1);
     double tail = w.e + (w.v - z0);
     return mk64(z0, ((z0 + 1.0) * t1) + tail);
 }
@@ -283,7 +304,7 @@ static double newton_log_z64(int dv, double z0, double z1, double r0) {
 }
 
 /* _log_core (explog.py:338-358) */
-static tf64 log_core64(int dv, double y0, double y1) {
+static tf64 log_core64(int dv, L64* L, double y0, double y1) {
     double z0, z1;
     int n = 0;
     if (y0 < 0.5 || y0 > 2.0) {
@@ -294,8 +315,8 @@ static tf64 log_core64(int dv, double y0, double y1) {
         z0 = y0;
         z1 = y1;
     }
-    double r0 = (y1 == 0.0 && z1 == 0.0) ? lm64(LM_LOG, z0)
-                                          : lm64(LM_LOG1P, (z0 - 1.0) + z1);
+    double r0 = (y1 == 0.0 && z1 == 0.0) ? lm64(L, LM_LOG, z0)
+                                          : lm64(L, LM_LOG1P, (z0 - 1.0) + z1);
     double r1 = newton_log_z64(dv, z0, z1, r0);
     if (fabs(r1) > NEWTON_TOL * fabs(r0) + NEWTON_TOL) {
         r0 = r0 + r1;
@@ -313,16 +334,16 @@ static tf64 correct64(tf64 core, double lib0) {
 }
 
 /* ExpLog.tlog (explog.py:394-399) */
-static tf64 tlog64(int dv, double y0, double y1) {
+static tf64 tlog64(int dv, L64* L, double y0, double y1) {
     tf64 v = renorm64(mk64(y0, y1));
-    tf64 core = log_core64(dv, v.v, v.e);
-    return correct64(core, lm64(LM_LOG, y0));
+    tf64 core = log_core64(dv, L, v.v, v.e);
+    return correct64(core, lm64(L, LM_LOG, y0));
 }
 
 /* ExpLog.tlogp (explog.py:389-392) */
-static tf64 tlogp64(int dv, tf64 y) {
-    tf64 core = log_core64(dv, y.v, y.e);
-    return correct64(core, lm64(LM_LOG, y.v));
+static tf64 tlogp64(int dv, L64* L, tf64 y) {
+    tf64 core = log_core64(dv, L, y.v, y.e);
+    return correct64(core, lm64(L, LM_LOG, y.v));
 }
 
 /* _newton_log1p_in_band (explog.py:410-424) */
@@ -340,8 +361,8 @@ static double newton_log1p64(int dv, double y0, double y1, double x0) {
 }
 
 /* _log1p_core (explog.py:426-432) */
-static tf64 log1p_core64(int dv, double y0, double y1) {
-    double x0 = lm64(LM_LOG1P, y0);
+static tf64 log1p_core64(int dv, L64* L, double y0, double y1) {
+    double x0 = lm64(L, LM_LOG1P, y0);
     double x1 = newton_log1p64(dv, y0, y1, x0);
     if (fabs(x1) > NEWTON_TOL * fabs(x0) + NEWTON_TOL) {
         x0 = x0 + x1;
@@ -351,27 +372,27 @@ static tf64 log1p_core64(int dv, double y0, double y1) {
 }
 
 /* _plog1p_raw (explog.py:440-444) */
-static tf64 plog1p_raw64(int dv, tf64 y) {
+static tf64 plog1p_raw64(int dv, L64* L, tf64 y) {
     if (y.v < -0.5 || y.v > 1.0) {
         tf64 w = renorm64(t_add_d64(y, 1.0));
-        return tlogp64(dv, w);
+        return tlogp64(dv, L, w);
     }
-    return log1p_core64(dv, y.v, y.e);
+    return log1p_core64(dv, L, y.v, y.e);
 }
 
 /* ExpLog.tlog1p (explog.py:464-467) */
-static tf64 tlog1p64(int dv, double y0, double y1) {
+static tf64 tlog1p64(int dv, L64* L, double y0, double y1) {
     tf64 v = renorm64(mk64(y0, y1));
-    tf64 core = plog1p_raw64(dv, v);
-    return correct64(core, lm64(LM_LOG1P, y0));
+    tf64 core = plog1p_raw64(dv, L, v);
+    return correct64(core, lm64(L, LM_LOG1P, y0));
 }
 
-static tf64 eval64(int fn, int dv, double x0, double x1) {
+static tf64 eval64(int fn, int dv, L64* L, double x0, double x1) {
     switch (fn) {
-        case FN_TEXP: return texp64(dv, x0, x1);
-        case FN_TEXPM1: return texpm1_64(dv, x0, x1);
-        case FN_TLOG: return tlog64(dv, x0, x1);
-        default: return tlog1p64(dv, x0, x1);
+        case FN_TEXP: return texp64(dv, L, x0, x1);
+        case FN_TEXPM1: return texpm1_64(dv, L, x0, x1);
+        case FN_TLOG: return tlog64(dv, L, x0, x1);
+        default: return tlog1p64(dv, L, x0, x1);
     }
 }
 
@@ -749,7 +770,7 @@ static void body64(void* p, int64_t lo, int64_t hi, int64_t* acc) {
     job64_t* j = (job64_t*)p;
     (void)acc;
     for (int64_t i = lo; i < hi; ++i) {
-        tf64 r = eval64(j->fn, j->dv, j->x0[i], j->x1[i]);
+        tf64 r = eval64(j->fn, j->dv, NULL, j->x0[i], j->x1[i]);
         j->z0[i] = r.v;
         j->z1[i] = r.e;
     }
@@ -761,6 +782,37 @@ EXPORT int tfo_eval_f64(int fn, int dv, const double* x0, const double* x1,
     job64_t j = {fn, dv, x0, x1, z0, z1};
     parallel_for(n, nthreads, body64, &j);
     return 0;
+}
+
+typedef struct {
+    int fn, dv, n_known;
+    const double *x0, *x1, *ans;
+    double *z0, *z1, *req_arg;
+    int8_t* req_fn;
+} job64r_t;
+
+static void body64r(void* p, int64_t lo, int64_t hi, int64_t* acc) {
+    job64r_t* j = (job64r_t*)p;
+    for (int64_t i = lo; i < hi; ++i) {
+        L64 L = {j->ans + (size_t)i * MAXCALLS, j->n_known, 0, j->req_arg + i, j->req_fn + i};
+        j->req_fn[i] = LM_NONE;
+        tf64 r = eval64(j->fn, j->dv, &L, j->x0[i], j->x1[i]);
+        if (j->req_fn[i] != LM_NONE) {
+            ++*acc;
+        } else {
+            j->z0[i] = r.v;
+            j->z1[i] = r.e;
+        }
+    }
+}
+
+/* binary64 with a replayed libm (answers supplied by the caller per pass) */
+EXPORT int64_t tfo_eval_f64_pass(int fn, int dv, const double* x0, const double* x1,
+                                 double* z0, double* z1, int64_t n, const double* ans,
+                                 int n_known, double* req_arg, int8_t* req_fn, int nthreads) {
+    if (fn < 0 || fn > 3 || n < 0 || n_known < 0 || n_known > MAXCALLS) return -1;
+    job64r_t j = {fn, dv, n_known, x0, x1, ans, z0, z1, req_arg, req_fn};
+    return parallel_for(n, nthreads, body64r, &j);
 }
 
 typedef struct {

@@ -282,14 +282,18 @@ TF_DEV bool fast_tlog(const STab<double>& tb, double y0, double y1, double& z0, 
   ok &= newton_quiet(r1, r0);
   TF<double> nl = t_mul_d_u(mk(P<double>::LN2_V, P<double>::LN2_E), (double)n);
   TF<double> core = t_add_u(mk(r0, r1), nl);
-  // d = (rh + rl) / y0 to ~2^-100 relative, then z0 = RN(core - d + d^2/2)
-  double rh = sub(v.v, y0), rl = v.e;
-  double rc = __drcp_rn(y0);
-  double q = mul(rh, rc);
-  double ql = mul(add(fmaop(-q, y0, rh), rl), rc);
-  TF<double> a = two_sum_u(core.v, -q);
-  double tail = add(add(a.e, core.e), sub(mul(mul(0.5, q), q), ql));
+  // renorm is error-free, so v - y0 == y1 exactly: log(y0) = log(v) - log1p(d),
+  // d = y1 / y0 = ys1 / ys0 (both scaled by 2^-n, ys0 in [0.5, 2]) to ~2^-100.
+  double sc = p2d_bf(-n);
+  double ys0 = mul(y0, sc), ys1 = mul(y1, sc);
+  double rc = rcp_nr(ys0);
+  double d0 = mul(ys1, rc);
+  double d1 = mul(fmaop(-d0, ys0, ys1), rc);
+  TF<double> a = two_sum_u(core.v, -d0);
+  double tail = add(add(a.e, core.e), sub(mul(mul(0.5, d0), d0), d1));
   z0 = add(a.v, tail);
+  double dl = sub(y0, 1.0);                          // exact near 1
+  if (abits(dl) <= NEAR1_64) z0 = log_near1(dl);
   z1 = add(core.e, sub(core.v, z0));                 // _correct (372-373)
   return ok;
 }
@@ -315,13 +319,16 @@ TF_DEV bool fast_tlog(const STab<float>& tb, float y0, float y1, float& z0, floa
   ok &= newton_quiet(r1, r0);
   TF<float> nl = t_mul_d_u(mk(P<float>::LN2_V, P<float>::LN2_E), (float)n);
   TF<float> core = t_add_u(mk(r0, r1), nl);
-  float rh = sub(v.v, y0), rl = v.e;
-  float rc = __frcp_rn(y0);
-  float q = mul(rh, rc);
-  float ql = mul(add(fmaop(-q, y0, rh), rl), rc);
-  TF<float> a = two_sum_u(core.v, -q);
-  float tail = add(add(a.e, core.e), sub(mul(mul(0.5f, q), q), ql));
+  float sc = p2f_bf(-n);
+  float ys0 = mul(y0, sc), ys1 = mul(y1, sc);
+  float rc = rcp_nr(ys0);
+  float d0 = mul(ys1, rc);
+  float d1 = mul(fmaop(-d0, ys0, ys1), rc);
+  TF<float> a = two_sum_u(core.v, -d0);
+  float tail = add(add(a.e, core.e), sub(mul(mul(0.5f, d0), d0), d1));
   z0 = add(a.v, tail);
+  float dl = sub(y0, 1.0f);
+  if (abits(dl) <= NEAR1_32) z0 = log_near1(dl);
   z1 = add(core.e, sub(core.v, z0));
   return ok;
 }
@@ -354,7 +361,7 @@ template <class T> TF_DEV bool fast_tlog1p(const STab<T>& tb, T y0, T y1, T& z0,
   T x1 = add(u.v, u.e);
   ok &= newton_quiet(x1, x0);
   bool tiny = D ? abits(y0) < B64_TINY54 : abits(y0) < (uint64_t)B32_TINY25;
-  T d = mul(add(sub(v.v, y0), v.e), D ? (T)__drcp_rn((double)add(T(1), y0)) : (T)__frcp_rn((float)add(T(1), y0)));
+  T d = mul(y1, rcp_nr(add(T(1), y0)));              // v - y0 == y1 exactly
   z0 = tiny ? y0 : add(x0, sub(x1, d));
   z1 = add(x1, sub(x0, z0));                          // _correct (372-373)
   return ok;

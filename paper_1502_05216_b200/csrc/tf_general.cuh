@@ -57,6 +57,20 @@ TF_DEV double ldexp_d(double x, int k) {
   return mul(x, p2d(k));
 }
 
+// reciprocal of x in [0.5, 2]: MUFU approximation + one Newton step (~2^-44)
+TF_DEV double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fmaop(-x, r, 1.0);
+  return fmaop(r, e, r);
+}
+TF_DEV float rcp_nr(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  float e = fmaop(-x, r, 1.0f);
+  return fmaop(r, e, r);
+}
+
 // ------------------------------------------------------------ exp cores
 // decompose_exp (expcore.py:35-50).  Python round() is ties-to-even == rint.
 template <class T> TF_DEV void decompose_exp(T x, int* m, int* n, T* y) {
@@ -310,10 +324,36 @@ template <class T> TF_DEV TF<T> log1p_core_c(T y0, T y1) {
   return mk(x0, x1);
 }
 
+// log(1 + d) for an exact |d| <= 2^-20 (resp. 2^-7 in binary32), correctly
+// rounded up to ~2^-40 ulp: d - d^2/2 with d^2 split exactly by an FMA, then
+// d^3/3 - d^4/4 + d^5/5.  Near y = 1 the log core's absolute accuracy is not
+// enough to round log(y) when d has few significant bits (y = 1 + k*2^-52),
+// where the exact value sits within d^3/3 of a rounding midpoint.
+TF_DEV double log_near1(double d) {
+  double q = mul(d, d);
+  double qe = fmaop(d, d, -q);
+  double c = mul(mul(q, d), fmaop(d, fmaop(d, 0.2, -0.25), 0x1.5555555555555p-2));
+  double lo = fmaop(-0.5, qe, c);
+  TF<double> s = fast_two_sum_u(d, mul(-0.5, q));
+  return add(s.v, add(s.e, lo));
+}
+TF_DEV float log_near1(float d) {
+  float q = mul(d, d);
+  float qe = fmaop(d, d, -q);
+  float c = mul(mul(q, d), fmaop(d, fmaop(d, 0.2f, -0.25f), 0x1.555556p-2f));
+  float lo = fmaop(-0.5f, qe, c);
+  TF<float> s = fast_two_sum_u(d, mul(-0.5f, q));
+  return add(s.v, add(s.e, lo));
+}
+constexpr uint64_t NEAR1_64 = 0x3eb0000000000000ull;  // 2^-20
+constexpr uint32_t NEAR1_32 = 0x3c000000u;            // 2^-7
+
 TF_DEV double log_cr(double y) {
   if (is_nan(y) || y < 0.0) return Lim<double>::qnan();
   if (y == 0.0) return -Lim<double>::inf();
   if (is_inf(y)) return y;
+  double d = sub(y, 1.0);
+  if (abits(d) <= NEAR1_64) return log_near1(d);   // y in [1 - 2^-20, 1 + 2^-20]: d exact
   TF<double> c = log_core_c(y, 0.0);
   return add(c.v, c.e);
 }
