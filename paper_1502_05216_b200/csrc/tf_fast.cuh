@@ -109,6 +109,76 @@ TF_DEV TF<float> taylor_expm1_u(float y) {    // N_m1=5
   return t_mul_u(t, mk(P<float>::INVF_V, P<float>::INVF_E));
 }
 
+// Rolled, lane-vectorised Taylor-Horner cores: one loop iteration performs
+// one twofold Horner step for all VW lanes, so the VW independent dependency
+// chains interleave while the hot code stays a few hundred bytes (a fully
+// unrolled 2-lane tlog1p was ~24 KB of SASS and stalled on instruction fetch).
+// Coefficients N!/k! come from constant memory with a warp-uniform index.
+template <int VW> TF_DEV void taylor_exp_v(const double (&y)[VW], TF<double> (&t)[VW]) {
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    double s = add(y[e], 12.0);
+    s = add(mul(s, y[e]), 132.0);
+    s = add(mul(s, y[e]), 1320.0);
+    t[e] = mk(s, 0.0);
+  }
+#pragma unroll 1
+  for (int k = 0; k < 9; ++k) {
+    const double c = c_texp64[k];
+#pragma unroll
+    for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_u(t[e], y[e]), c);
+  }
+}
+template <int VW> TF_DEV void taylor_exp_v(const float (&y)[VW], TF<float> (&t)[VW]) {
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    float s = add(y[e], 6.0f);
+    s = add(mul(s, y[e]), 30.0f);
+    t[e] = mk(s, 0.0f);
+  }
+#pragma unroll 1
+  for (int k = 0; k < 4; ++k) {
+    const float c = c_texp32[k];
+#pragma unroll
+    for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_u(t[e], y[e]), c);
+  }
+}
+template <int VW> TF_DEV void taylor_expm1_v(const double (&y)[VW], TF<double> (&t)[VW]) {
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    double s = add(y[e], 10.0);
+    s = add(mul(s, y[e]), 90.0);
+    s = add(mul(s, y[e]), 720.0);
+    t[e] = mk(s, 0.0);
+  }
+#pragma unroll 1
+  for (int k = 0; k < 6; ++k) {
+    const double c = c_texpm1_64[k];
+#pragma unroll
+    for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_u(t[e], y[e]), c);
+  }
+#pragma unroll
+  for (int e = 0; e < VW; ++e)
+    t[e] = t_mul_u(t_mul_d_u(t[e], y[e]), mk(P<double>::INVF_V, P<double>::INVF_E));
+}
+template <int VW> TF_DEV void taylor_expm1_v(const float (&y)[VW], TF<float> (&t)[VW]) {
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    float s = add(y[e], 5.0f);
+    s = add(mul(s, y[e]), 20.0f);
+    t[e] = mk(s, 0.0f);
+  }
+#pragma unroll 1
+  for (int k = 0; k < 2; ++k) {
+    const float c = c_texpm1_32[k];
+#pragma unroll
+    for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_u(t[e], y[e]), c);
+  }
+#pragma unroll
+  for (int e = 0; e < VW; ++e)
+    t[e] = t_mul_u(t_mul_d_u(t[e], y[e]), mk(P<float>::INVF_V, P<float>::INVF_E));
+}
+
 // decompose_exp via the magic constant: M = round-half-even(x * 32) in the
 // low word, y = x - M/32 exact (the reference's two ops give the same value).
 TF_DEV void decomp_exp_u(double x, int& m, int& n, double& y) {
@@ -140,14 +210,20 @@ TF_DEV void decomp_expm1_u(float x, int& n, float& y) {
   y = fmaop(sub(t, MG), -0.0078125f, x);
 }
 
-// pexpm10_raw, in-band branch only (expcore.py:142-146)
-template <class T> TF_DEV TF<T> pexpm10_inband_u(const STab<T>& tb, T x) {
-  int n;
-  T y;
-  decomp_expm1_u(x, n, y);
-  TF<T> c = tv<T>(tb.CM1[n - P<T>::CM1_LO]);
-  TF<T> t = taylor_expm1_u(y);
-  return t_add_u(t_mul_u(c, t), t_add_u(c, t));
+// pexpm10_raw, in-band branch only (expcore.py:142-146), VW lanes
+template <class T, int VW>
+TF_DEV void pexpm10_inband_v(const STab<T>& tb, const T (&x)[VW], TF<T> (&w)[VW]) {
+  T y[VW];
+  int n[VW];
+#pragma unroll
+  for (int e = 0; e < VW; ++e) decomp_expm1_u(x[e], n[e], y[e]);
+  TF<T> t[VW];
+  taylor_expm1_v<VW>(y, t);
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    TF<T> c = tv<T>(tb.CM1[n[e] - P<T>::CM1_LO]);
+    w[e] = t_add_u(t_mul_u(c, t[e]), t_add_u(c, t[e]));
+  }
 }
 
 // expm1(x1) for a tiny twofold tail: x + x^2/2 + x^3/6, correctly rounded
@@ -186,192 +262,233 @@ TF_DEV bool newton_quiet(float r1, float r0) {
 }
 
 // ================================================================ texp
-TF_DEV bool fast_texp(const STab<double>& tb, double x0, double x1, double& z0, double& z1) {
-  bool ok = abits(x0) <= (sgn(x0) ? B64_TEXP_NEG : B64_TEXP_POS);
-  ok &= abits(x1) < B64_X1_TINY;
-  x0 = ok ? x0 : 0.0;
-  int m, n;
-  double y;
-  decomp_exp_u(x0, m, n, y);
-  TF<double> t = taylor_exp_u(y);
-  TF<double> ct = t_mul_u(tv<double>(tb.C[n - P<double>::C_LO]), t);
-  TF<double> v = t_mul_u(tv<double>(tb.E[m - P<double>::E_LO]), ct);
-  z0 = add(v.v, v.e);                                   // CR exp(x0)
-  double t1 = t1_tiny(x1);
-  z1 = add(mul(z0, t1), add(v.e, sub(v.v, z0)));       // explog.py:275
-  return ok;
+template <int VW>
+TF_DEV void fast_texp(const STab<double>& tb, const double (&x0)[VW], const double (&x1)[VW],
+                      double (&z0)[VW], double (&z1)[VW], bool (&ok)[VW]) {
+  double y[VW];
+  int m[VW], n[VW];
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    ok[e] = abits(x0[e]) <= (sgn(x0[e]) ? B64_TEXP_NEG : B64_TEXP_POS) &&
+            abits(x1[e]) < B64_X1_TINY;
+    decomp_exp_u(ok[e] ? x0[e] : 0.0, m[e], n[e], y[e]);
+  }
+  TF<double> t[VW];
+  taylor_exp_v<VW>(y, t);
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    TF<double> ct = t_mul_u(tv<double>(tb.C[n[e] - P<double>::C_LO]), t[e]);
+    TF<double> v = t_mul_u(tv<double>(tb.E[m[e] - P<double>::E_LO]), ct);
+    z0[e] = add(v.v, v.e);                                      // CR exp(x0)
+    z1[e] = add(mul(z0[e], t1_tiny(x1[e])), add(v.e, sub(v.v, z0[e])));  // explog.py:275
+  }
 }
 
-TF_DEV bool fast_texp(const STab<float>& tb, float x0, float x1, float& z0, float& z1) {
-  bool ok = abits(x0) <= (sgn(x0) ? B32_TEXP_NEG : B32_TEXP_POS);
-  ok &= abits(x1) < B32_X1_TINY;
-  x0 = ok ? x0 : 0.0f;
-  int m, n;
-  float y;
-  decomp_exp_u(x0, m, n, y);
-  TF<float> t = taylor_exp_u(y);
-  TF<float> ct = t_mul_u(tv<float>(tb.C[n - P<float>::C_LO]), t);
-  TF<float> v = t_mul_u(tv<float>(tb.E[m - P<float>::E_LO]), ct);
-  // value part: near the subnormal range use the 2^64-scaled coarse table so
-  // the twofold keeps full precision (result is normal: exact unscaling)
-  bool scaled = m <= -35;  // e^(2m) < 2^-100: residuals would underflow
-  int is = scaled ? m - TF32_ESC_LO : 0;
-  TF<float> es = tv<float>(tb.ESC[is]);
-  TF<float> vs = t_mul_u(scaled ? es : tv<float>(tb.E[m - P<float>::E_LO]), ct);
-  z0 = mul(add(vs.v, vs.e), scaled ? 0x1p-64f : 1.0f);
-  float t1 = t1_tiny(x1);
-  z1 = add(mul(z0, t1), add(v.e, sub(v.v, z0)));
-  return ok;
+template <int VW>
+TF_DEV void fast_texp(const STab<float>& tb, const float (&x0)[VW], const float (&x1)[VW],
+                      float (&z0)[VW], float (&z1)[VW], bool (&ok)[VW]) {
+  float y[VW];
+  int m[VW], n[VW];
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    ok[e] = abits(x0[e]) <= (sgn(x0[e]) ? B32_TEXP_NEG : B32_TEXP_POS) &&
+            abits(x1[e]) < B32_X1_TINY;
+    decomp_exp_u(ok[e] ? x0[e] : 0.0f, m[e], n[e], y[e]);
+  }
+  TF<float> t[VW];
+  taylor_exp_v<VW>(y, t);
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    TF<float> ct = t_mul_u(tv<float>(tb.C[n[e] - P<float>::C_LO]), t[e]);
+    TF<float> ev = tv<float>(tb.E[m[e] - P<float>::E_LO]);
+    TF<float> v = t_mul_u(ev, ct);
+    // value part: near the subnormal range use the 2^64-scaled coarse table so
+    // the twofold keeps full precision (result is normal: exact unscaling)
+    bool scaled = m[e] <= -35;  // e^(2m) < 2^-100: residuals would underflow
+    TF<float> es = tv<float>(tb.ESC[scaled ? m[e] - TF32_ESC_LO : 0]);
+    TF<float> vs = t_mul_u(scaled ? es : ev, ct);
+    z0[e] = mul(add(vs.v, vs.e), scaled ? 0x1p-64f : 1.0f);
+    z1[e] = add(mul(z0[e], t1_tiny(x1[e])), add(v.e, sub(v.v, z0[e])));
+  }
 }
 
 // ============================================================== texpm1
 // binary64: the in-band core is the bulk (cfg 2: 99.5%)
-TF_DEV bool fast_texpm1(const STab<double>& tb, double x0, double x1, double& z0, double& z1) {
-  bool ok = abits(x0) <= B64_LN2;
-  ok &= abits(x1) < B64_X1_TINY;
-  x0 = ok ? x0 : 0.0;
-  TF<double> w = pexpm10_inband_u(tb, x0);
-  z0 = abits(x0) < B64_TINY54 ? x0 : add(w.v, w.e);    // CR expm1(x0)
-  double t1 = t1_tiny(x1);
-  double tail = add(w.e, sub(w.v, z0));
-  z1 = add(mul(add(z0, 1.0), t1), tail);               // explog.py:309-310
-  return ok;
+template <int VW>
+TF_DEV void fast_texpm1(const STab<double>& tb, const double (&x0)[VW], const double (&x1)[VW],
+                        double (&z0)[VW], double (&z1)[VW], bool (&ok)[VW]) {
+  double xs[VW];
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    ok[e] = abits(x0[e]) <= B64_LN2 && abits(x1[e]) < B64_X1_TINY;
+    xs[e] = ok[e] ? x0[e] : 0.0;
+  }
+  TF<double> w[VW];
+  pexpm10_inband_v<double, VW>(tb, xs, w);
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    z0[e] = abits(xs[e]) < B64_TINY54 ? xs[e] : add(w[e].v, w[e].e);   // CR expm1(x0)
+    double tail = add(w[e].e, sub(w[e].v, z0[e]));
+    z1[e] = add(mul(add(z0[e], 1.0), t1_tiny(x1[e])), tail);          // explog.py:309-310
+  }
 }
 
 // binary32: the pexp0 - 1 fallback is the bulk (cfg 4: 99.2%)
-TF_DEV bool fast_texpm1(const STab<float>& tb, float x0, float x1, float& z0, float& z1) {
-  uint32_t ax = abits(x0);
-  bool ok = ax > B32_LN2 && ax <= (sgn(x0) ? B32_LO : B32_TEXP_POS);
-  ok &= abits(x1) < B32_X1_TINY;
-  x0 = ok ? x0 : 1.0f;
-  int m, n;
-  float y;
-  decomp_exp_u(x0, m, n, y);
-  TF<float> t = taylor_exp_u(y);
-  TF<float> v = t_mul_u(tv<float>(tb.E[m - P<float>::E_LO]), t_mul_u(tv<float>(tb.C[n - P<float>::C_LO]), t));
-  TF<float> w = t_add_d_u(v, -1.0f);                    // expcore.py:147
-  z0 = add(w.v, w.e);
-  float t1 = t1_tiny(x1);
-  float tail = add(w.e, sub(w.v, z0));
-  z1 = add(mul(add(z0, 1.0f), t1), tail);
-  return ok;
+template <int VW>
+TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const float (&x1)[VW],
+                        float (&z0)[VW], float (&z1)[VW], bool (&ok)[VW]) {
+  float y[VW];
+  int m[VW], n[VW];
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    uint32_t ax = abits(x0[e]);
+    ok[e] = ax > B32_LN2 && ax <= (sgn(x0[e]) ? B32_LO : B32_TEXP_POS) &&
+            abits(x1[e]) < B32_X1_TINY;
+    decomp_exp_u(ok[e] ? x0[e] : 1.0f, m[e], n[e], y[e]);
+  }
+  TF<float> t[VW];
+  taylor_exp_v<VW>(y, t);
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    TF<float> v = t_mul_u(tv<float>(tb.E[m[e] - P<float>::E_LO]),
+                          t_mul_u(tv<float>(tb.C[n[e] - P<float>::C_LO]), t[e]));
+    TF<float> w = t_add_d_u(v, -1.0f);                          // expcore.py:147
+    z0[e] = add(w.v, w.e);
+    float tail = add(w.e, sub(w.v, z0[e]));
+    z1[e] = add(mul(add(z0[e], 1.0f), t1_tiny(x1[e])), tail);
+  }
 }
 
 // ================================================================= tlog
 // explog.py:394-399 -> _log_core (338-358) -> _newton_log_z (320-336),
 // with the value part replaced by a correctly rounded log(y0):
-//   log(y0) = log(v) - log1p(d),  d = (v - y0)/y0,  v = renorm(y0 + y1).
-TF_DEV bool fast_tlog(const STab<double>& tb, double y0, double y1, double& z0, double& z1) {
-  uint32_t eb0 = (uint32_t)hi32(y0) >> 20;          // sign|exponent
-  bool ok = eb0 - 1u < 2046u;                        // positive normal
-  ok &= abits(y1) == 0 || bexp(y1) + 50 <= (int)eb0;
-  y0 = ok ? y0 : 1.0;
-  y1 = ok ? y1 : 0.0;
-  TF<double> v = renorm_u(mk(y0, y1));
-  uint64_t vb = ubits(v.v);
-  bool band = vb >= B64_HALF && vb <= B64_TWO;
-  int n = band ? 0 : (int)(vb >> 52) - 1022;
-  double zc0 = band ? v.v : __longlong_as_double((vb & 0x800fffffffffffffull) | (1022ull << 52));
-  double zc1 = band ? v.e : (abits(v.e) == 0 ? 0.0 : mul(v.e, p2d_bf(-n)));
-  double r0 = seed_log1p(add(sub(zc0, 1.0), zc1));
-  ok &= abits(r0) <= B64_LN2;
-  TF<double> s = pexpm10_inband_u(tb, -r0);
-  TF<double> w = fast_two_sum_u(sub(zc0, 1.0), zc1);
-  TF<double> u = t_add_u(t_mul_u(mk(zc0, zc1), s), w);
-  double r1 = add(u.v, u.e);
-  ok &= newton_quiet(r1, r0);
-  TF<double> nl = t_mul_d_u(mk(P<double>::LN2_V, P<double>::LN2_E), (double)n);
-  TF<double> core = t_add_u(mk(r0, r1), nl);
-  // renorm is error-free, so v - y0 == y1 exactly: log(y0) = log(v) - log1p(d),
-  // d = y1 / y0 = ys1 / ys0 (both scaled by 2^-n, ys0 in [0.5, 2]) to ~2^-100.
-  double sc = p2d_bf(-n);
-  double ys0 = mul(y0, sc), ys1 = mul(y1, sc);
-  double rc = rcp_nr(ys0);
-  double d0 = mul(ys1, rc);
-  double d1 = mul(fmaop(-d0, ys0, ys1), rc);
-  TF<double> a = two_sum_u(core.v, -d0);
-  double tail = add(add(a.e, core.e), sub(mul(mul(0.5, d0), d0), d1));
-  z0 = add(a.v, tail);
-  double dl = sub(y0, 1.0);                          // exact near 1
-  if (abits(dl) <= NEAR1_64) z0 = log_near1(dl);
-  z1 = add(core.e, sub(core.v, z0));                 // _correct (372-373)
-  return ok;
-}
+//   log(y0) = log(v) - log1p(d),  d = y1 / y0  (renorm is error-free: v - y0 == y1),
+// and near 1 by the exact-d series (log_near1).
+template <class T> struct LogC;
+template <> struct LogC<double> {
+  static constexpr uint32_t NORM_SPAN = 2046u;
+  static constexpr int SMALL = 50, EBIAS = 1022;
+  static constexpr uint64_t HALF = B64_HALF, TWO = B64_TWO, LN2B = B64_LN2, NEAR1 = NEAR1_64;
+  TF_DEV static uint32_t eb(double x) { return (uint32_t)hi32(x) >> 20; }
+  TF_DEV static int n_of(double v) { return (int)(ubits(v) >> 52) - 1022; }
+  TF_DEV static double mant(double v) {
+    return __longlong_as_double((ubits(v) & 0x800fffffffffffffull) | (1022ull << 52));
+  }
+  TF_DEV static double p2(int k) { return p2d_bf(k); }
+};
+template <> struct LogC<float> {
+  static constexpr uint32_t NORM_SPAN = 254u;
+  static constexpr int SMALL = 21, EBIAS = 126;
+  static constexpr uint32_t HALF = B32_HALF, TWO = B32_TWO, LN2B = B32_LN2, NEAR1 = NEAR1_32;
+  TF_DEV static uint32_t eb(float x) { return ubits(x) >> 23; }
+  TF_DEV static int n_of(float v) { return (int)(ubits(v) >> 23) - 126; }
+  TF_DEV static float mant(float v) {
+    return __int_as_float((ubits(v) & 0x807fffffu) | (126u << 23));
+  }
+  TF_DEV static float p2(int k) { return p2f_bf(k); }
+};
 
-TF_DEV bool fast_tlog(const STab<float>& tb, float y0, float y1, float& z0, float& z1) {
-  uint32_t eb0 = ubits(y0) >> 23;
-  bool ok = eb0 - 1u < 254u;
-  ok &= abits(y1) == 0 || bexp(y1) + 21 <= (int)eb0;
-  y0 = ok ? y0 : 1.0f;
-  y1 = ok ? y1 : 0.0f;
-  TF<float> v = renorm_u(mk(y0, y1));
-  uint32_t vb = ubits(v.v);
-  bool band = vb >= B32_HALF && vb <= B32_TWO;
-  int n = band ? 0 : (int)(vb >> 23) - 126;
-  float zc0 = band ? v.v : __int_as_float((vb & 0x807fffffu) | (126u << 23));
-  float zc1 = band ? v.e : (abits(v.e) == 0 ? 0.0f : mul(v.e, p2f_bf(-n)));
-  float r0 = seed_log1p(add(sub(zc0, 1.0f), zc1));
-  ok &= abits(r0) <= B32_LN2;
-  TF<float> s = pexpm10_inband_u(tb, -r0);
-  TF<float> w = fast_two_sum_u(sub(zc0, 1.0f), zc1);
-  TF<float> u = t_add_u(t_mul_u(mk(zc0, zc1), s), w);
-  float r1 = add(u.v, u.e);
-  ok &= newton_quiet(r1, r0);
-  TF<float> nl = t_mul_d_u(mk(P<float>::LN2_V, P<float>::LN2_E), (float)n);
-  TF<float> core = t_add_u(mk(r0, r1), nl);
-  float sc = p2f_bf(-n);
-  float ys0 = mul(y0, sc), ys1 = mul(y1, sc);
-  float rc = rcp_nr(ys0);
-  float d0 = mul(ys1, rc);
-  float d1 = mul(fmaop(-d0, ys0, ys1), rc);
-  TF<float> a = two_sum_u(core.v, -d0);
-  float tail = add(add(a.e, core.e), sub(mul(mul(0.5f, d0), d0), d1));
-  z0 = add(a.v, tail);
-  float dl = sub(y0, 1.0f);
-  if (abits(dl) <= NEAR1_32) z0 = log_near1(dl);
-  z1 = add(core.e, sub(core.v, z0));
-  return ok;
+template <class T, int VW>
+TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW], T (&z0)[VW],
+                      T (&z1)[VW], bool (&ok)[VW]) {
+  using C = LogC<T>;
+  T y0[VW], y1[VW], zc0[VW], zc1[VW], r0[VW], mr0[VW];
+  int n[VW];
+  TF<T> v[VW];
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    uint32_t eb0 = C::eb(y0i[e]);                     // sign|exponent
+    ok[e] = eb0 - 1u < C::NORM_SPAN &&                 // positive normal y0
+            (abits(y1i[e]) == 0 || bexp(y1i[e]) + C::SMALL <= (int)eb0);
+    y0[e] = ok[e] ? y0i[e] : T(1);
+    y1[e] = ok[e] ? y1i[e] : T(0);
+    v[e] = renorm_u(mk(y0[e], y1[e]));
+    auto vb = ubits(v[e].v);
+    bool band = vb >= C::HALF && vb <= C::TWO;
+    n[e] = band ? 0 : C::n_of(v[e].v);
+    zc0[e] = band ? v[e].v : C::mant(v[e].v);
+    zc1[e] = band ? v[e].e : (abits(v[e].e) == 0 ? T(0) : mul(v[e].e, C::p2(-n[e])));
+    r0[e] = seed_log1p(add(sub(zc0[e], T(1)), zc1[e]));   // explog.py:346-349
+    ok[e] = ok[e] && abits(r0[e]) <= C::LN2B;
+    mr0[e] = -r0[e];
+  }
+  TF<T> s[VW];
+  pexpm10_inband_v<T, VW>(tb, mr0, s);
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    TF<T> w = fast_two_sum_u(sub(zc0[e], T(1)), zc1[e]);
+    TF<T> u = t_add_u(t_mul_u(mk(zc0[e], zc1[e]), s[e]), w);
+    T r1 = add(u.v, u.e);
+    ok[e] = ok[e] && newton_quiet(r1, r0[e]);
+    TF<T> nl = t_mul_d_u(mk(P<T>::LN2_V, P<T>::LN2_E), (T)n[e]);
+    TF<T> core = t_add_u(mk(r0[e], r1), nl);
+    T sc = C::p2(-n[e]);
+    T ys0 = mul(y0[e], sc), ys1 = mul(y1[e], sc);
+    T rc = rcp_nr(ys0);
+    T d0 = mul(ys1, rc);
+    T d1 = mul(fmaop(-d0, ys0, ys1), rc);
+    TF<T> a = two_sum_u(core.v, -d0);
+    T tail = add(add(a.e, core.e), sub(mul(mul(T(0.5), d0), d0), d1));
+    T zz = add(a.v, tail);
+    T dl = sub(y0[e], T(1));                          // exact near 1
+    if (abits(dl) <= C::NEAR1) zz = log_near1(dl);
+    z0[e] = zz;
+    z1[e] = add(core.e, sub(core.v, zz));            // _correct (372-373)
+  }
 }
 
 // =============================================================== tlog1p
 // In-band branch of _plog1p_raw (explog.py:440-444, 410-432); the
 // out-of-band branch (y0 < -1/2 or y0 > 1) goes to the exact path.
-// log1p(y0) = log1p(v) - log1p(d), d = (v - y0)/(1 + y0), |d| ~ 2^-53 |log1p(y0)|.
-template <class T> TF_DEV bool fast_tlog1p(const STab<T>& tb, T y0, T y1, T& z0, T& z1) {
+// log1p(y0) = log1p(v) - log1p(d), d = y1 / (1 + y0), |d| ~ 2^-53 |log1p(y0)|.
+template <class T, int VW>
+TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW], T (&z0)[VW],
+                        T (&z1)[VW], bool (&ok)[VW]) {
   constexpr bool D = sizeof(T) == 8;
-  const int SMALL = D ? 50 : 21;
-  bool ok = is_finite(y0) && (abits(y1) == 0 || bexp(y1) + SMALL <= bexp(y0));
-  y0 = ok ? y0 : T(0);
-  y1 = ok ? y1 : T(0);
-  TF<T> v = renorm_u(mk(y0, y1));
-  if (D) ok &= abits(v.v) <= (sgn(v.v) ? (uint64_t)B64_HALF : (uint64_t)B64_ONE);
-  else ok &= abits(v.v) <= (sgn(v.v) ? B32_HALF : B32_ONE);
-  v.v = ok ? v.v : T(0);
-  v.e = ok ? v.e : T(0);
-  T x0 = seed_log1p(v.v);
-  TF<T> s = pexpm10_inband_u(tb, T(-x0));
-  TF<T> u;
-  if (v.e == T(0)) {                                  // explog.py:418-420
-    TF<T> w = fast_two_sum_u(T(1), v.v);
-    u = t_add_d_u(t_mul_u(w, s), v.v);
-  } else {                                            // explog.py:421-423
-    TF<T> ys = t_mul_u(v, s);
-    u = t_add_u(t_add_u(ys, v), s);
+  T y0[VW], y1[VW], x0[VW], mx0[VW];
+  TF<T> v[VW];
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    ok[e] = is_finite(y0i[e]) &&
+            (abits(y1i[e]) == 0 || bexp(y1i[e]) + LogC<T>::SMALL <= bexp(y0i[e]));
+    y0[e] = ok[e] ? y0i[e] : T(0);
+    y1[e] = ok[e] ? y1i[e] : T(0);
+    v[e] = renorm_u(mk(y0[e], y1[e]));
+    if (D) ok[e] = ok[e] && abits(v[e].v) <= (sgn(v[e].v) ? (uint64_t)B64_HALF : (uint64_t)B64_ONE);
+    else ok[e] = ok[e] && abits(v[e].v) <= (sgn(v[e].v) ? B32_HALF : B32_ONE);
+    v[e].v = ok[e] ? v[e].v : T(0);
+    v[e].e = ok[e] ? v[e].e : T(0);
+    x0[e] = seed_log1p(v[e].v);
+    mx0[e] = -x0[e];
   }
-  T x1 = add(u.v, u.e);
-  ok &= newton_quiet(x1, x0);
-  bool tiny = D ? abits(y0) < B64_TINY54 : abits(y0) < (uint64_t)B32_TINY25;
-  T d = mul(y1, rcp_nr(add(T(1), y0)));              // v - y0 == y1 exactly
-  z0 = tiny ? y0 : add(x0, sub(x1, d));
-  z1 = add(x1, sub(x0, z0));                          // _correct (372-373)
-  return ok;
+  TF<T> s[VW];
+  pexpm10_inband_v<T, VW>(tb, mx0, s);
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    TF<T> u;
+    if (v[e].e == T(0)) {                              // explog.py:418-420
+      TF<T> w = fast_two_sum_u(T(1), v[e].v);
+      u = t_add_d_u(t_mul_u(w, s[e]), v[e].v);
+    } else {                                           // explog.py:421-423
+      TF<T> ys = t_mul_u(v[e], s[e]);
+      u = t_add_u(t_add_u(ys, v[e]), s[e]);
+    }
+    T x1 = add(u.v, u.e);
+    ok[e] = ok[e] && newton_quiet(x1, x0[e]);
+    bool tiny = D ? abits(y0[e]) < B64_TINY54 : abits(y0[e]) < (uint64_t)B32_TINY25;
+    T d = mul(y1[e], rcp_nr(add(T(1), y0[e])));       // v - y0 == y1 exactly
+    z0[e] = tiny ? y0[e] : add(x0[e], sub(x1, d));
+    z1[e] = add(x1, sub(x0[e], z0[e]));               // _correct (372-373)
+  }
 }
 
-template <class T, int FN> TF_DEV bool fast_eval(const STab<T>& tb, T x0, T x1, T& z0, T& z1) {
-  if (FN == FN_TEXP) return fast_texp(tb, x0, x1, z0, z1);
-  if (FN == FN_TEXPM1) return fast_texpm1(tb, x0, x1, z0, z1);
-  if (FN == FN_TLOG) return fast_tlog(tb, x0, x1, z0, z1);
-  return fast_tlog1p(tb, x0, x1, z0, z1);
+template <class T, int FN, int VW>
+TF_DEV void fast_eval(const STab<T>& tb, const T (&x0)[VW], const T (&x1)[VW], T (&z0)[VW],
+                      T (&z1)[VW], bool (&ok)[VW]) {
+  if constexpr (FN == FN_TEXP) fast_texp<VW>(tb, x0, x1, z0, z1, ok);
+  else if constexpr (FN == FN_TEXPM1) fast_texpm1<VW>(tb, x0, x1, z0, z1, ok);
+  else if constexpr (FN == FN_TLOG) fast_tlog<T, VW>(tb, x0, x1, z0, z1, ok);
+  else fast_tlog1p<T, VW>(tb, x0, x1, z0, z1, ok);
 }
 
 }  // namespace tf

@@ -91,25 +91,30 @@ template <class T> TF_DEV void decompose_expm1(T x, int* n, T* y) {
   *n = (int)M;
 }
 
+// Taylor coefficients N!/k! (params.py:48-59), constant memory, warp-uniform index
+__constant__ double c_texp64[9] = {11880.0, 95040.0, 665280.0, 3991680.0, 19958400.0,
+                                   79833600.0, 239500800.0, 479001600.0, 479001600.0};
+__constant__ double c_texpm1_64[6] = {5040.0, 30240.0, 151200.0, 604800.0, 1814400.0,
+                                      3628800.0};
+__constant__ float c_texp32[4] = {120.f, 360.f, 720.f, 720.f};
+__constant__ float c_texpm1_32[2] = {60.f, 120.f};
+
 // _seed + taylor_exp / taylor_expm1 (expcore.py:82-116)
 TF_DEV TF<double> taylor_exp_c(double y) {
   double s = add(y, 12.0);
   s = add(mul(s, y), 132.0);
   s = add(mul(s, y), 1320.0);
   TF<double> t = mk(s, 0.0);
-  const double c[9] = {11880.0, 95040.0, 665280.0, 3991680.0, 19958400.0,
-                       79833600.0, 239500800.0, 479001600.0, 479001600.0};
-#pragma unroll
-  for (int k = 0; k < 9; ++k) t = t_add_d_c(t_mul_d_c(t, y), c[k]);
+#pragma unroll 1
+  for (int k = 0; k < 9; ++k) t = t_add_d_c(t_mul_d_c(t, y), c_texp64[k]);
   return t;
 }
 TF_DEV TF<float> taylor_exp_c(float y) {
   float s = add(y, 6.0f);
   s = add(mul(s, y), 30.0f);
   TF<float> t = mk(s, 0.0f);
-  const float c[4] = {120.f, 360.f, 720.f, 720.f};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) t = t_add_d_c(t_mul_d_c(t, y), c[k]);
+#pragma unroll 1
+  for (int k = 0; k < 4; ++k) t = t_add_d_c(t_mul_d_c(t, y), c_texp32[k]);
   return t;
 }
 TF_DEV TF<double> taylor_expm1_c(double y) {
@@ -117,9 +122,8 @@ TF_DEV TF<double> taylor_expm1_c(double y) {
   s = add(mul(s, y), 90.0);
   s = add(mul(s, y), 720.0);
   TF<double> t = mk(s, 0.0);
-  const double c[6] = {5040.0, 30240.0, 151200.0, 604800.0, 1814400.0, 3628800.0};
-#pragma unroll
-  for (int k = 0; k < 6; ++k) t = t_add_d_c(t_mul_d_c(t, y), c[k]);
+#pragma unroll 1
+  for (int k = 0; k < 6; ++k) t = t_add_d_c(t_mul_d_c(t, y), c_texpm1_64[k]);
   t = t_mul_d_c(t, y);
   return t_mul_c(t, mk(P<double>::INVF_V, P<double>::INVF_E));
 }
@@ -127,9 +131,8 @@ TF_DEV TF<float> taylor_expm1_c(float y) {
   float s = add(y, 5.0f);
   s = add(mul(s, y), 20.0f);
   TF<float> t = mk(s, 0.0f);
-  const float c[2] = {60.f, 120.f};
-#pragma unroll
-  for (int k = 0; k < 2; ++k) t = t_add_d_c(t_mul_d_c(t, y), c[k]);
+#pragma unroll 1
+  for (int k = 0; k < 2; ++k) t = t_add_d_c(t_mul_d_c(t, y), c_texpm1_32[k]);
   t = t_mul_d_c(t, y);
   return t_mul_c(t, mk(P<float>::INVF_V, P<float>::INVF_E));
 }

@@ -97,11 +97,10 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
 #pragma unroll
       for (int e = 0; e < VW; ++e) { a[e] = T(0); b[e] = T(0); }
     }
+    bool ok[VW];
+    fast_eval<T, FN, VW>(tb, a, b, r0, r1, ok);
 #pragma unroll
-    for (int e = 0; e < VW; ++e) {
-      bool ok = fast_eval<T, FN>(tb, a[e], b[e], r0[e], r1[e]);
-      rare[e] = valid && (!ok || force);
-    }
+    for (int e = 0; e < VW; ++e) rare[e] = valid && (!ok[e] || force);
     if (valid) {
       st<T, VW>(z0, vi, r0);
       st<T, VW>(z1, vi, r1);
