@@ -55,6 +55,22 @@ TF_DEV void st(T* p, uint64_t vi, const T (&a)[VW]) {
   }
 }
 
+// ---- asynchronous global -> shared staging (LDGSTS), one 16 B vector per
+// thread and array per stage: the loads of iteration i+STAGES-1 are in flight
+// while iteration i computes, so DRAM latency hides behind FP64 work even at
+// the modest occupancy the 64-register fast paths allow.  Each thread reads
+// back only the slots it filled itself, so no block barrier is needed.
+TF_DEV void cp_async16(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid ? 16 : 0;  // src-size 0: zero-fill, nothing read
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz)
+               : "memory");
+}
+TF_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N> TF_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // Evaluate the queued rare elements q[0..cnt) (cnt <= 32) with the exact path.
 template <class T, int FN>
 TF_DEV void drain(const uint32_t* q, int cnt, const T* __restrict__ x0, const T* __restrict__ x1,
@@ -73,8 +89,11 @@ __global__ void __launch_bounds__(BLOCK, 4)
 k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
        T* __restrict__ z1, uint32_t n, int flags) {
   constexpr int QCAP = 32 + 32 * VW;
+  constexpr int STAGES = 3;
+  constexpr bool ASYNC = VW * sizeof(T) == 16;
   __shared__ STab<T> tb;
   __shared__ uint32_t qs[WARPS][QCAP];
+  __shared__ __align__(16) T stg[ASYNC ? STAGES : 1][2][BLOCK][VW];
   load_tables(tb);
   __syncthreads();
 
@@ -85,17 +104,45 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   int qn = 0;  // warp-uniform
   const uint64_t nvec = n / VW;
   const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
-  for (uint64_t base = (uint64_t)blockIdx.x * BLOCK + warp * 32; base < nvec; base += stride) {
+  const uint64_t first = (uint64_t)blockIdx.x * BLOCK + warp * 32;
+  if constexpr (ASYNC) {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      uint64_t vi = first + s * stride + lane;
+      bool v = vi < nvec;
+      cp_async16(stg[s][0][threadIdx.x], x0 + (v ? vi * VW : 0), v);
+      cp_async16(stg[s][1][threadIdx.x], x1 + (v ? vi * VW : 0), v);
+      cp_async_commit();
+    }
+  }
+  int it = 0;
+  for (uint64_t base = first; base < nvec; base += stride, ++it) {
     const uint64_t vi = base + lane;
     const bool valid = vi < nvec;
     T a[VW], b[VW], r0[VW], r1[VW];
     bool rare[VW];
-    if (valid) {
-      ld<T, VW>(x0, vi, a);
-      ld<T, VW>(x1, vi, b);
-    } else {
+    if constexpr (ASYNC) {
+      uint64_t pv = base + (STAGES - 1) * stride + lane;
+      bool pvalid = pv < nvec;
+      int ps = (it + STAGES - 1) % STAGES;
+      cp_async16(stg[ps][0][threadIdx.x], x0 + (pvalid ? pv * VW : 0), pvalid);
+      cp_async16(stg[ps][1][threadIdx.x], x1 + (pvalid ? pv * VW : 0), pvalid);
+      cp_async_commit();
+      cp_async_wait<STAGES - 1>();
+      const int cs = it % STAGES;
 #pragma unroll
-      for (int e = 0; e < VW; ++e) { a[e] = T(0); b[e] = T(0); }
+      for (int e = 0; e < VW; ++e) {
+        a[e] = stg[cs][0][threadIdx.x][e];
+        b[e] = stg[cs][1][threadIdx.x][e];
+      }
+    } else {
+      if (valid) {
+        ld<T, VW>(x0, vi, a);
+        ld<T, VW>(x1, vi, b);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) { a[e] = T(0); b[e] = T(0); }
+      }
     }
     bool ok[VW];
     fast_eval<T, FN, VW>(tb, a, b, r0, r1, ok);
@@ -130,6 +177,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
       __syncwarp();
     }
   }
+  if constexpr (ASYNC) cp_async_wait<0>();
   // ragged tail (n % VW elements): exact path, first warp of block 0
   const uint32_t tail = (uint32_t)(n - nvec * VW);
   if (blockIdx.x == 0 && warp == 0 && tail) {
