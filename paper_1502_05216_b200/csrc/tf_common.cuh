@@ -39,6 +39,12 @@ TF_DEV bool is_nan(double x) { return abits(x) > 0x7ff0000000000000ull; }
 TF_DEV bool is_nan(float x) { return abits(x) > 0x7f800000u; }
 TF_DEV bool is_inf(double x) { return abits(x) == 0x7ff0000000000000ull; }
 TF_DEV bool is_inf(float x) { return abits(x) == 0x7f800000u; }
+// |x| high word / zero test on the integer pipe (a 64-bit "& 0x7fff..." mask
+// is pattern-matched into DADD |x|, which would burn an FP64 pipe slot)
+TF_DEV uint32_t ahi(double x) { return (uint32_t)__double2hiint(x) & 0x7fffffffu; }
+TF_DEV uint32_t ahi(float x) { return __float_as_uint(x) & 0x7fffffffu; }
+TF_DEV bool zbits(double x) { return ((__double2hiint(x) & 0x7fffffff) | __double2loint(x)) == 0; }
+TF_DEV bool zbits(float x) { return (__float_as_uint(x) & 0x7fffffffu) == 0; }
 // biased exponent field
 TF_DEV int bexp(double x) { return (hi32(x) >> 20) & 0x7ff; }
 TF_DEV int bexp(float x) { return (int)((ubits(x) >> 23) & 0xff); }

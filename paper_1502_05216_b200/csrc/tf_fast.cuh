@@ -63,6 +63,16 @@ constexpr uint32_t B32_HALF = 0x3f000000u;
 constexpr uint32_t B32_ONE = 0x3f800000u;
 constexpr uint32_t B32_TWO = 0x40000000u;
 
+// the same bands as high words (conservative where marked "<")
+constexpr uint32_t H64_TEXP_POS = 0x40862e14u;  // |x| <= 709.76...
+constexpr uint32_t H64_TEXP_NEG = 0x40857800u;  // |x| <= 687.0...
+constexpr uint32_t H64_X1_TINY = 0x3e400000u;   // < 2^-27
+constexpr uint32_t H64_TINY54 = 0x3c900000u;    // < 2^-54
+constexpr uint32_t H64_LN2 = 0x3fe62e42u;       // < LN2 (slightly conservative)
+constexpr uint32_t H64_HALF = 0x3fe00000u;      // < 0.5
+constexpr uint32_t H64_ONE = 0x3ff00000u;       // < 1
+constexpr uint32_t H64_NEAR1 = 0x3eb00000u;     // < 2^-20
+
 TF_DEV bool sgn(double x) { return hi32(x) < 0; }
 TF_DEV bool sgn(float x) { return (int)ubits(x) < 0; }
 
@@ -122,7 +132,7 @@ template <int VW> TF_DEV void taylor_exp_v(const double (&y)[VW], TF<double> (&t
     s = add(mul(s, y[e]), 1320.0);
     t[e] = mk(s, 0.0);
   }
-#pragma unroll 1
+#pragma unroll 3
   for (int k = 0; k < 9; ++k) {
     const double c = c_texp64[k];
 #pragma unroll
@@ -136,7 +146,7 @@ template <int VW> TF_DEV void taylor_exp_v(const float (&y)[VW], TF<float> (&t)[
     s = add(mul(s, y[e]), 30.0f);
     t[e] = mk(s, 0.0f);
   }
-#pragma unroll 1
+#pragma unroll
   for (int k = 0; k < 4; ++k) {
     const float c = c_texp32[k];
 #pragma unroll
@@ -151,7 +161,7 @@ template <int VW> TF_DEV void taylor_expm1_v(const double (&y)[VW], TF<double> (
     s = add(mul(s, y[e]), 720.0);
     t[e] = mk(s, 0.0);
   }
-#pragma unroll 1
+#pragma unroll 3
   for (int k = 0; k < 6; ++k) {
     const double c = c_texpm1_64[k];
 #pragma unroll
@@ -168,7 +178,7 @@ template <int VW> TF_DEV void taylor_expm1_v(const float (&y)[VW], TF<float> (&t
     s = add(mul(s, y[e]), 20.0f);
     t[e] = mk(s, 0.0f);
   }
-#pragma unroll 1
+#pragma unroll
   for (int k = 0; k < 2; ++k) {
     const float c = c_texpm1_32[k];
 #pragma unroll
@@ -230,12 +240,12 @@ TF_DEV void pexpm10_inband_v(const STab<T>& tb, const T (&x)[VW], TF<T> (&w)[VW]
 // (|x| < 2^-27 for binary64, < 2^-16 for binary32 via binary64).
 TF_DEV double t1_tiny(double x) {
   double r = fmaop(mul(x, x), fmaop(x, 0x1.5555555555555p-3, 0.5), x);
-  return abits(x) == 0 ? x : r;
+  return zbits(x) ? x : r;
 }
 TF_DEV float t1_tiny(float x) {
   double d = (double)x;
   double r = fmaop(mul(d, d), fmaop(d, 0x1.5555555555555p-3, 0.5), d);
-  return abits(x) == 0 ? x : __double2float_rn(r);
+  return zbits(x) ? x : __double2float_rn(r);
 }
 
 // 2^k for k in [-1074, 1023], branch-free
@@ -269,8 +279,8 @@ TF_DEV void fast_texp(const STab<double>& tb, const double (&x0)[VW], const doub
   int m[VW], n[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    ok[e] = abits(x0[e]) <= (sgn(x0[e]) ? B64_TEXP_NEG : B64_TEXP_POS) &&
-            abits(x1[e]) < B64_X1_TINY;
+    ok[e] = ahi(x0[e]) <= (sgn(x0[e]) ? H64_TEXP_NEG : H64_TEXP_POS) &&
+            ahi(x1[e]) < H64_X1_TINY;
     decomp_exp_u(ok[e] ? x0[e] : 0.0, m[e], n[e], y[e]);
   }
   TF<double> t[VW];
@@ -291,8 +301,8 @@ TF_DEV void fast_texp(const STab<float>& tb, const float (&x0)[VW], const float 
   int m[VW], n[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    ok[e] = abits(x0[e]) <= (sgn(x0[e]) ? B32_TEXP_NEG : B32_TEXP_POS) &&
-            abits(x1[e]) < B32_X1_TINY;
+    ok[e] = ahi(x0[e]) <= (sgn(x0[e]) ? B32_TEXP_NEG : B32_TEXP_POS) &&
+            ahi(x1[e]) < B32_X1_TINY;
     decomp_exp_u(ok[e] ? x0[e] : 0.0f, m[e], n[e], y[e]);
   }
   TF<float> t[VW];
@@ -320,14 +330,14 @@ TF_DEV void fast_texpm1(const STab<double>& tb, const double (&x0)[VW], const do
   double xs[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    ok[e] = abits(x0[e]) <= B64_LN2 && abits(x1[e]) < B64_X1_TINY;
+    ok[e] = ahi(x0[e]) < H64_LN2 && ahi(x1[e]) < H64_X1_TINY;
     xs[e] = ok[e] ? x0[e] : 0.0;
   }
   TF<double> w[VW];
   pexpm10_inband_v<double, VW>(tb, xs, w);
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    z0[e] = abits(xs[e]) < B64_TINY54 ? xs[e] : add(w[e].v, w[e].e);   // CR expm1(x0)
+    z0[e] = ahi(xs[e]) < H64_TINY54 ? xs[e] : add(w[e].v, w[e].e);   // CR expm1(x0)
     double tail = add(w[e].e, sub(w[e].v, z0[e]));
     z1[e] = add(mul(add(z0[e], 1.0), t1_tiny(x1[e])), tail);          // explog.py:309-310
   }
@@ -341,9 +351,9 @@ TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const floa
   int m[VW], n[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    uint32_t ax = abits(x0[e]);
+    uint32_t ax = ahi(x0[e]);
     ok[e] = ax > B32_LN2 && ax <= (sgn(x0[e]) ? B32_LO : B32_TEXP_POS) &&
-            abits(x1[e]) < B32_X1_TINY;
+            ahi(x1[e]) < B32_X1_TINY;
     decomp_exp_u(ok[e] ? x0[e] : 1.0f, m[e], n[e], y[e]);
   }
   TF<float> t[VW];
@@ -368,7 +378,8 @@ template <class T> struct LogC;
 template <> struct LogC<double> {
   static constexpr uint32_t NORM_SPAN = 2046u;
   static constexpr int SMALL = 50, EBIAS = 1022;
-  static constexpr uint64_t HALF = B64_HALF, TWO = B64_TWO, LN2B = B64_LN2, NEAR1 = NEAR1_64;
+  static constexpr uint64_t HALF = B64_HALF, TWO = B64_TWO;
+  static constexpr uint32_t LN2H = H64_LN2, NEAR1H = H64_NEAR1;
   TF_DEV static uint32_t eb(double x) { return (uint32_t)hi32(x) >> 20; }
   TF_DEV static int n_of(double v) { return (int)(ubits(v) >> 52) - 1022; }
   TF_DEV static double mant(double v) {
@@ -379,7 +390,8 @@ template <> struct LogC<double> {
 template <> struct LogC<float> {
   static constexpr uint32_t NORM_SPAN = 254u;
   static constexpr int SMALL = 21, EBIAS = 126;
-  static constexpr uint32_t HALF = B32_HALF, TWO = B32_TWO, LN2B = B32_LN2, NEAR1 = NEAR1_32;
+  static constexpr uint32_t HALF = B32_HALF, TWO = B32_TWO;
+  static constexpr uint32_t LN2H = B32_LN2 + 1u, NEAR1H = NEAR1_32 + 1u;
   TF_DEV static uint32_t eb(float x) { return ubits(x) >> 23; }
   TF_DEV static int n_of(float v) { return (int)(ubits(v) >> 23) - 126; }
   TF_DEV static float mant(float v) {
@@ -399,7 +411,7 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
   for (int e = 0; e < VW; ++e) {
     uint32_t eb0 = C::eb(y0i[e]);                     // sign|exponent
     ok[e] = eb0 - 1u < C::NORM_SPAN &&                 // positive normal y0
-            (abits(y1i[e]) == 0 || bexp(y1i[e]) + C::SMALL <= (int)eb0);
+            (zbits(y1i[e]) || bexp(y1i[e]) + C::SMALL <= (int)eb0);
     y0[e] = ok[e] ? y0i[e] : T(1);
     y1[e] = ok[e] ? y1i[e] : T(0);
     v[e] = renorm_u(mk(y0[e], y1[e]));
@@ -407,9 +419,9 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     bool band = vb >= C::HALF && vb <= C::TWO;
     n[e] = band ? 0 : C::n_of(v[e].v);
     zc0[e] = band ? v[e].v : C::mant(v[e].v);
-    zc1[e] = band ? v[e].e : (abits(v[e].e) == 0 ? T(0) : mul(v[e].e, C::p2(-n[e])));
+    zc1[e] = band ? v[e].e : (zbits(v[e].e) ? T(0) : mul(v[e].e, C::p2(-n[e])));
     r0[e] = seed_log1p(add(sub(zc0[e], T(1)), zc1[e]));   // explog.py:346-349
-    ok[e] = ok[e] && abits(r0[e]) <= C::LN2B;
+    ok[e] = ok[e] && ahi(r0[e]) < C::LN2H;
     mr0[e] = -r0[e];
   }
   TF<T> s[VW];
@@ -431,7 +443,7 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     T tail = add(add(a.e, core.e), sub(mul(mul(T(0.5), d0), d0), d1));
     T zz = add(a.v, tail);
     T dl = sub(y0[e], T(1));                          // exact near 1
-    if (abits(dl) <= C::NEAR1) zz = log_near1(dl);
+    if (ahi(dl) < C::NEAR1H) zz = log_near1(dl);
     z0[e] = zz;
     z1[e] = add(core.e, sub(core.v, zz));            // _correct (372-373)
   }
@@ -450,12 +462,12 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
     ok[e] = is_finite(y0i[e]) &&
-            (abits(y1i[e]) == 0 || bexp(y1i[e]) + LogC<T>::SMALL <= bexp(y0i[e]));
+            (zbits(y1i[e]) || bexp(y1i[e]) + LogC<T>::SMALL <= bexp(y0i[e]));
     y0[e] = ok[e] ? y0i[e] : T(0);
     y1[e] = ok[e] ? y1i[e] : T(0);
     v[e] = renorm_u(mk(y0[e], y1[e]));
-    if (D) ok[e] = ok[e] && abits(v[e].v) <= (sgn(v[e].v) ? (uint64_t)B64_HALF : (uint64_t)B64_ONE);
-    else ok[e] = ok[e] && abits(v[e].v) <= (sgn(v[e].v) ? B32_HALF : B32_ONE);
+    if (D) ok[e] = ok[e] && ahi(v[e].v) < (sgn(v[e].v) ? H64_HALF : H64_ONE);
+    else ok[e] = ok[e] && ahi(v[e].v) <= (sgn(v[e].v) ? B32_HALF : B32_ONE);
     v[e].v = ok[e] ? v[e].v : T(0);
     v[e].e = ok[e] ? v[e].e : T(0);
     x0[e] = seed_log1p(v[e].v);
@@ -475,7 +487,7 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
     }
     T x1 = add(u.v, u.e);
     ok[e] = ok[e] && newton_quiet(x1, x0[e]);
-    bool tiny = D ? abits(y0[e]) < B64_TINY54 : abits(y0[e]) < (uint64_t)B32_TINY25;
+    bool tiny = ahi(y0[e]) < (D ? H64_TINY54 : B32_TINY25);
     T d = mul(y1[e], rcp_nr(add(T(1), y0[e])));       // v - y0 == y1 exactly
     z0[e] = tiny ? y0[e] : add(x0[e], sub(x1, d));
     z1[e] = add(x1, sub(x0[e], z0[e]));               // _correct (372-373)

@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(BLOCK, 4)
 k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
        T* __restrict__ z1, uint32_t n, int flags) {
   constexpr int QCAP = 32 + 32 * VW;
-  constexpr int STAGES = 3;
+  constexpr int STAGES = 2;
   constexpr bool ASYNC = VW * sizeof(T) == 16;
   __shared__ STab<T> tb;
   __shared__ uint32_t qs[WARPS][QCAP];
@@ -102,39 +102,36 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   const bool force = flags & TF_FLAG_FORCE_EXACT;
   const bool count = flags & TF_FLAG_COUNT_EXACT;
   int qn = 0;  // warp-uniform
-  const uint64_t nvec = n / VW;
-  const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
-  const uint64_t first = (uint64_t)blockIdx.x * BLOCK + warp * 32;
+  // 32-bit index arithmetic: the host splits launches at 2^31 elements
+  const uint32_t nvec = n / VW;
+  const uint32_t stride = gridDim.x * BLOCK;
+  const uint32_t first = blockIdx.x * BLOCK + warp * 32;
   if constexpr (ASYNC) {
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-      uint64_t vi = first + s * stride + lane;
-      bool v = vi < nvec;
-      cp_async16(stg[s][0][threadIdx.x], x0 + (v ? vi * VW : 0), v);
-      cp_async16(stg[s][1][threadIdx.x], x1 + (v ? vi * VW : 0), v);
-      cp_async_commit();
-    }
+    uint32_t vi = first + lane;
+    bool v = vi < nvec;
+    cp_async16(stg[0][0][threadIdx.x], x0 + (v ? vi * VW : 0u), v);
+    cp_async16(stg[0][1][threadIdx.x], x1 + (v ? vi * VW : 0u), v);
+    cp_async_commit();
   }
-  int it = 0;
-  for (uint64_t base = first; base < nvec; base += stride, ++it) {
-    const uint64_t vi = base + lane;
+  int cs = 0;
+  for (uint32_t base = first; base < nvec; base += stride) {
+    const uint32_t vi = base + lane;
     const bool valid = vi < nvec;
     T a[VW], b[VW], r0[VW], r1[VW];
     bool rare[VW];
     if constexpr (ASYNC) {
-      uint64_t pv = base + (STAGES - 1) * stride + lane;
+      uint32_t pv = vi + stride;
       bool pvalid = pv < nvec;
-      int ps = (it + STAGES - 1) % STAGES;
-      cp_async16(stg[ps][0][threadIdx.x], x0 + (pvalid ? pv * VW : 0), pvalid);
-      cp_async16(stg[ps][1][threadIdx.x], x1 + (pvalid ? pv * VW : 0), pvalid);
+      cp_async16(stg[cs ^ 1][0][threadIdx.x], x0 + (pvalid ? pv * VW : 0u), pvalid);
+      cp_async16(stg[cs ^ 1][1][threadIdx.x], x1 + (pvalid ? pv * VW : 0u), pvalid);
       cp_async_commit();
-      cp_async_wait<STAGES - 1>();
-      const int cs = it % STAGES;
+      cp_async_wait<1>();
 #pragma unroll
       for (int e = 0; e < VW; ++e) {
         a[e] = stg[cs][0][threadIdx.x][e];
         b[e] = stg[cs][1][threadIdx.x][e];
       }
+      cs ^= 1;
     } else {
       if (valid) {
         ld<T, VW>(x0, vi, a);
@@ -156,7 +153,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
     for (int e = 0; e < VW; ++e) {
       unsigned mask = __ballot_sync(0xffffffffu, rare[e]);
       if (mask) {
-        if (rare[e]) q[qn + __popc(mask & ((1u << lane) - 1u))] = (uint32_t)(vi * VW + e);
+        if (rare[e]) q[qn + __popc(mask & ((1u << lane) - 1u))] = vi * VW + e;
         qn += __popc(mask);
       }
     }
@@ -179,7 +176,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   }
   if constexpr (ASYNC) cp_async_wait<0>();
   // ragged tail (n % VW elements): exact path, first warp of block 0
-  const uint32_t tail = (uint32_t)(n - nvec * VW);
+  const uint32_t tail = n - nvec * VW;
   if (blockIdx.x == 0 && warp == 0 && tail) {
     if (lane < (int)tail) q[qn + lane] = (uint32_t)(nvec * VW + lane);
     qn += tail;
