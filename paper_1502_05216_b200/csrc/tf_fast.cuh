@@ -27,6 +27,7 @@ template <class T> struct STab {
   typename V2<T>::t C[P<T>::C_N];
   typename V2<T>::t CM1[P<T>::CM1_N];
   typename V2<T>::t ESC[sizeof(T) == 8 ? TF64_ESC_COUNT : TF32_ESC_COUNT];
+  typename V2<T>::t SEED[TF64_SEED_COUNT];
 };
 
 template <class T> __device__ void load_tables(STab<T>& s) {
@@ -39,6 +40,9 @@ template <class T> __device__ void load_tables(STab<T>& s) {
   for (int i = threadIdx.x; i < P<T>::C_N; i += blockDim.x) { s.C[i].x = srcC[2 * i]; s.C[i].y = srcC[2 * i + 1]; }
   for (int i = threadIdx.x; i < P<T>::CM1_N; i += blockDim.x) { s.CM1[i].x = srcM[2 * i]; s.CM1[i].y = srcM[2 * i + 1]; }
   for (int i = threadIdx.x; i < NS; i += blockDim.x) { s.ESC[i].x = srcS[2 * i]; s.ESC[i].y = srcS[2 * i + 1]; }
+  const typename V2<T>::t* srcD =
+      sizeof(T) == 8 ? (const typename V2<T>::t*)g_SEED64 : (const typename V2<T>::t*)g_SEED32;
+  for (int i = threadIdx.x; i < TF64_SEED_COUNT; i += blockDim.x) s.SEED[i] = srcD[i];
 }
 
 template <class T, class V> TF_DEV TF<T> tv(V a) { return mk(a.x, a.y); }
@@ -420,7 +424,8 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     n[e] = band ? 0 : C::n_of(v[e].v);
     zc0[e] = band ? v[e].v : C::mant(v[e].v);
     zc1[e] = band ? v[e].e : (zbits(v[e].e) ? T(0) : mul(v[e].e, C::p2(-n[e])));
-    r0[e] = seed_log1p(add(sub(zc0[e], T(1)), zc1[e]));   // explog.py:346-349
+    r0[e] = seed_log1p_t(add(sub(zc0[e], T(1)), zc1[e]),      // explog.py:346-349
+                         [&](int i) { return tb.SEED[i]; });
     ok[e] = ok[e] && ahi(r0[e]) < C::LN2H;
     mr0[e] = -r0[e];
   }
@@ -470,7 +475,7 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
     else ok[e] = ok[e] && ahi(v[e].v) <= (sgn(v[e].v) ? B32_HALF : B32_ONE);
     v[e].v = ok[e] ? v[e].v : T(0);
     v[e].e = ok[e] ? v[e].e : T(0);
-    x0[e] = seed_log1p(v[e].v);
+    x0[e] = seed_log1p_t(v[e].v, [&](int i) { return tb.SEED[i]; });   // explog.py:427
     mx0[e] = -x0[e];
   }
   TF<T> s[VW];

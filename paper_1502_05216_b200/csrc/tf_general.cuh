@@ -25,6 +25,8 @@ __device__ const float g_E32[] = {TF32_E_INIT};
 __device__ const float g_C32[] = {TF32_C_INIT};
 __device__ const float g_CM132[] = {TF32_CM1_INIT};
 __device__ const float g_ESC32[] = {TF32_ESC_INIT};
+__device__ const double2 g_SEED64[] = {TF64_SEED_INIT};
+__device__ const float2 g_SEED32[] = {TF32_SEED_INIT};
 
 template <class T> struct GT;
 template <> struct GT<double> {
@@ -253,8 +255,63 @@ TF_DEV float expm1_cr(float x) {
 // ------------------------------------------------------------ log cores
 // Newton seeds: the reference calls libm log / log1p (explog.py:347-349,427);
 // CUDA's are within 1 ulp and the Newton step absorbs the difference.
-TF_DEV double seed_log1p(double x) { return log1p(x); }
-TF_DEV float seed_log1p(float x) { return log1pf(x); }
+//
+// The seed is a compact table-driven log1p (relative error ~2^-52 / 2^-23,
+// 13 FP64 ops, no branches) over a in [-1/2, 1], where every caller's argument
+// lies: f = 1 + a split exactly as f + clo, bucket (invc, logc) from the
+// exponent and 7 leading mantissa bits of f, r = f * invc - 1 (|r| <= 2^-8),
+// log1p(a) = logc + log1p(r) + clo/f; |a| < 2^-8 uses r = a directly.  The
+// fast kernels read the table from shared memory, the exact path through the
+// read-only cache, so both produce the same seed bits.
+TF_DEV double seed_poly(double r) {  // log1p(r), |r| <= 2^-8 (+slack), degree 7
+  double q = mul(r, r);
+  double p = fmaop(r, 0x1.2492492492492p-3, -0x1.5555555555555p-3);
+  p = fmaop(r, p, 0x1.999999999999ap-3);
+  p = fmaop(r, p, -0.25);
+  p = fmaop(r, p, 0x1.5555555555555p-2);
+  p = fmaop(r, p, -0.5);
+  return fmaop(q, p, r);
+}
+TF_DEV float seed_poly(float r) {   // degree 4
+  float q = mul(r, r);
+  float p = fmaop(r, -0.25f, 0x1.555556p-2f);
+  p = fmaop(r, p, -0.5f);
+  return fmaop(q, p, r);
+}
+template <class Get> TF_DEV double seed_log1p_t(double a, Get get) {
+  double f = add(1.0, a);
+  double clo = sub(a, sub(f, 1.0));                    // 1 + a == f + clo exactly
+  uint32_t h = (uint32_t)hi32(f);
+  int idx = (((int)(h >> 20) - 1022) << 7) | (int)((h >> 13) & 127u);
+  bool small = ahi(a) < 0x3f700000u;                  // |a| < 2^-8
+  idx = small ? 128 : min(max(idx, 0), 256);
+  double2 t = get(idx);
+  double r = small ? a : fmaop(f, t.x, -1.0);
+  double p = seed_poly(r);
+  return add(small ? 0.0 : t.y, fmaop(small ? 0.0 : clo, t.x, p));
+}
+template <class Get> TF_DEV float seed_log1p_t(float a, Get get) {
+  float f = add(1.0f, a);
+  float clo = sub(a, sub(f, 1.0f));
+  uint32_t h = ubits(f);
+  int idx = (((int)(h >> 23) - 126) << 7) | (int)((h >> 16) & 127u);
+  bool small = ahi(a) < 0x3b800000u;                  // |a| < 2^-8
+  idx = small ? 128 : min(max(idx, 0), 256);
+  float2 t = get(idx);
+  float r = small ? a : fmaop(f, t.x, -1.0f);
+  float p = seed_poly(r);
+  return add(small ? 0.0f : t.y, fmaop(small ? 0.0f : clo, t.x, p));
+}
+// exact path: table seed on [-1/2, 1] (bit-identical to the fast kernels),
+// CUDA log1p elsewhere (non-finite / out-of-domain arguments only)
+TF_DEV double seed_log1p(double x) {
+  if (x >= -0.5 && x <= 1.0) return seed_log1p_t(x, [](int i) { return __ldg(&g_SEED64[i]); });
+  return log1p(x);
+}
+TF_DEV float seed_log1p(float x) {
+  if (x >= -0.5f && x <= 1.0f) return seed_log1p_t(x, [](int i) { return __ldg(&g_SEED32[i]); });
+  return log1pf(x);
+}
 
 // The Newton tolerance test is plain binary64 Python arithmetic in both lanes
 // (explog.py:351, 429).
