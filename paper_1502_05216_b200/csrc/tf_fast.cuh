@@ -455,47 +455,103 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
 }
 
 // =============================================================== tlog1p
-// In-band branch of _plog1p_raw (explog.py:440-444, 410-432); the
-// out-of-band branch (y0 < -1/2 or y0 > 1) goes to the exact path.
-// log1p(y0) = log1p(v) - log1p(d), d = y1 / (1 + y0), |d| ~ 2^-53 |log1p(y0)|.
+// _plog1p_raw (explog.py:440-444) with both branches sharing ONE in-band
+// pexpm10 evaluation (the Taylor core is ~3/4 of the work):
+//   in-band  (-1/2 <= v0 <= 1): _log1p_core (426-432) -> _newton_log1p_in_band
+//            (410-424), seed log1p(v0);
+//   out-of-band: w = renorm(v + 1), tlogp(w) = _correct(_log_core(w), log(w0))
+//            (389-392, 338-358), seed log1p((z0 - 1) + z1) after frexp.
+// UNIFIED=false (binary64, cfg 2: 0.45% out-of-band) sends the out-of-band
+// lanes to the exact path instead; UNIFIED=true (binary32, cfg 4: 50/50)
+// evaluates them here with a lane-selected prologue/epilogue.
+// Value parts: log1p(y0) = log1p(v) - log1p(d), d = y1/(1 + y0) (renorm is
+// error-free); log(w0) = log(w) - log1p(w1/w0).
 template <class T, int VW>
 TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW], T (&z0)[VW],
                         T (&z1)[VW], bool (&ok)[VW]) {
   constexpr bool D = sizeof(T) == 8;
-  T y0[VW], y1[VW], x0[VW], mx0[VW];
+  constexpr bool UNIFIED = !D;
+  using C = LogC<T>;
+  T y0[VW], y1[VW], sd[VW], ms[VW], zc0[VW], zc1[VW];
+  int n[VW];
+  bool inb[VW];
   TF<T> v[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
     ok[e] = is_finite(y0i[e]) &&
-            (zbits(y1i[e]) || bexp(y1i[e]) + LogC<T>::SMALL <= bexp(y0i[e]));
+            (zbits(y1i[e]) || bexp(y1i[e]) + C::SMALL <= bexp(y0i[e]));
     y0[e] = ok[e] ? y0i[e] : T(0);
     y1[e] = ok[e] ? y1i[e] : T(0);
     v[e] = renorm_u(mk(y0[e], y1[e]));
-    if (D) ok[e] = ok[e] && ahi(v[e].v) < (sgn(v[e].v) ? H64_HALF : H64_ONE);
-    else ok[e] = ok[e] && ahi(v[e].v) <= (sgn(v[e].v) ? B32_HALF : B32_ONE);
-    v[e].v = ok[e] ? v[e].v : T(0);
-    v[e].e = ok[e] ? v[e].e : T(0);
-    x0[e] = seed_log1p_t(v[e].v, [&](int i) { return tb.SEED[i]; });   // explog.py:427
-    mx0[e] = -x0[e];
+    if (D) inb[e] = ahi(v[e].v) < (sgn(v[e].v) ? H64_HALF : H64_ONE);
+    else inb[e] = ahi(v[e].v) <= (sgn(v[e].v) ? B32_HALF : B32_ONE);
+    T arg = v[e].v;
+    n[e] = 0;
+    zc0[e] = T(1);
+    zc1[e] = T(0);
+    if (UNIFIED) {
+      // out-of-band prologue; v0 > -1 keeps w0 = 1 + v0 positive and normal
+      ok[e] = ok[e] && (inb[e] || !sgn(v[e].v) || ahi(v[e].v) < B32_ONE);
+      TF<T> w = renorm_u(t_add_d_u(v[e], T(1)));
+      auto wb = ubits(w.v);
+      bool band = wb >= C::HALF && wb <= C::TWO;
+      int nn = band ? 0 : C::n_of(w.v);
+      T c0 = band ? w.v : C::mant(w.v);
+      T c1 = band ? w.e : (zbits(w.e) ? T(0) : mul(w.e, C::p2(-nn)));
+      if (!inb[e]) {
+        n[e] = nn;
+        zc0[e] = c0;
+        zc1[e] = c1;
+        arg = add(sub(c0, T(1)), c1);
+      }
+    } else {
+      ok[e] = ok[e] && inb[e];
+    }
+    if (!ok[e]) { arg = T(0); inb[e] = true; }
+    sd[e] = seed_log1p_t(arg, [&](int i) { return tb.SEED[i]; });  // explog.py:347-349, 427
+    ok[e] = ok[e] && (inb[e] || ahi(sd[e]) < C::LN2H);
+    ms[e] = -sd[e];
   }
   TF<T> s[VW];
-  pexpm10_inband_v<T, VW>(tb, mx0, s);
+  pexpm10_inband_v<T, VW>(tb, ms, s);
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    TF<T> u;
-    if (v[e].e == T(0)) {                              // explog.py:418-420
-      TF<T> w = fast_two_sum_u(T(1), v[e].v);
-      u = t_add_d_u(t_mul_u(w, s[e]), v[e].v);
-    } else {                                           // explog.py:421-423
-      TF<T> ys = t_mul_u(v[e], s[e]);
-      u = t_add_u(t_add_u(ys, v[e]), s[e]);
+    if (inb[e]) {
+      TF<T> u;
+      if (v[e].e == T(0)) {                              // explog.py:418-420
+        TF<T> w = fast_two_sum_u(T(1), v[e].v);
+        u = t_add_d_u(t_mul_u(w, s[e]), v[e].v);
+      } else {                                           // explog.py:421-423
+        TF<T> ys = t_mul_u(v[e], s[e]);
+        u = t_add_u(t_add_u(ys, v[e]), s[e]);
+      }
+      T x1 = add(u.v, u.e);
+      ok[e] = ok[e] && newton_quiet(x1, sd[e]);
+      bool tiny = ahi(y0[e]) < (D ? H64_TINY54 : B32_TINY25);
+      T d = mul(y1[e], rcp_nr(add(T(1), y0[e])));       // v - y0 == y1 exactly
+      z0[e] = tiny ? y0[e] : add(sd[e], sub(x1, d));
+      z1[e] = add(x1, sub(sd[e], z0[e]));               // _correct (372-373)
+    } else if (UNIFIED) {
+      // _newton_log_z (320-336) on (zc0, zc1), then + n ln2 (355-358)
+      TF<T> wz = fast_two_sum_u(sub(zc0[e], T(1)), zc1[e]);
+      TF<T> u = t_add_u(t_mul_u(mk(zc0[e], zc1[e]), s[e]), wz);
+      T r1 = add(u.v, u.e);
+      ok[e] = ok[e] && newton_quiet(r1, sd[e]);
+      TF<T> nl = t_mul_d_u(mk(P<T>::LN2_V, P<T>::LN2_E), (T)n[e]);
+      TF<T> core = t_add_u(mk(sd[e], r1), nl);
+      // tlogp's value part log(w0) (correct, 366-373): w1/w0 = zc1/zc0
+      T rc = rcp_nr(zc0[e]);
+      T d0 = mul(zc1[e], rc);
+      T d1 = mul(fmaop(-d0, zc0[e], zc1[e]), rc);
+      TF<T> a = two_sum_u(core.v, -d0);
+      T t0 = add(a.v, add(add(a.e, core.e), sub(mul(mul(T(0.5), d0), d0), d1)));
+      T t1 = add(core.e, sub(core.v, t0));
+      // final value part log1p(y0) = log(w) - log1p(y1 / (1 + y0))
+      T dd = mul(y1[e], rcp_nr(add(T(1), y0[e])));
+      T zz = add(core.v, sub(core.e, dd));
+      z0[e] = zz;
+      z1[e] = add(t1, sub(t0, zz));                      // _correct (372-373)
     }
-    T x1 = add(u.v, u.e);
-    ok[e] = ok[e] && newton_quiet(x1, x0[e]);
-    bool tiny = ahi(y0[e]) < (D ? H64_TINY54 : B32_TINY25);
-    T d = mul(y1[e], rcp_nr(add(T(1), y0[e])));       // v - y0 == y1 exactly
-    z0[e] = tiny ? y0[e] : add(x0[e], sub(x1, d));
-    z1[e] = add(x1, sub(x0[e], z0[e]));               // _correct (372-373)
   }
 }
 

@@ -292,7 +292,9 @@ __global__ void k_compare(const T* z0, const T* z1, const T* r0, const T* r1, ui
     if (fa && fb) {
       double ref = (double)b0 + (double)b1;
       double d = ((double)a0 - (double)b0) + ((double)a1 - (double)b1);
-      double tol = fmax(rel * fabs(ref), abs_guard);
+      T ab1 = fabs(b1);
+      double ulp1 = (double)nextafter(ab1, Lim<T>::inf()) - (double)ab1;  // rounding of z1 itself
+      double tol = fmax(fmax(rel * fabs(ref), abs_guard), ulp1);
       if (!(fabs(d) <= tol)) c[3]++;
     } else {
       // same class per field: NaN <-> NaN, inf of the same sign
