@@ -493,6 +493,8 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       // out-of-band prologue; v0 > -1 keeps w0 = 1 + v0 positive and normal
       ok[e] = ok[e] && (inb[e] || !sgn(v[e].v) || ahi(v[e].v) < B32_ONE);
       TF<T> w = renorm_u(t_add_d_u(v[e], T(1)));
+      // |d| = |y1 / (1 + y0)| <= ~2^-13 so log1p(d) = d - d^2/2 suffices below
+      ok[e] = ok[e] && (inb[e] || zbits(y1[e]) || bexp(y1[e]) + 14 <= bexp(w.v));
       auto wb = ubits(w.v);
       bool band = wb >= C::HALF && wb <= C::TWO;
       int nn = band ? 0 : C::n_of(w.v);
@@ -548,7 +550,7 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       T t1 = add(core.e, sub(core.v, t0));
       // final value part log1p(y0) = log(w) - log1p(y1 / (1 + y0))
       T dd = mul(y1[e], rcp_nr(add(T(1), y0[e])));
-      T zz = add(core.v, sub(core.e, dd));
+      T zz = add(core.v, sub(core.e, fmaop(mul(T(-0.5), dd), dd, dd)));
       z0[e] = zz;
       z1[e] = add(t1, sub(t0, zz));                      // _correct (372-373)
     }
