@@ -275,6 +275,25 @@ TF_DEV bool newton_quiet(float r1, float r0) {
   return e1 + 22 <= max(e0, 127);
 }
 
+// binary32 value part RN(h + l) from a twofold core that is only accurate to
+// ~2^-36 relative (the reference's own binary32 L0 bound):
+// flag the element when h + l lies within 2^-32 |z| of a rounding boundary
+// (probability ~2^-9 ulp-relative, i.e. ~1e-5 of elements) so the exact path,
+// which rounds a binary64 core, decides it.  Exact powers of two are flagged
+// too (the boundary below them is at a quarter ulp).
+TF_DEV float rn_guard(float h, float l, bool& hard) {
+  float z = add(h, l);
+  float rho = add(sub(h, z), l);                    // (h + l) - z
+  int ez = bexp(z);
+  float half = __int_as_float(max(ez - 24, 1) << 23);   // ulp(z) / 2
+  hard = fabsf(fabsf(rho) - half) <= 0x1p-32f * fabsf(z) || (ubits(z) & 0x7fffffu) == 0u;
+  return z;
+}
+TF_DEV double rn_guard(double h, double l, bool& hard) {  // binary64 cores: ~2^-100, no guard
+  hard = false;
+  return add(h, l);
+}
+
 // ================================================================ texp
 template <int VW>
 TF_DEV void fast_texp(const STab<double>& tb, const double (&x0)[VW], const double (&x1)[VW],
@@ -321,7 +340,9 @@ TF_DEV void fast_texp(const STab<float>& tb, const float (&x0)[VW], const float 
     bool scaled = m[e] <= -35;  // e^(2m) < 2^-100: residuals would underflow
     TF<float> es = tv<float>(tb.ESC[scaled ? m[e] - TF32_ESC_LO : 0]);
     TF<float> vs = t_mul_u(scaled ? es : ev, ct);
-    z0[e] = mul(add(vs.v, vs.e), scaled ? 0x1p-64f : 1.0f);
+    bool hard;
+    z0[e] = mul(rn_guard(vs.v, vs.e, hard), scaled ? 0x1p-64f : 1.0f);
+    ok[e] = ok[e] && !hard;
     z1[e] = add(mul(z0[e], t1_tiny(x1[e])), add(v.e, sub(v.v, z0[e])));
   }
 }
@@ -367,7 +388,9 @@ TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const floa
     TF<float> v = t_mul_u(tv<float>(tb.E[m[e] - P<float>::E_LO]),
                           t_mul_u(tv<float>(tb.C[n[e] - P<float>::C_LO]), t[e]));
     TF<float> w = t_add_d_u(v, -1.0f);                          // expcore.py:147
-    z0[e] = add(w.v, w.e);
+    bool hard;
+    z0[e] = rn_guard(w.v, w.e, hard);
+    ok[e] = ok[e] && !hard;
     float tail = add(w.e, sub(w.v, z0[e]));
     z1[e] = add(mul(add(z0[e], 1.0f), t1_tiny(x1[e])), tail);
   }
@@ -446,9 +469,11 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     T d1 = mul(fmaop(-d0, ys0, ys1), rc);
     TF<T> a = two_sum_u(core.v, -d0);
     T tail = add(add(a.e, core.e), sub(mul(mul(T(0.5), d0), d0), d1));
-    T zz = add(a.v, tail);
+    bool hard;
+    T zz = rn_guard(a.v, tail, hard);
     T dl = sub(y0[e], T(1));                          // exact near 1
     if (ahi(dl) < C::NEAR1H) zz = log_near1(dl);
+    else ok[e] = ok[e] && !hard;
     z0[e] = zz;
     z1[e] = add(core.e, sub(core.v, zz));            // _correct (372-373)
   }
@@ -531,7 +556,10 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       ok[e] = ok[e] && newton_quiet(x1, sd[e]);
       bool tiny = ahi(y0[e]) < (D ? H64_TINY54 : B32_TINY25);
       T d = mul(y1[e], rcp_nr(add(T(1), y0[e])));       // v - y0 == y1 exactly
-      z0[e] = tiny ? y0[e] : add(sd[e], sub(x1, d));
+      bool hard;
+      T zz = rn_guard(sd[e], sub(x1, d), hard);
+      z0[e] = tiny ? y0[e] : zz;
+      ok[e] = ok[e] && (tiny || !hard);
       z1[e] = add(x1, sub(sd[e], z0[e]));               // _correct (372-373)
     } else if (UNIFIED) {
       // _newton_log_z (320-336) on (zc0, zc1), then + n ln2 (355-358)
@@ -550,7 +578,9 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       T t1 = add(core.e, sub(core.v, t0));
       // final value part log1p(y0) = log(w) - log1p(y1 / (1 + y0))
       T dd = mul(y1[e], rcp_nr(add(T(1), y0[e])));
-      T zz = add(core.v, sub(core.e, fmaop(mul(T(-0.5), dd), dd, dd)));
+      bool hard;
+      T zz = rn_guard(core.v, sub(core.e, fmaop(mul(T(-0.5), dd), dd, dd)), hard);
+      ok[e] = ok[e] && !hard;
       z0[e] = zz;
       z1[e] = add(t1, sub(t0, zz));                      // _correct (372-373)
     }
