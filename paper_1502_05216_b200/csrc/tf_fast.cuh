@@ -280,13 +280,15 @@ TF_DEV bool newton_quiet(float r1, float r0) {
 // flag the element when h + l lies within 2^-32 |z| of a rounding boundary
 // (probability ~2^-9 ulp-relative, i.e. ~1e-5 of elements) so the exact path,
 // which rounds a binary64 core, decides it.  Exact powers of two are flagged
-// too (the boundary below them is at a quarter ulp).
+// by the quarter-ulp boundary below them as well.
 TF_DEV float rn_guard(float h, float l, bool& hard) {
   float z = add(h, l);
   float rho = add(sub(h, z), l);                    // (h + l) - z
   int ez = bexp(z);
   float half = __int_as_float(max(ez - 24, 1) << 23);   // ulp(z) / 2
-  hard = fabsf(fabsf(rho) - half) <= 0x1p-32f * fabsf(z) || (ubits(z) & 0x7fffffu) == 0u;
+  float tol = 0x1p-32f * fabsf(z);
+  bool pow2 = (ubits(z) & 0x7fffffu) == 0u;
+  hard = fabsf(fabsf(rho) - half) <= tol || (pow2 && fabsf(fabsf(rho) - 0.5f * half) <= tol);
   return z;
 }
 TF_DEV double rn_guard(double h, double l, bool& hard) {  // binary64 cores: ~2^-100, no guard
