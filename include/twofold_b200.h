@@ -59,6 +59,7 @@ extern "C" {
 /* tf_eval flags */
 #define TF_FLAG_FORCE_EXACT 1 /* route every element through the exact path (testing) */
 #define TF_FLAG_COUNT_EXACT 2 /* count exact-path elements (tf_exact_count) */
+#define TF_FLAG_MARK_EXACT 4  /* diagnostics: write (NaN, -12345) instead of evaluating them */
 
 /* synthetic distributions for tf_generate (BASELINE.json configs; workloads.py) */
 #define TF_DIST_EXP64 0

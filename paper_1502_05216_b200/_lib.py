@@ -19,6 +19,7 @@ TF_OK, TF_ERR_ARG, TF_ERR_CUDA = 0, -1, -2
 FN_CODES = {"texp": 0, "texpm1": 1, "tlog": 2, "tlog1p": 3}
 FLAG_FORCE_EXACT = 1
 FLAG_COUNT_EXACT = 2
+FLAG_MARK_EXACT = 4
 DIST_CODES = {"exp64": 0, "pow10_64": 1, "pow10c_64": 2, "log64": 3, "exp32": 4, "log32": 5,
               "exp64s": 6, "logu64s": 7}
 

@@ -74,12 +74,17 @@ template <int N> TF_DEV void cp_async_wait() {
 // Evaluate the queued rare elements q[0..cnt) (cnt <= 32) with the exact path.
 template <class T, int FN>
 TF_DEV void drain(const uint32_t* q, int cnt, const T* __restrict__ x0, const T* __restrict__ x1,
-                  T* __restrict__ z0, T* __restrict__ z1, int lane, bool count) {
+                  T* __restrict__ z0, T* __restrict__ z1, int lane, bool count, bool mark) {
   if (lane < cnt) {
     uint32_t i = q[lane];
-    TF<T> r = eval_gen<T, FN>(x0[i], x1[i]);
-    z0[i] = r.v;
-    z1[i] = r.e;
+    if (mark) {  // diagnostics: tag exact-path elements instead of evaluating them
+      z0[i] = Lim<T>::qnan();
+      z1[i] = T(-12345);
+    } else {
+      TF<T> r = eval_gen<T, FN>(x0[i], x1[i]);
+      z0[i] = r.v;
+      z1[i] = r.e;
+    }
   }
   if (count && lane == 0) atomicAdd(&g_rare_count, (unsigned long long)cnt);
 }
@@ -101,6 +106,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   uint32_t* q = qs[warp];
   const bool force = flags & TF_FLAG_FORCE_EXACT;
   const bool count = flags & TF_FLAG_COUNT_EXACT;
+  const bool mark = flags & TF_FLAG_MARK_EXACT;
   int qn = 0;  // warp-uniform
   // 32-bit index arithmetic: the host splits launches at 2^31 elements
   const uint32_t nvec = n / VW;
@@ -159,7 +165,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
     }
     while (qn >= 32) {
       __syncwarp();
-      drain<T, FN>(q, 32, x0, x1, z0, z1, lane, count);
+      drain<T, FN>(q, 32, x0, x1, z0, z1, lane, count, mark);
       __syncwarp();
       uint32_t mv = (lane + 32 < qn) ? q[lane + 32] : 0u;
       uint32_t mv2 = (lane + 64 < qn) ? q[lane + 64] : 0u;
@@ -184,7 +190,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   while (qn > 0) {
     __syncwarp();
     int c = qn < 32 ? qn : 32;
-    drain<T, FN>(q, c, x0, x1, z0, z1, lane, count);
+    drain<T, FN>(q, c, x0, x1, z0, z1, lane, count, mark);
     __syncwarp();
     uint32_t mv = (lane + 32 < qn) ? q[lane + 32] : 0u;
     uint32_t mv2 = (lane + 64 < qn) ? q[lane + 64] : 0u;
