@@ -77,6 +77,18 @@ constexpr uint32_t H64_HALF = 0x3fe00000u;      // < 0.5
 constexpr uint32_t H64_ONE = 0x3ff00000u;       // < 1
 constexpr uint32_t H64_NEAR1 = 0x3eb00000u;     // < 2^-20
 
+// biased exponent that keeps counting down through the subnormals (so a
+// subnormal error part still compares by magnitude): 2^(eexp - bias) <= |x|
+TF_DEV int eexp(double x) {
+  int b = bexp(x);
+  unsigned long long m = ubits(x) & 0x000fffffffffffffull;
+  return b ? b : 12 - __clzll((long long)m);
+}
+TF_DEV int eexp(float x) {
+  int b = bexp(x);
+  return b ? b : 9 - __clz((int)(ubits(x) & 0x7fffffu));
+}
+
 TF_DEV bool sgn(double x) { return hi32(x) < 0; }
 TF_DEV bool sgn(float x) { return (int)ubits(x) < 0; }
 
@@ -281,16 +293,17 @@ TF_DEV bool newton_quiet(float r1, float r0) {
 // (probability ~2^-9 ulp-relative, i.e. ~1e-5 of elements) so the exact path,
 // which rounds a binary64 core, decides it.  Exact powers of two are flagged
 // by the quarter-ulp boundary below them as well.
-TF_DEV float rn_guard(float h, float l, bool& hard) {
+template <int TOL = -32> TF_DEV float rn_guard(float h, float l, bool& hard) {
   float z = add(h, l);
   float rho = add(sub(h, z), l);                    // (h + l) - z
   int ez = bexp(z);
   float half = __int_as_float(max(ez - 24, 1) << 23);   // ulp(z) / 2
-  float tol = 0x1p-32f * fabsf(z);
+  float tol = __int_as_float((127 + TOL) << 23) * fabsf(z);
   bool pow2 = (ubits(z) & 0x7fffffu) == 0u;
   hard = fabsf(fabsf(rho) - half) <= tol || (pow2 && fabsf(fabsf(rho) - 0.5f * half) <= tol);
   return z;
 }
+template <int TOL = -32>
 TF_DEV double rn_guard(double h, double l, bool& hard) {  // binary64 cores: ~2^-100, no guard
   hard = false;
   return add(h, l);
@@ -343,7 +356,7 @@ TF_DEV void fast_texp(const STab<float>& tb, const float (&x0)[VW], const float 
     TF<float> es = tv<float>(tb.ESC[scaled ? m[e] - TF32_ESC_LO : 0]);
     TF<float> vs = t_mul_u(scaled ? es : ev, ct);
     bool hard;
-    z0[e] = mul(rn_guard(vs.v, vs.e, hard), scaled ? 0x1p-64f : 1.0f);
+    z0[e] = mul(rn_guard<-35>(vs.v, vs.e, hard), scaled ? 0x1p-64f : 1.0f);
     ok[e] = ok[e] && !hard;
     z1[e] = add(mul(z0[e], t1_tiny(x1[e])), add(v.e, sub(v.v, z0[e])));
   }
@@ -391,7 +404,7 @@ TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const floa
                           t_mul_u(tv<float>(tb.C[n[e] - P<float>::C_LO]), t[e]));
     TF<float> w = t_add_d_u(v, -1.0f);                          // expcore.py:147
     bool hard;
-    z0[e] = rn_guard(w.v, w.e, hard);
+    z0[e] = rn_guard<-35>(w.v, w.e, hard);
     ok[e] = ok[e] && !hard;
     float tail = add(w.e, sub(w.v, z0[e]));
     z1[e] = add(mul(add(z0[e], 1.0f), t1_tiny(x1[e])), tail);
@@ -440,7 +453,7 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
   for (int e = 0; e < VW; ++e) {
     uint32_t eb0 = C::eb(y0i[e]);                     // sign|exponent
     ok[e] = eb0 - 1u < C::NORM_SPAN &&                 // positive normal y0
-            (zbits(y1i[e]) || bexp(y1i[e]) + C::SMALL <= (int)eb0);
+            (zbits(y1i[e]) || eexp(y1i[e]) + C::SMALL <= (int)eb0);
     y0[e] = ok[e] ? y0i[e] : T(1);
     y1[e] = ok[e] ? y1i[e] : T(0);
     v[e] = renorm_u(mk(y0[e], y1[e]));
@@ -505,8 +518,11 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
   TF<T> v[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    ok[e] = is_finite(y0i[e]) &&
-            (zbits(y1i[e]) || bexp(y1i[e]) + C::SMALL <= bexp(y0i[e]));
+    // |y1| << |y0| keeps d = y1/(1+y0) tiny; below 2^-54 the value part is y0
+    // itself and no correction is needed, so any finite y1 is fine there
+    bool tiny0 = ahi(y0i[e]) < (D ? H64_TINY54 : B32_TINY25);
+    ok[e] = is_finite(y0i[e]) && is_finite(y1i[e]) &&
+            (tiny0 || zbits(y1i[e]) || eexp(y1i[e]) + C::SMALL <= eexp(y0i[e]));
     y0[e] = ok[e] ? y0i[e] : T(0);
     y1[e] = ok[e] ? y1i[e] : T(0);
     v[e] = renorm_u(mk(y0[e], y1[e]));
