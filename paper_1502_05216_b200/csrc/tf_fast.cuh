@@ -595,7 +595,9 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       T t0 = add(a.v, add(add(a.e, core.e), sub(mul(mul(T(0.5), d0), d0), d1)));
       T t1 = add(core.e, sub(core.v, t0));
       // final value part log1p(y0) = log(w) - log1p(y1 / (1 + y0))
-      T dd = mul(y1[e], rcp_nr(add(T(1), y0[e])));
+      // 1 + y0 ~ w0 = zc0 * 2^n: divide in the scaled domain (1/(1 + y0) can
+      // underflow the approximate reciprocal when y0 ~ FLT_MAX)
+      T dd = mul(mul(y1[e], C::p2(-n[e])), rcp_nr(zc0[e]));
       bool hard;
       T zz = rn_guard(core.v, sub(core.e, fmaop(mul(T(-0.5), dd), dd, dd)), hard);
       ok[e] = ok[e] && !hard;

@@ -26,13 +26,17 @@ def run(fn, width, x0, x1, flags=0):
 
 
 res = {}
-for width in (64, 32):
+CFGS = os.environ.get("DUMP_CFGS")
+GOLD = os.environ.get("DUMP_GOLDEN", "1") == "1"
+for width in ((64, 32) if GOLD else ()):
     for fn in ("texp", "texpm1", "tlog", "tlog1p"):
         g = np.load(os.path.join(ROOT, "tests", "golden", f"golden_{fn}_f{width}.npz"))
         a0, a1 = run(fn, width, g["x0"], g["x1"])
         b0, b1 = run(fn, width, g["x0"], g["x1"], _lib.FLAG_FORCE_EXACT)
         res[f"g_{fn}_{width}"] = np.stack([a0, a1, b0, b1])
 for cfg, (fn, width, dist, _) in workloads.CONFIGS.items():
+    if CFGS and cfg not in CFGS.split(","):
+        continue
     x0, x1 = workloads.generate(dist, 0, N, seed=1)
     a0, a1 = run(fn, width, x0, x1)
     b0, b1 = run(fn, width, x0, x1, _lib.FLAG_FORCE_EXACT)
