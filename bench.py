@@ -298,25 +298,27 @@ def run_ours(args):
     # ---- end to end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        host = {}
+        host, hout = {}, {}
         for fn, _ in HEADLINE:
             a0, a1 = ins[fn]
             host[fn] = (a0.cpu().pin_memory(), a1.cpu().pin_memory())
+            hout[fn] = (torch.empty(n, dtype=torch.float64).pin_memory(),
+                        torch.empty(n, dtype=torch.float64).pin_memory())
         # warm the pipeline
         for fn, _ in HEADLINE:
-            getattr(f64, fn)(Twofold(*host[fn]))
+            getattr(f64, fn)(Twofold(*host[fn]), out=hout[fn])
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
         barrier()
         tw = time.perf_counter()
         for _ in range(e2e_steps):
             for fn, _ in HEADLINE:
-                z = getattr(f64, fn)(Twofold(*host[fn]))
+                z = getattr(f64, fn)(Twofold(*host[fn]), out=hout[fn])
         torch.cuda.synchronize()
         t_e2e = max_over_ranks((time.perf_counter() - tw) / e2e_steps)
         _ = float(z.value[0])  # the result is on the host
         e2e = {"value": 2 * n * world / t_e2e, "unit": "elements/s",
                "h2d_bytes_per_step": 2 * 2 * n * 8, "d2h_bytes_per_step": 2 * 2 * n * 8,
-               "ms_per_step": t_e2e * 1e3, "path": "api(64).texpm1/tlog1p on pinned CPU tensors"}
+               "ms_per_step": t_e2e * 1e3, "path": "api(64).texpm1/tlog1p(Twofold(pinned CPU tensors), out=pinned CPU tensors)"}
 
     # ---- parity sample + the one small NCCL reduce of error statistics
     stats = parity_sample(args, ins, outs, n, rank, world, dev)
@@ -368,15 +370,14 @@ def run_ours(args):
 
 def parity_sample(args, ins, outs, n, rank, world, dev):
     """Check a seeded sample of each rank's outputs against the CPU oracle, then
-    sum the per-rank counters with one tiny NCCL all-reduce."""
-    import torch
-
+    combine the per-rank counters with the one small all-reduce of the run
+    (paper_1502_05216_b200.dist.reduce_stats; NCCL here, gloo in the tests)."""
     from oracle import oracle as O
     from oracle.compare import compare
+    from paper_1502_05216_b200.dist import reduce_stats
 
     m = min(args.parity_sample, n)
-    keys = ("n", "z0_mismatch", "z0_gt1ulp", "tol_violations", "class_mismatch")
-    vec = []
+    out = {}
     for fn, _ in HEADLINE:
         x0 = ins[fn][0][:m].cpu().numpy()
         x1 = ins[fn][1][:m].cpu().numpy()
@@ -384,16 +385,9 @@ def parity_sample(args, ins, outs, n, rank, world, dev):
         z1 = outs[fn][1][:m].cpu().numpy()
         r0, r1 = O.evaluate(fn, 64, x0, x1, backend="dv")
         r = compare(z0, z1, r0, r1, 64)
-        vec.extend(r[k] for k in keys)
-    t = torch.tensor(vec, dtype=torch.float64, device=dev)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    v = t.cpu().tolist()
-    out = {}
-    for i, (fn, _) in enumerate(HEADLINE):
-        out[fn] = {k: int(v[i * len(keys) + j]) for j, k in enumerate(keys)}
+        out[fn] = reduce_stats(r, device=dev)
+        out[fn].pop("bad_idx", None)
+        out[fn].pop("z0_ulp_hist", None)
     out["oracle"] = "CPU port, dv backend (bit-exact vs reference goldens)"
     return out
 

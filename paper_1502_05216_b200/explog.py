@@ -79,21 +79,21 @@ class ExpLog:
         self._np = np.float64 if width == 64 else np.float32
 
     # ---- the four twofold-argument functions (explog.py:265, 299, 394, 464)
-    def texp(self, x):
+    def texp(self, x, out=None):
         """Twofold e**(x0+x1); value part = correctly rounded exp(x0)."""
-        return self._call("texp", x)
+        return self._call("texp", x, out)
 
-    def texpm1(self, x):
+    def texpm1(self, x, out=None):
         """Twofold e**(x0+x1) - 1; value part = correctly rounded expm1(x0)."""
-        return self._call("texpm1", x)
+        return self._call("texpm1", x, out)
 
-    def tlog(self, y):
+    def tlog(self, y, out=None):
         """Twofold ln of any twofold; value part = correctly rounded log(y0)."""
-        return self._call("tlog", y)
+        return self._call("tlog", y, out)
 
-    def tlog1p(self, y):
+    def tlog1p(self, y, out=None):
         """Twofold ln(1 + y0 + y1); value part = correctly rounded log1p(y0)."""
-        return self._call("tlog1p", y)
+        return self._call("tlog1p", y, out)
 
     def function(self, name: str):
         if name not in FUNCTION_NAMES:
@@ -117,7 +117,7 @@ class ExpLog:
                 raise TypeError("both twofold parts must be torch tensors")
             if x0.is_cuda or x1.is_cuda:
                 return self._device(fn, x0, x1, out)
-            return self._host_torch(fn, x0, x1)
+            return self._host_torch(fn, x0, x1, out)
         if np.isscalar(x0) and np.isscalar(x1) or (isinstance(x0, (int, float)) and
                                                    isinstance(x1, (int, float))):
             a0 = np.array([x0], dtype=self._np)
@@ -170,16 +170,22 @@ class ExpLog:
             self._launch(fn, a0, a1, z0, z1, a0.numel(), stream, flags)
         return Twofold(z0, z1)
 
-    def _host_torch(self, fn, x0, x1):
-        import torch
-
+    def _host_torch(self, fn, x0, x1, out=None):
         dt = self._torch_dtype()
         if x0.shape != x1.shape:
             raise ValueError(f"twofold parts differ in shape: {tuple(x0.shape)} vs "
                              f"{tuple(x1.shape)}")
         a0 = x0.to(dt).contiguous().reshape(-1)
         a1 = x1.to(dt).contiguous().reshape(-1)
-        z0, z1 = _pipeline(self, fn, a0, a1)
+        if out is not None:
+            o0, o1 = out
+            if (o0.shape != x0.shape or o1.shape != x0.shape or o0.dtype != dt or
+                    o1.dtype != dt or o0.is_cuda or o1.is_cuda or not o0.is_contiguous()
+                    or not o1.is_contiguous()):
+                raise ValueError("out= host tensors must be contiguous CPU tensors of the "
+                                 "input shape and lane dtype (pinned for full PCIe speed)")
+            out = (o0.reshape(-1), o1.reshape(-1))
+        z0, z1 = _pipeline(self, fn, a0, a1, out=out)
         return Twofold(z0.reshape(x0.shape), z1.reshape(x0.shape))
 
     def _host_numpy(self, fn, a0, a1):
@@ -191,9 +197,10 @@ class ExpLog:
         return z0.numpy().reshape(a0.shape), z1.numpy().reshape(a0.shape)
 
 
-def _pipeline(lib: ExpLog, fn: str, h0, h1, device=None, chunk: int = HOST_CHUNK):
+def _pipeline(lib: ExpLog, fn: str, h0, h1, device=None, chunk: int = HOST_CHUNK, out=None):
     """Evaluate host tensors: chunked H2D -> kernel -> D2H on two streams so the
-    copy engines run both directions while the kernels execute."""
+    copy engines run both directions while the kernels execute.  `out` may
+    supply (pinned) host result tensors; otherwise pinned ones are allocated."""
     import torch
 
     if not torch.cuda.is_available():
@@ -202,8 +209,11 @@ def _pipeline(lib: ExpLog, fn: str, h0, h1, device=None, chunk: int = HOST_CHUNK
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     n = h0.numel()
     pinned = h0.is_pinned() and h1.is_pinned()
-    z0 = torch.empty(n, dtype=h0.dtype, pin_memory=True)
-    z1 = torch.empty(n, dtype=h0.dtype, pin_memory=True)
+    if out is not None:
+        z0, z1 = out
+    else:
+        z0 = torch.empty(n, dtype=h0.dtype, pin_memory=True)
+        z1 = torch.empty(n, dtype=h0.dtype, pin_memory=True)
     if n == 0:
         return z0, z1
     if not pinned:
