@@ -148,7 +148,7 @@ template <int VW> TF_DEV void taylor_exp_v(const double (&y)[VW], TF<double> (&t
     s = add(mul(s, y[e]), 1320.0);
     t[e] = mk(s, 0.0);
   }
-#pragma unroll 3
+#pragma unroll
   for (int k = 0; k < 9; ++k) {
     const double c = c_texp64[k];
 #pragma unroll
@@ -177,7 +177,7 @@ template <int VW> TF_DEV void taylor_expm1_v(const double (&y)[VW], TF<double> (
     s = add(mul(s, y[e]), 720.0);
     t[e] = mk(s, 0.0);
   }
-#pragma unroll 3
+#pragma unroll
   for (int k = 0; k < 6; ++k) {
     const double c = c_texpm1_64[k];
 #pragma unroll

@@ -22,6 +22,9 @@
 namespace tf {
 
 constexpr int BLOCK = 256;
+#ifndef TF_MINB
+#define TF_MINB 4
+#endif
 constexpr int WARPS = BLOCK / 32;
 
 __device__ unsigned long long g_rare_count = 0;
@@ -90,7 +93,7 @@ TF_DEV void drain(const uint32_t* q, int cnt, const T* __restrict__ x0, const T*
 }
 
 template <class T, int FN, int VW>
-__global__ void __launch_bounds__(BLOCK, 4)
+__global__ void __launch_bounds__(BLOCK, TF_MINB)
 k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
        T* __restrict__ z1, uint32_t n, int flags) {
   constexpr int QCAP = 32 + 32 * VW;
