@@ -104,8 +104,9 @@ TF_API int tf_compare(int width, const void* z0, const void* z1, const void* r0,
                       int64_t n, double rel, double abs_guard, unsigned long long* stats_dev,
                       void* stream);
 
-/* FMA-pipe calibration: `blocks` CTAs x 256 threads x `iters` x 8 dependent
- * FMAs of the given width (2048 ops per thread per iteration block). */
+/* FP-pipe calibration: `blocks` CTAs x 256 threads x `iters` x 8 independent
+ * ops of the given width; width + 100 selects DADD/FADD chains, width + 200
+ * DMUL/FMUL chains, plain width FMA chains. */
 TF_API int tf_fma_peak(int width, void* out_dev, int blocks, int iters, void* stream);
 
 /* Elements routed through the exact path since the last reset (needs

@@ -323,16 +323,22 @@ __global__ void k_compare(const T* z0, const T* z1, const T* r0, const T* r1, ui
 }
 
 // ------------------------------------------------ pipe peak calibration
-// 8 independent FMA chains per thread; every FMA counts as one op (the unit of
-// the algorithmic op counts).  Used by bench.py for the roofline denominator.
-template <class T>
+// 8 independent chains per thread of one opcode (OP 0 = fma, 1 = add, 2 = mul);
+// every op counts as one op (the unit of the algorithmic op counts).  bench.py
+// takes the best of the three as the roofline denominator (on B200 DADD/DMUL
+// issue slightly faster than DFMA).
+template <class T, int OP>
 __global__ void __launch_bounds__(256) k_fma_peak(T* out, int iters, T a, T b) {
   T c[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) c[k] = T(threadIdx.x + k);
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) c[k] = fmaop(c[k], a, b);
+    for (int k = 0; k < 8; ++k) {
+      if (OP == 0) c[k] = fmaop(c[k], a, b);
+      if (OP == 1) c[k] = add(c[k], b);
+      if (OP == 2) c[k] = mul(c[k], a);
+    }
   }
   T s = T(0);
 #pragma unroll
@@ -553,12 +559,19 @@ TF_API int tf_compare(int width, const void* z0, const void* z1, const void* r0,
 TF_API int tf_fma_peak(int width, void* out_dev, int blocks, int iters, void* stream) {
   if (blocks <= 0 || iters <= 0 || !out_dev) return fail(TF_ERR_ARG, "bad peak arguments%s");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (width == 64)
-    tf::k_fma_peak<double><<<blocks, 256, 0, s>>>((double*)out_dev, iters, 0.999999, 1e-7);
-  else if (width == 32)
-    tf::k_fma_peak<float><<<blocks, 256, 0, s>>>((float*)out_dev, iters, 0.999999f, 1e-7f);
-  else
+  int op = width / 100, w = width % 100;  // width + 100 * op selects add (1) / mul (2)
+  if (op < 0 || op > 2) return fail(TF_ERR_ARG, "bad peak opcode%s");
+  if (w == 64) {
+    if (op == 0) tf::k_fma_peak<double, 0><<<blocks, 256, 0, s>>>((double*)out_dev, iters, 0.999999, 1e-7);
+    if (op == 1) tf::k_fma_peak<double, 1><<<blocks, 256, 0, s>>>((double*)out_dev, iters, 0.999999, 1e-7);
+    if (op == 2) tf::k_fma_peak<double, 2><<<blocks, 256, 0, s>>>((double*)out_dev, iters, 0.999999, 1e-7);
+  } else if (w == 32) {
+    if (op == 0) tf::k_fma_peak<float, 0><<<blocks, 256, 0, s>>>((float*)out_dev, iters, 0.999999f, 1e-7f);
+    if (op == 1) tf::k_fma_peak<float, 1><<<blocks, 256, 0, s>>>((float*)out_dev, iters, 0.999999f, 1e-7f);
+    if (op == 2) tf::k_fma_peak<float, 2><<<blocks, 256, 0, s>>>((float*)out_dev, iters, 0.999999f, 1e-7f);
+  } else {
     return fail(TF_ERR_ARG, "unsupported width%s");
+  }
   return cuda_check("k_fma_peak launch");
 }
 

@@ -8,5 +8,5 @@ import json
 d = json.loads(open("gpurun_out/bench.log").read().strip().splitlines()[-1])
 print("headline Gelem/s", round(d["value"] / 1e9, 2), {k: round(v, 4) for k, v in d["kernel_ms"].items()}, "frac", round(d["roofline"]["frac"], 3), d["clocks"])
 for k, v in d["per_function"].items():
-    print(f'{k:12s} {v["elements_per_s"]/1e9:7.1f} Gelem/s  fma_frac {v["fma_pipe_frac"]:.3f}  hbm_frac {v["hbm_frac"]:.3f}')
+    print(f'{k:12s} {v["elements_per_s"]/1e9:7.1f} Gelem/s  fp_frac {v["fp_pipe_frac"]:.3f}  hbm_frac {v["hbm_frac"]:.3f}')
 PY
