@@ -477,15 +477,13 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     ok[e] = ok[e] && newton_quiet(r1, r0[e]);
     TF<T> nl = t_mul_d_u(mk(P<T>::LN2_V, P<T>::LN2_E), (T)n[e]);
     TF<T> core = t_add_u(mk(r0[e], r1), nl);
-    T sc = C::p2(-n[e]);
-    T ys0 = mul(y0[e], sc), ys1 = mul(y1[e], sc);
-    T rc = rcp_nr(ys0);
-    T d0 = mul(ys1, rc);
-    T d1 = mul(fmaop(-d0, ys0, ys1), rc);
-    TF<T> a = two_sum_u(core.v, -d0);
-    T tail = add(add(a.e, core.e), sub(mul(mul(T(0.5), d0), d0), d1));
+    // Away from 1 (|y0 - 1| >= 2^-20, 2^-7 in binary32) |log y0| is large next
+    // to d = y1/y0 (|d| <= 2^-50 |log y0|, 2^-17 in binary32), so
+    // log(y0) = core - d to well below an ulp with d known to ~2^-22:
+    // y1 * 2^-n over zc0 (= v0 * 2^-n, within an ulp of y0 * 2^-n).
+    T d0 = mul(mul(y1[e], C::p2(-n[e])), rcp_approx(zc0[e]));
     bool hard;
-    T zz = rn_guard(a.v, tail, hard);
+    T zz = rn_guard(core.v, sub(core.e, d0), hard);
     T dl = sub(y0[e], T(1));                          // exact near 1
     if (ahi(dl) < C::NEAR1H) zz = log_near1(dl);
     else ok[e] = ok[e] && !hard;
@@ -573,7 +571,8 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       T x1 = add(u.v, u.e);
       ok[e] = ok[e] && newton_quiet(x1, sd[e]);
       bool tiny = ahi(y0[e]) < (D ? H64_TINY54 : B32_TINY25);
-      T d = mul(y1[e], rcp_nr(add(T(1), y0[e])));       // v - y0 == y1 exactly
+      // v - y0 == y1 exactly; |d| ~ 2^-53 |log1p(y0)|: ~2^-22 accuracy suffices
+      T d = mul(y1[e], rcp_approx(add(T(1), y0[e])));
       bool hard;
       T zz = rn_guard(sd[e], sub(x1, d), hard);
       z0[e] = tiny ? y0[e] : zz;
@@ -588,16 +587,16 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       TF<T> nl = t_mul_d_u(mk(P<T>::LN2_V, P<T>::LN2_E), (T)n[e]);
       TF<T> core = t_add_u(mk(sd[e], r1), nl);
       // tlogp's value part log(w0) (correct, 366-373): w1/w0 = zc1/zc0
+      // (out-of-band: |log w0| >= ln 2 - tiny, |w1/w0| <= 2^-24)
       T rc = rcp_nr(zc0[e]);
-      T d0 = mul(zc1[e], rc);
-      T d1 = mul(fmaop(-d0, zc0[e], zc1[e]), rc);
-      TF<T> a = two_sum_u(core.v, -d0);
-      T t0 = add(a.v, add(add(a.e, core.e), sub(mul(mul(T(0.5), d0), d0), d1)));
+      bool hard0;
+      T t0 = rn_guard(core.v, sub(core.e, mul(zc1[e], rc)), hard0);
+      ok[e] = ok[e] && !hard0;
       T t1 = add(core.e, sub(core.v, t0));
       // final value part log1p(y0) = log(w) - log1p(y1 / (1 + y0))
       // 1 + y0 ~ w0 = zc0 * 2^n: divide in the scaled domain (1/(1 + y0) can
       // underflow the approximate reciprocal when y0 ~ FLT_MAX)
-      T dd = mul(mul(y1[e], C::p2(-n[e])), rcp_nr(zc0[e]));
+      T dd = mul(mul(y1[e], C::p2(-n[e])), rc);
       bool hard;
       T zz = rn_guard(core.v, sub(core.e, fmaop(mul(T(-0.5), dd), dd, dd)), hard);
       ok[e] = ok[e] && !hard;

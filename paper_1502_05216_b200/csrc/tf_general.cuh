@@ -66,6 +66,17 @@ TF_DEV double rcp_nr(double x) {
   double e = fmaop(-x, r, 1.0);
   return fmaop(r, e, r);
 }
+// bare MUFU reciprocal (~2^-22): for corrections that only need a few bits
+TF_DEV double rcp_approx(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+TF_DEV float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 TF_DEV float rcp_nr(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
