@@ -69,7 +69,7 @@ constexpr uint32_t B32_TWO = 0x40000000u;
 
 // the same bands as high words (conservative where marked "<")
 constexpr uint32_t H64_TEXP_POS = 0x40862e14u;  // |x| <= 709.76...
-constexpr uint32_t H64_TEXP_NEG = 0x40857800u;  // |x| <= 687.0...
+constexpr uint32_t H64_TEXP_NEG = 0x408622e1u;  // |x| < 708.3907 (exp normal)
 constexpr uint32_t H64_X1_TINY = 0x3e400000u;   // < 2^-27
 constexpr uint32_t H64_TINY54 = 0x3c900000u;    // < 2^-54
 constexpr uint32_t H64_LN2 = 0x3fe62e42u;       // < LN2 (slightly conservative)
@@ -252,18 +252,6 @@ TF_DEV void pexpm10_inband_v(const STab<T>& tb, const T (&x)[VW], TF<T> (&w)[VW]
   }
 }
 
-// expm1(x1) for a tiny twofold tail: x + x^2/2 + x^3/6, correctly rounded
-// (|x| < 2^-27 for binary64, < 2^-16 for binary32 via binary64).
-TF_DEV double t1_tiny(double x) {
-  double r = fmaop(mul(x, x), fmaop(x, 0x1.5555555555555p-3, 0.5), x);
-  return zbits(x) ? x : r;
-}
-TF_DEV float t1_tiny(float x) {
-  double d = (double)x;
-  double r = fmaop(mul(d, d), fmaop(d, 0x1.5555555555555p-3, 0.5), d);
-  return zbits(x) ? x : __double2float_rn(r);
-}
-
 // 2^k for k in [-1074, 1023], branch-free
 TF_DEV double p2d_bf(int k) {
   long long nb = (long long)(k + 1023) << 52;
@@ -327,8 +315,15 @@ TF_DEV void fast_texp(const STab<double>& tb, const double (&x0)[VW], const doub
   for (int e = 0; e < VW; ++e) {
     TF<double> ct = t_mul_u(tv<double>(tb.C[n[e] - P<double>::C_LO]), t[e]);
     TF<double> v = t_mul_u(tv<double>(tb.E[m[e] - P<double>::E_LO]), ct);
-    z0[e] = add(v.v, v.e);                                      // CR exp(x0)
-    z1[e] = add(mul(z0[e], t1_tiny(x1[e])), add(v.e, sub(v.v, z0[e])));  // explog.py:275
+    double zz = add(v.v, v.e);                                  // CR exp(x0)
+    if (m[e] <= TF64_ESC_LO + TF64_ESC_COUNT - 1) {
+      // e^x < 2^-987: the unscaled product's residuals underflow, so round the
+      // value part from the 2^128-scaled coarse entry (result normal: exact unscale)
+      TF<double> vs = t_mul_u(tv<double>(tb.ESC[m[e] - TF64_ESC_LO]), ct);
+      zz = mul(add(vs.v, vs.e), 0x1p-128);
+    }
+    z0[e] = zz;
+    z1[e] = add(mul(zz, t1_tiny(x1[e])), add(v.e, sub(v.v, zz)));  // explog.py:275
   }
 }
 

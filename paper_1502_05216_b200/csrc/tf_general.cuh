@@ -59,6 +59,12 @@ TF_DEV double ldexp_d(double x, int k) {
   return mul(x, p2d(k));
 }
 
+// biased exponent continuing through the subnormals (2^(e - 1023) <= |x|)
+TF_DEV int eexp_g(double x) {
+  int b = bexp(x);
+  return b ? b : 12 - __clzll((long long)(ubits(x) & 0x000fffffffffffffull));
+}
+
 // reciprocal of x in [0.5, 2]: MUFU approximation + one Newton step (~2^-44)
 TF_DEV double rcp_nr(double x) {
   double r;
@@ -222,6 +228,19 @@ TF_DEV double exp_cr(double x) {
   return add(v.v, v.e);
 }
 
+// expm1(x1) for a tiny twofold tail: x + x^2/2 + x^3/6, correctly rounded
+// (|x| < 2^-27 for binary64, < 2^-16 for binary32 via binary64); also the t1
+// of the fast kernels, so both paths produce the same bits.
+TF_DEV double t1_tiny(double x) {
+  double r = fmaop(mul(x, x), fmaop(x, 0x1.5555555555555p-3, 0.5), x);
+  return zbits(x) ? x : r;
+}
+TF_DEV float t1_tiny(float x) {
+  double d = (double)x;
+  double r = fmaop(mul(d, d), fmaop(d, 0x1.5555555555555p-3, 0.5), d);
+  return zbits(x) ? x : __double2float_rn(r);
+}
+
 TF_DEV double expm1_cr(double x) {
   if (is_nan(x) || x == 0.0) return x;
   if (abits(x) < 0x3c90000000000000ull) return x;   // |x| < 2^-54
@@ -261,6 +280,14 @@ TF_DEV float expm1_cr(float x) {
   if (x < -18.0f) return -1.0f;
   TF<double> w = pexpm10_raw_c((double)x);
   return rn32_twofold(w.v, w.e);
+}
+
+// t1 = expm1(x1) (explog.py:273, 307): the tail of a coupled input is tiny
+TF_DEV double expm1_t1(double x) {
+  return ((uint32_t)hi32(x) & 0x7fffffffu) < 0x3e400000u ? t1_tiny(x) : expm1_cr(x);
+}
+TF_DEV float expm1_t1(float x) {
+  return (ubits(x) & 0x7fffffffu) < 0x37800000u ? t1_tiny(x) : expm1_cr(x);
 }
 
 // ------------------------------------------------------------ log cores
@@ -472,18 +499,34 @@ TF_DEV float log1p_cr(float y) {
 // ExpLog.texp (explog.py:265-275)
 template <class T> TF_DEV TF<T> texp_gen(T x0, T x1) {
   TF<T> v = pexp0_raw_c(x0);
-  T z0 = exp_cr(x0);
+  T z0;
+  if constexpr (sizeof(T) == 8) {
+    // inside [-687, 709.76] the raw core is normal and accurate: RN(v0 + v1) is
+    // exp_cr(x0) without a second evaluation
+    uint32_t h = (uint32_t)hi32(x0);
+    bool band = (h & 0x7fffffffu) <= ((int)h < 0 ? 0x40857800u : 0x40862e14u);
+    z0 = band ? add(v.v, v.e) : exp_cr(x0);
+  } else {
+    z0 = exp_cr(x0);
+  }
   if (z0 == v.v && is_inf(z0)) return mk(z0, z0);
-  T t1 = expm1_cr(x1);
+  T t1 = expm1_t1(x1);
   return mk(z0, add(mul(z0, t1), add(v.e, sub(v.v, z0))));
 }
 
 // ExpLog.texpm1 (explog.py:299-310)
 template <class T> TF_DEV TF<T> texpm1_gen(T x0, T x1) {
   TF<T> w = pexpm10_raw_c(x0);
-  T z0 = expm1_cr(x0);
+  T z0;
+  if constexpr (sizeof(T) == 8) {
+    // the same RN(w0 + w1) expm1_cr computes for these x, without re-evaluating
+    bool reuse = x0 >= -38.0 && x0 <= 709.0 && abits(x0) >= 0x3c90000000000000ull;
+    z0 = reuse ? add(w.v, w.e) : expm1_cr(x0);
+  } else {
+    z0 = expm1_cr(x0);
+  }
   if (z0 == w.v && is_inf(z0)) return mk(z0, z0);
-  T t1 = expm1_cr(x1);
+  T t1 = expm1_t1(x1);
   T tail = add(w.e, sub(w.v, z0));
   return mk(z0, add(mul(add(z0, T(1)), t1), tail));
 }
@@ -498,20 +541,53 @@ template <class T> TF_DEV TF<T> correct_c(TF<T> core, T lib0) {
 template <class T> TF_DEV TF<T> tlog_gen(T y0, T y1) {
   TF<T> v = renorm_c(mk(y0, y1));
   TF<T> core = log_core_c(v.v, v.e);
-  return correct_c(core, log_cr(y0));
+  T lib0;
+  if constexpr (sizeof(T) == 8) {
+    // y1 == 0: the core IS log_core(y0, 0), the core log_cr would recompute
+    bool reuse = y1 == 0.0 && y0 > 0.0 && is_finite(y0) && abits(sub(y0, 1.0)) > NEAR1_64;
+    lib0 = reuse ? add(core.v, core.e) : log_cr(y0);
+  } else {
+    lib0 = log_cr(y0);
+  }
+  return correct_c(core, lib0);
 }
 
 // ExpLog.tlog1p (explog.py:440-467) incl. tlogp for the out-of-band branch
 template <class T> TF_DEV TF<T> tlog1p_gen(T y0, T y1) {
   TF<T> v = renorm_c(mk(y0, y1));
-  TF<T> core;
-  if (v.v < T(-0.5) || v.v > T(1)) {
+  TF<T> core, raw;
+  bool oob = v.v < T(-0.5) || v.v > T(1);
+  if (oob) {
     TF<T> w = renorm_c(t_add_d_c(v, T(1)));
-    core = correct_c(log_core_c(w.v, w.e), log_cr(w.v));     // tlogp (389-392)
+    raw = log_core_c(w.v, w.e);
+    T lw0;
+    if constexpr (sizeof(T) == 8) {
+      // log(w0) = log(w) - log1p(w1/w0): w is renormalized (|w1/w0| <= 2^-53)
+      // and out of band (|log w0| > 0.4), so one correction term is exact enough
+      bool fine = is_finite(raw.v) && is_finite(w.v) && w.v > 0.0 && !zbits(w.v);
+      lw0 = fine ? add(raw.v, sub(raw.e, __ddiv_rn(w.e, w.v))) : log_cr(w.v);
+    } else {
+      lw0 = log_cr(w.v);
+    }
+    core = correct_c(raw, lw0);                                  // tlogp (389-392)
   } else {
     core = log1p_core_c(v.v, v.e);
+    raw = core;
   }
-  return correct_c(core, log1p_cr(y0));
+  T lib0;
+  if constexpr (sizeof(T) == 8) {
+    // log1p(y0) = log1p(v) - log1p(y1 / (1 + y0)) (renorm is error-free); when
+    // |y1| <= 2^-50 (1 + y0) the quotient is negligible beyond its first term
+    // (near y0 = -1, e.g. the cfg-2 clamp, 1 + y0 is tiny and this falls back)
+    double a1 = add(1.0, y0);
+    bool coupled = is_finite(y0) && is_finite(raw.v) && is_finite(raw.e) && a1 > 0.0 &&
+                   abits(y0) >= 0x3c90000000000000ull &&
+                   (zbits(y1) || (is_finite(y1) && eexp_g(y1) + 50 <= eexp_g(a1)));
+    lib0 = coupled ? add(raw.v, sub(raw.e, __ddiv_rn(y1, a1))) : log1p_cr(y0);
+  } else {
+    lib0 = log1p_cr(y0);
+  }
+  return correct_c(core, lib0);
 }
 
 enum Fn { FN_TEXP = 0, FN_TEXPM1 = 1, FN_TLOG = 2, FN_TLOG1P = 3 };
