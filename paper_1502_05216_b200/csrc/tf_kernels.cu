@@ -158,10 +158,13 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
       st<T, VW>(z0, vi, r0);
       st<T, VW>(z1, vi, r1);
     }
+    bool anyrare = false;
 #pragma unroll
-    for (int e = 0; e < VW; ++e) {
-      unsigned mask = __ballot_sync(0xffffffffu, rare[e]);
-      if (mask) {
+    for (int e = 0; e < VW; ++e) anyrare |= rare[e];
+    if (__any_sync(0xffffffffu, anyrare)) {  // one vote in the common all-fast case
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        unsigned mask = __ballot_sync(0xffffffffu, rare[e]);
         if (rare[e]) q[qn + __popc(mask & ((1u << lane) - 1u))] = vi * VW + e;
         qn += __popc(mask);
       }
