@@ -26,6 +26,28 @@ TF_DEV float sub(float a, float b) { return __fsub_rn(a, b); }
 TF_DEV float mul(float a, float b) { return __fmul_rn(a, b); }
 TF_DEV float fmaop(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 
+// Packed binary32 pairs: Blackwell's FADD2/FMUL2/FFMA2 evaluate two IEEE
+// round-to-nearest binary32 ops per instruction (same FP32 pipe rate, half the
+// issue slots).  Two independent lanes of a binary32 kernel ride in one f2.
+struct f2 { unsigned long long u; };
+TF_DEV f2 pk(float a, float b) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.u) : "f"(a), "f"(b));
+  return r;
+}
+TF_DEV float lo(f2 x) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.u)); return a; }
+TF_DEV float hi(f2 x) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.u)); return b; }
+TF_DEV f2 add(f2 a, f2 b) { f2 r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(a.u), "l"(b.u)); return r; }
+TF_DEV f2 sub(f2 a, f2 b) { f2 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(a.u), "l"(b.u)); return r; }
+TF_DEV f2 mul(f2 a, f2 b) { f2 r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(a.u), "l"(b.u)); return r; }
+TF_DEV f2 fmaop(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.u) : "l"(a.u), "l"(b.u), "l"(c.u));
+  return r;
+}
+TF_DEV f2 operator-(f2 a) { a.u ^= 0x8000000080000000ull; return a; }
+TF_DEV f2 splat(float c) { return pk(c, c); }
+
 // ------------------------------------------------- integer-pipe classifiers
 TF_DEV int hi32(double x) { return __double2hiint(x); }
 TF_DEV uint32_t ubits(float x) { return __float_as_uint(x); }

@@ -156,6 +156,30 @@ template <int VW> TF_DEV void taylor_exp_v(const double (&y)[VW], TF<double> (&t
   }
 }
 template <int VW> TF_DEV void taylor_exp_v(const float (&y)[VW], TF<float> (&t)[VW]) {
+  if constexpr (VW % 2 == 0) {  // lane pairs on FADD2/FMUL2/FFMA2
+    constexpr int NP = VW / 2;
+    f2 yp[NP];
+    TF<f2> tp[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      yp[p] = pk(y[2 * p], y[2 * p + 1]);
+      f2 s = add(yp[p], splat(6.0f));
+      s = add(mul(s, yp[p]), splat(30.0f));
+      tp[p] = mk(s, splat(0.0f));
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const f2 c = splat(c_texp32[k]);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) tp[p] = t_add_d_u(t_mul_d_u(tp[p], yp[p]), c);
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      t[2 * p] = mk(lo(tp[p].v), lo(tp[p].e));
+      t[2 * p + 1] = mk(hi(tp[p].v), hi(tp[p].e));
+    }
+    return;
+  }
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
     float s = add(y[e], 6.0f);
@@ -188,6 +212,31 @@ template <int VW> TF_DEV void taylor_expm1_v(const double (&y)[VW], TF<double> (
     t[e] = t_mul_u(t_mul_d_u(t[e], y[e]), mk(P<double>::INVF_V, P<double>::INVF_E));
 }
 template <int VW> TF_DEV void taylor_expm1_v(const float (&y)[VW], TF<float> (&t)[VW]) {
+  if constexpr (VW % 2 == 0) {
+    constexpr int NP = VW / 2;
+    f2 yp[NP];
+    TF<f2> tp[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      yp[p] = pk(y[2 * p], y[2 * p + 1]);
+      f2 s = add(yp[p], splat(5.0f));
+      s = add(mul(s, yp[p]), splat(20.0f));
+      tp[p] = mk(s, splat(0.0f));
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const f2 c = splat(c_texpm1_32[k]);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) tp[p] = t_add_d_u(t_mul_d_u(tp[p], yp[p]), c);
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      tp[p] = t_mul_u(t_mul_d_u(tp[p], yp[p]), mk(splat(P<float>::INVF_V), splat(P<float>::INVF_E)));
+      t[2 * p] = mk(lo(tp[p].v), lo(tp[p].e));
+      t[2 * p + 1] = mk(hi(tp[p].v), hi(tp[p].e));
+    }
+    return;
+  }
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
     float s = add(y[e], 5.0f);
