@@ -39,12 +39,15 @@ TF_DEV float lo(f2 x) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(
 TF_DEV float hi(f2 x) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.u)); return b; }
 TF_DEV f2 add(f2 a, f2 b) { f2 r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(a.u), "l"(b.u)); return r; }
 TF_DEV f2 sub(f2 a, f2 b) { f2 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(a.u), "l"(b.u)); return r; }
-// ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even under
-// -fmad=false, which would change the reference's rounding; a product is
-// therefore issued as fma(a, b, -0) -- RN(a*b) exactly, and not fusable.
+// ptxas (CUDA 12.9) contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even
+// under -fmad=false (and rewrites fma(a, b, -0) back into FMUL2 first), which
+// would change the reference's rounding.  A product is therefore issued as
+// fma(a, b, z) with z = (-0, -0) read from constant memory: RN(a*b) exactly,
+// but opaque to ptxas, so it can neither be turned into FMUL2 nor fused.
+__constant__ unsigned long long c_nz2 = 0x8000000080000000ull;
 TF_DEV f2 mul(f2 a, f2 b) {
   f2 r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.u) : "l"(a.u), "l"(b.u), "l"(0x8000000080000000ull));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.u) : "l"(a.u), "l"(b.u), "l"(c_nz2));
   return r;
 }
 TF_DEV f2 fmaop(f2 a, f2 b, f2 c) {
