@@ -155,37 +155,6 @@ template <int VW> TF_DEV void taylor_exp_v(const double (&y)[VW], TF<double> (&t
     for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_u(t[e], y[e]), c);
   }
 }
-// packed single-pair cores (lanes 2p, 2p+1)
-TF_DEV TF<f2> taylor_exp_p(f2 yp) {
-  f2 s = add(yp, splat(6.0f));
-  s = add(mul(s, yp), splat(30.0f));
-  TF<f2> t = mk(s, splat(0.0f));
-#pragma unroll
-  for (int k = 0; k < 4; ++k) t = t_add_d_u(t_mul_d_u(t, yp), splat(c_texp32[k]));
-  return t;
-}
-TF_DEV TF<f2> pk2(float2 a, float2 b) { return mk(pk(a.x, b.x), pk(a.y, b.y)); }
-
-// RN(h + l) for a lane pair with the binary32 near-boundary guard (rn_guard)
-template <int TOL>
-TF_DEV f2 rn_guard2(f2 h, f2 l, bool& hard0, bool& hard1) {
-  f2 z = add(h, l);
-  f2 rho = add(sub(h, z), l);
-  const float ztab[2] = {lo(z), hi(z)}, rtab[2] = {lo(rho), hi(rho)};
-  bool hard[2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    float zz = ztab[i], r = rtab[i];
-    float half = __int_as_float(max(bexp(zz) - 24, 1) << 23);
-    float tol = __int_as_float((127 + TOL) << 23) * fabsf(zz);
-    bool pow2 = (ubits(zz) & 0x7fffffu) == 0u;
-    hard[i] = fabsf(fabsf(r) - half) <= tol || (pow2 && fabsf(fabsf(r) - 0.5f * half) <= tol);
-  }
-  hard0 = hard[0];
-  hard1 = hard[1];
-  return z;
-}
-
 template <int VW> TF_DEV void taylor_exp_v(const float (&y)[VW], TF<float> (&t)[VW]) {
   if constexpr (VW % 2 == 0) {  // lane pairs on FADD2/FMUL2/FFMA2
     constexpr int NP = VW / 2;
@@ -418,28 +387,6 @@ TF_DEV void fast_texp(const STab<float>& tb, const float (&x0)[VW], const float 
             ahi(x1[e]) < B32_X1_TINY;
     decomp_exp_u(ok[e] ? x0[e] : 0.0f, m[e], n[e], y[e]);
   }
-  if constexpr (VW % 2 == 0) {  // lane pairs end to end on FADD2/FMUL2/FFMA2
-#pragma unroll
-    for (int p = 0; p < VW / 2; ++p) {
-      const int a = 2 * p, b = 2 * p + 1;
-      TF<f2> t = taylor_exp_p(pk(y[a], y[b]));
-      TF<f2> ct = t_mul_u(pk2(tb.C[n[a] - P<float>::C_LO], tb.C[n[b] - P<float>::C_LO]), t);
-      float2 ea = tb.E[m[a] - P<float>::E_LO], eb = tb.E[m[b] - P<float>::E_LO];
-      TF<f2> v = t_mul_u(pk2(ea, eb), ct);
-      bool sa = m[a] <= -35, sb = m[b] <= -35;  // e^(2m) < 2^-100: scaled coarse entry
-      float2 esa = sa ? tb.ESC[m[a] - TF32_ESC_LO] : ea;
-      float2 esb = sb ? tb.ESC[m[b] - TF32_ESC_LO] : eb;
-      TF<f2> vs = t_mul_u(pk2(esa, esb), ct);
-      bool ha, hb;
-      f2 zz = mul(rn_guard2<-35>(vs.v, vs.e, ha, hb), pk(sa ? 0x1p-64f : 1.0f, sb ? 0x1p-64f : 1.0f));
-      ok[a] = ok[a] && !ha;
-      ok[b] = ok[b] && !hb;
-      f2 zt = add(mul(zz, pk(t1_tiny(x1[a]), t1_tiny(x1[b]))), add(v.e, sub(v.v, zz)));
-      z0[a] = lo(zz); z0[b] = hi(zz);
-      z1[a] = lo(zt); z1[b] = hi(zt);
-    }
-    return;
-  }
   TF<float> t[VW];
   taylor_exp_v<VW>(y, t);
 #pragma unroll
@@ -492,25 +439,6 @@ TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const floa
     ok[e] = ax > B32_LN2 && ax <= (sgn(x0[e]) ? B32_LO : B32_TEXP_POS) &&
             ahi(x1[e]) < B32_X1_TINY;
     decomp_exp_u(ok[e] ? x0[e] : 1.0f, m[e], n[e], y[e]);
-  }
-  if constexpr (VW % 2 == 0) {
-#pragma unroll
-    for (int p = 0; p < VW / 2; ++p) {
-      const int a = 2 * p, b = 2 * p + 1;
-      TF<f2> t = taylor_exp_p(pk(y[a], y[b]));
-      TF<f2> ct = t_mul_u(pk2(tb.C[n[a] - P<float>::C_LO], tb.C[n[b] - P<float>::C_LO]), t);
-      TF<f2> v = t_mul_u(pk2(tb.E[m[a] - P<float>::E_LO], tb.E[m[b] - P<float>::E_LO]), ct);
-      TF<f2> w = t_add_d_u(v, splat(-1.0f));                    // expcore.py:147
-      bool ha, hb;
-      f2 zz = rn_guard2<-35>(w.v, w.e, ha, hb);
-      ok[a] = ok[a] && !ha;
-      ok[b] = ok[b] && !hb;
-      f2 tail = add(w.e, sub(w.v, zz));
-      f2 zt = add(mul(add(zz, splat(1.0f)), pk(t1_tiny(x1[a]), t1_tiny(x1[b]))), tail);
-      z0[a] = lo(zz); z0[b] = hi(zz);
-      z1[a] = lo(zt); z1[b] = hi(zt);
-    }
-    return;
   }
   TF<float> t[VW];
   taylor_exp_v<VW>(y, t);
