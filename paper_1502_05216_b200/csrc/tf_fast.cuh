@@ -155,14 +155,24 @@ template <int VW> TF_DEV void taylor_exp_v(const double (&y)[VW], TF<double> (&t
     for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_u(t[e], y[e]), c);
   }
 }
+// t_mul_d (eft.py:214-219) for lane pairs without a sign-flip instruction:
+// with nb = -b precomputed, fma(x0, nb, v) = RN(v - x0 b) = -e exactly, and
+// x1 b + e = x1 b - (-e) is the same IEEE addition.
+TF_DEV TF<f2> t_mul_d_p(TF<f2> x, f2 b, f2 nb) {
+  f2 v = mul(x.v, b);
+  f2 ne = fmaop(x.v, nb, v);
+  return mk(v, sub(mul(x.e, b), ne));
+}
+
 template <int VW> TF_DEV void taylor_exp_v(const float (&y)[VW], TF<float> (&t)[VW]) {
   if constexpr (VW % 2 == 0) {  // lane pairs on FADD2/FMUL2/FFMA2
     constexpr int NP = VW / 2;
-    f2 yp[NP];
+    f2 yp[NP], nyp[NP];
     TF<f2> tp[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       yp[p] = pk(y[2 * p], y[2 * p + 1]);
+      nyp[p] = pk(-y[2 * p], -y[2 * p + 1]);
       f2 s = add(yp[p], splat(6.0f));
       s = add(mul(s, yp[p]), splat(30.0f));
       tp[p] = mk(s, splat(0.0f));
@@ -171,7 +181,7 @@ template <int VW> TF_DEV void taylor_exp_v(const float (&y)[VW], TF<float> (&t)[
     for (int k = 0; k < 4; ++k) {
       const f2 c = splat(c_texp32[k]);
 #pragma unroll
-      for (int p = 0; p < NP; ++p) tp[p] = t_add_d_u(t_mul_d_u(tp[p], yp[p]), c);
+      for (int p = 0; p < NP; ++p) tp[p] = t_add_d_u(t_mul_d_p(tp[p], yp[p], nyp[p]), c);
     }
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -214,11 +224,12 @@ template <int VW> TF_DEV void taylor_expm1_v(const double (&y)[VW], TF<double> (
 template <int VW> TF_DEV void taylor_expm1_v(const float (&y)[VW], TF<float> (&t)[VW]) {
   if constexpr (VW % 2 == 0) {
     constexpr int NP = VW / 2;
-    f2 yp[NP];
+    f2 yp[NP], nyp[NP];
     TF<f2> tp[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       yp[p] = pk(y[2 * p], y[2 * p + 1]);
+      nyp[p] = pk(-y[2 * p], -y[2 * p + 1]);
       f2 s = add(yp[p], splat(5.0f));
       s = add(mul(s, yp[p]), splat(20.0f));
       tp[p] = mk(s, splat(0.0f));
@@ -227,11 +238,11 @@ template <int VW> TF_DEV void taylor_expm1_v(const float (&y)[VW], TF<float> (&t
     for (int k = 0; k < 2; ++k) {
       const f2 c = splat(c_texpm1_32[k]);
 #pragma unroll
-      for (int p = 0; p < NP; ++p) tp[p] = t_add_d_u(t_mul_d_u(tp[p], yp[p]), c);
+      for (int p = 0; p < NP; ++p) tp[p] = t_add_d_u(t_mul_d_p(tp[p], yp[p], nyp[p]), c);
     }
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      tp[p] = t_mul_u(t_mul_d_u(tp[p], yp[p]), mk(splat(P<float>::INVF_V), splat(P<float>::INVF_E)));
+      tp[p] = t_mul_u(t_mul_d_p(tp[p], yp[p], nyp[p]), mk(splat(P<float>::INVF_V), splat(P<float>::INVF_E)));
       t[2 * p] = mk(lo(tp[p].v), lo(tp[p].e));
       t[2 * p + 1] = mk(hi(tp[p].v), hi(tp[p].e));
     }
