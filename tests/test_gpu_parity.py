@@ -146,3 +146,68 @@ def test_config_sample_vs_oracle(cfg, cuda):
         assert strict["class_mismatch"] == 0 and strict["tol_violations"] == 0, strict
         assert strict["z0_mismatch"] <= max(2, n // 100_000), strict
         assert ref["class_mismatch"] == 0, ref
+
+
+FULL = {
+    # config -> full BASELINE.json size (cfg 5 is the 2^30 sharded set; one GPU
+    # holds all of it: 4 arrays x 8 GiB)
+    "cfg1_texp_f64": 1 << 20,
+    "cfg2_texpm1_f64": 1 << 24,
+    "cfg2_tlog1p_f64": 1 << 24,
+    "cfg3_tlog_f64": 1 << 26,
+    "cfg4_texp_f32": 1 << 28,
+    "cfg4_texpm1_f32": 1 << 28,
+    "cfg4_tlog_f32": 1 << 28,
+    "cfg4_tlog1p_f32": 1 << 28,
+    "cfg5_texp_f64": 1 << 30,
+    "cfg5_tlog_f64": 1 << 30,
+}
+
+
+@pytest.mark.parametrize("cfg", sorted(FULL))
+def test_full_size_config(cfg, cuda):
+    """Whole BASELINE.json configs on the device: a strided sample against the
+    oracle, plus size-independent invariants over every element (the non-finite
+    census implied by the domain bounds, and no exact-path leakage of NaN)."""
+    import torch
+
+    from paper_1502_05216_b200 import _lib, api, workloads
+
+    fn, width, dist, n = workloads.CONFIGS[cfg]
+    n = FULL[cfg]
+    dt = torch.float64 if width == 64 else torch.float32
+    L = _lib.ensure_device(cuda.index)
+    x0 = torch.empty(n, dtype=dt, device=cuda)
+    x1 = torch.empty(n, dtype=dt, device=cuda)
+    _lib.check(L.tf_generate(_lib.DIST_CODES[dist], 1, 0, n, x0.data_ptr(), x1.data_ptr(), None),
+               "gen")
+    z = getattr(api(width), fn)((x0, x1))
+    z0, z1 = z.value, z.error
+    torch.cuda.synchronize()
+    # strided sample vs the oracle (reference algorithm)
+    stride = max(1, n // (1 << 16))
+    s0 = x0[::stride].cpu().numpy()
+    s1 = x1[::stride].cpu().numpy()
+    r = compare(z0[::stride].cpu().numpy(), z1[::stride].cpu().numpy(),
+                *O.evaluate(fn, width, s0, s1, backend="dv"), width)
+    assert r["class_mismatch"] == 0, r
+    if width == 64:
+        assert r["tol_violations"] == 0 and r["z0_gt1ulp"] == 0, r
+    # invariants over all n elements
+    if fn == "texp":
+        hi = float.fromhex("0x1.62e42fefa39f0p+9") if width == 64 else 88.72283935546875
+        assert torch.equal(torch.isnan(z0), torch.isnan(x0))
+        assert torch.equal(torch.isinf(z0), x0 >= hi)
+        assert bool((z0[~torch.isnan(x0)] >= 0).all())
+    elif fn == "texpm1":
+        assert torch.equal(torch.isnan(z0), torch.isnan(x0))
+        assert bool((z0[~torch.isnan(x0)] >= -1).all())
+    elif fn == "tlog":
+        assert torch.equal(torch.isnan(z0), torch.isnan(x0) | (x0 < 0))
+        assert torch.equal(z0 == -float("inf"), x0 == 0)
+    else:
+        assert torch.equal(torch.isnan(z0), torch.isnan(x0) | (x0 < -1))
+    fin = torch.isfinite(z0) & torch.isfinite(x0) & torch.isfinite(x1)
+    assert not bool(torch.isnan(z1[fin]).any())
+    del x0, x1, z0, z1, z
+    torch.cuda.empty_cache()
