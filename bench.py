@@ -332,9 +332,19 @@ def run_ours(args):
     dom_ms = kern_ms[dom]
     ops = ALG_OPS[(dom, 64)] * n / (dom_ms * 1e-3)
     gbs = 32 * n / (dom_ms * 1e-3) / 1e9
+    traffic = args.traffic
+    if traffic is None:
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                rec = json.load(f).get(f"k_eval<double,{dom}>")
+            if rec:  # per launch of the same size (ncu --set full capture)
+                traffic = rec["traffic_bytes"] * n / rec["elements"]
+        except (OSError, ValueError, KeyError):
+            traffic = None
     roof = {"bound": "fp64", "kernel": f"k_eval<double,{dom}>",
             "achieved": ops / 1e12, "peak": peak[64] / 1e12, "unit": "TFLOP/s",
-            "frac": ops / peak[64], "traffic": args.traffic,
+            "frac": ops / peak[64], "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
+            "algorithmic_bytes": 32 * n,
             "ops_per_element": ALG_OPS[(dom, 64)], "elements_per_launch": n,
             "launch_ms": dom_ms, "peak_source": "measured tf_fma_peak, best of DADD/DMUL/DFMA chains (this GPU, this run)",
             "hbm_achieved_gbs": gbs, "hbm_peak_gbs": _peaks()["hbm_gbs"],
