@@ -12,7 +12,7 @@ import subprocess
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libtwofold_b200.so")
+LIB_PATH = os.environ.get("TWOFOLD_B200_LIB") or os.path.join(HERE, "lib", "libtwofold_b200.so")
 CSRC = os.path.join(HERE, "csrc")
 
 TF_OK, TF_ERR_ARG, TF_ERR_CUDA = 0, -1, -2

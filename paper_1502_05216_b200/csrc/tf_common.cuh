@@ -35,8 +35,8 @@ TF_DEV f2 pk(float a, float b) {
   asm("mov.b64 %0, {%1, %2};" : "=l"(r.u) : "f"(a), "f"(b));
   return r;
 }
-TF_DEV float lo(f2 x) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.u)); return a; }
-TF_DEV float hi(f2 x) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.u)); return b; }
+TF_DEV float lo(f2 x) { return __uint_as_float((unsigned)(x.u & 0xffffffffull)); }
+TF_DEV float hi(f2 x) { return __uint_as_float((unsigned)(x.u >> 32)); }
 TF_DEV f2 add(f2 a, f2 b) { f2 r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(a.u), "l"(b.u)); return r; }
 TF_DEV f2 sub(f2 a, f2 b) { f2 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(a.u), "l"(b.u)); return r; }
 // ptxas (CUDA 12.9) contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even

@@ -188,8 +188,7 @@ template <int VW> TF_DEV void taylor_exp_v(const float (&y)[VW], TF<float> (&t)[
       t[2 * p] = mk(lo(tp[p].v), lo(tp[p].e));
       t[2 * p + 1] = mk(hi(tp[p].v), hi(tp[p].e));
     }
-    return;
-  }
+  } else {
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
     float s = add(y[e], 6.0f);
@@ -201,6 +200,7 @@ template <int VW> TF_DEV void taylor_exp_v(const float (&y)[VW], TF<float> (&t)[
     const float c = c_texp32[k];
 #pragma unroll
     for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_u(t[e], y[e]), c);
+  }
   }
 }
 template <int VW> TF_DEV void taylor_expm1_v(const double (&y)[VW], TF<double> (&t)[VW]) {
@@ -246,8 +246,7 @@ template <int VW> TF_DEV void taylor_expm1_v(const float (&y)[VW], TF<float> (&t
       t[2 * p] = mk(lo(tp[p].v), lo(tp[p].e));
       t[2 * p + 1] = mk(hi(tp[p].v), hi(tp[p].e));
     }
-    return;
-  }
+  } else {
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
     float s = add(y[e], 5.0f);
@@ -263,6 +262,7 @@ template <int VW> TF_DEV void taylor_expm1_v(const float (&y)[VW], TF<float> (&t
 #pragma unroll
   for (int e = 0; e < VW; ++e)
     t[e] = t_mul_u(t_mul_d_u(t[e], y[e]), mk(P<float>::INVF_V, P<float>::INVF_E));
+  }
 }
 
 // decompose_exp via the magic constant: M = round-half-even(x * 32) in the

@@ -21,11 +21,15 @@
 
 namespace tf {
 
-constexpr int BLOCK = 256;
 #ifndef TF_MINB
 #define TF_MINB 4
 #endif
-constexpr int WARPS = BLOCK / 32;
+#ifndef TF_MINB4
+#define TF_MINB4 2
+#endif
+#ifndef TF_VW64
+#define TF_VW64 2
+#endif
 
 __device__ unsigned long long g_rare_count = 0;
 
@@ -52,11 +56,23 @@ TF_DEV void st(T* p, uint64_t vi, const T (&a)[VW]) {
   if constexpr (VW == 1) {
     __stcs(p + vi, a[0]);
   } else if constexpr (sizeof(T) == 8) {
-    __stcs(reinterpret_cast<double2*>(p) + vi, make_double2(a[0], a[1]));
+#pragma unroll
+    for (int c = 0; c < VW / 2; ++c)
+      __stcs(reinterpret_cast<double2*>(p) + vi * (VW / 2) + c, make_double2(a[2 * c], a[2 * c + 1]));
   } else {
-    __stcs(reinterpret_cast<float4*>(p) + vi, make_float4(a[0], a[1], a[2], a[3]));
+#pragma unroll
+    for (int c = 0; c < VW / 4; ++c)
+      __stcs(reinterpret_cast<float4*>(p) + vi * (VW / 4) + c,
+             make_float4(a[4 * c], a[4 * c + 1], a[4 * c + 2], a[4 * c + 3]));
   }
 }
+
+// lanes per thread and occupancy per (width, vector width)
+template <class T, int VW> struct KCfg {
+  static constexpr bool WIDE = sizeof(T) == 8 && VW == 4;   // 4 binary64 lanes per thread
+  static constexpr int BLOCK = WIDE ? 128 : 256;             // static smem stays < 48 KB
+  static constexpr int MINB = WIDE ? TF_MINB4 : TF_MINB;
+};
 
 // ---- asynchronous global -> shared staging (LDGSTS), one 16 B vector per
 // thread and array per stage: the loads of iteration i+STAGES-1 are in flight
@@ -93,12 +109,16 @@ TF_DEV void drain(const uint32_t* q, int cnt, const T* __restrict__ x0, const T*
 }
 
 template <class T, int FN, int VW>
-__global__ void __launch_bounds__(BLOCK, TF_MINB)
+__global__ void __launch_bounds__((KCfg<T, VW>::BLOCK), (KCfg<T, VW>::MINB))
 k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
        T* __restrict__ z1, uint32_t n, int flags) {
+  constexpr int BLOCK = KCfg<T, VW>::BLOCK;
+  constexpr int WARPS = BLOCK / 32;
   constexpr int QCAP = 32 + 32 * VW;
   constexpr int STAGES = 2;
-  constexpr bool ASYNC = VW * sizeof(T) == 16;
+  constexpr bool ASYNC = VW * sizeof(T) % 16 == 0;
+  constexpr int NC = VW * (int)sizeof(T) / 16;        // 16-byte chunks per thread
+  constexpr int EC = 16 / (int)sizeof(T);             // elements per chunk
   __shared__ STab<T> tb;
   __shared__ uint32_t qs[WARPS][QCAP];
   __shared__ __align__(16) T stg[ASYNC ? STAGES : 1][2][BLOCK][VW];
@@ -118,8 +138,11 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   if constexpr (ASYNC) {
     uint32_t vi = first + lane;
     bool v = vi < nvec;
-    cp_async16(stg[0][0][threadIdx.x], x0 + (v ? vi * VW : 0u), v);
-    cp_async16(stg[0][1][threadIdx.x], x1 + (v ? vi * VW : 0u), v);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      cp_async16(&stg[0][0][threadIdx.x][c * EC], x0 + (v ? vi * VW + c * EC : 0u), v);
+      cp_async16(&stg[0][1][threadIdx.x][c * EC], x1 + (v ? vi * VW + c * EC : 0u), v);
+    }
     cp_async_commit();
   }
   int cs = 0;
@@ -131,8 +154,11 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
     if constexpr (ASYNC) {
       uint32_t pv = vi + stride;
       bool pvalid = pv < nvec;
-      cp_async16(stg[cs ^ 1][0][threadIdx.x], x0 + (pvalid ? pv * VW : 0u), pvalid);
-      cp_async16(stg[cs ^ 1][1][threadIdx.x], x1 + (pvalid ? pv * VW : 0u), pvalid);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        cp_async16(&stg[cs ^ 1][0][threadIdx.x][c * EC], x0 + (pvalid ? pv * VW + c * EC : 0u), pvalid);
+        cp_async16(&stg[cs ^ 1][1][threadIdx.x][c * EC], x1 + (pvalid ? pv * VW + c * EC : 0u), pvalid);
+      }
       cp_async_commit();
       cp_async_wait<1>();
 #pragma unroll
@@ -394,16 +420,16 @@ int launch_one(const T* x0, const T* x1, T* z0, T* z1, int64_t n, cudaStream_t s
   static int occ = 0;
   if (!occ) {
     int v = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, tf::k_eval<T, FN, VW>, tf::BLOCK, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, tf::k_eval<T, FN, VW>, tf::KCfg<T, VW>::BLOCK, 0);
     occ = v > 0 ? v : 1;
   }
   const int64_t CHUNK = (int64_t)1 << 31;  // queue indices are 32-bit
   for (int64_t off = 0; off < n; off += CHUNK) {
     int64_t m = n - off < CHUNK ? n - off : CHUNK;
-    int64_t vecs = (m / VW + tf::BLOCK - 1) / tf::BLOCK;
+    int64_t vecs = (m / VW + tf::KCfg<T, VW>::BLOCK - 1) / tf::KCfg<T, VW>::BLOCK;
     int64_t grid = (int64_t)device_sms() * occ;
     if (vecs < grid) grid = vecs > 0 ? vecs : 1;
-    tf::k_eval<T, FN, VW><<<(unsigned)grid, tf::BLOCK, 0, s>>>(x0 + off, x1 + off, z0 + off,
+    tf::k_eval<T, FN, VW><<<(unsigned)grid, tf::KCfg<T, VW>::BLOCK, 0, s>>>(x0 + off, x1 + off, z0 + off,
                                                               z1 + off, (uint32_t)m, flags);
   }
   return cuda_check("k_eval launch");
@@ -417,7 +443,7 @@ int launch(const T* x0, const T* x1, T* z0, T* z1, int64_t n, void* stream, int 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uintptr_t al = (uintptr_t)x0 | (uintptr_t)x1 | (uintptr_t)z0 | (uintptr_t)z1;
   if ((al & 15) == 0) {
-    if constexpr (sizeof(T) == 8) return launch_one<T, FN, 2>(x0, x1, z0, z1, n, s, flags);
+    if constexpr (sizeof(T) == 8) return launch_one<T, FN, TF_VW64>(x0, x1, z0, z1, n, s, flags);
     else return launch_one<T, FN, 4>(x0, x1, z0, z1, n, s, flags);
   }
   if ((al & (sizeof(T) - 1)) != 0) return fail(TF_ERR_ARG, "misaligned pointer%s");
