@@ -473,7 +473,8 @@ TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const floa
 // and near 1 by the exact-d series (log_near1).
 template <class T> struct LogC;
 template <> struct LogC<double> {
-  static constexpr uint32_t NORM_SPAN = 2046u;
+  static constexpr uint32_t NORM_SPAN = 2044u;   // positive normal and < 2^1022: 2^-n normal
+  static constexpr uint32_t DMAX = (1023u - 40u) << 20;  // |d| < 2^-40 (tlog value part)
   static constexpr int SMALL = 50, EBIAS = 1022;
   static constexpr uint64_t HALF = B64_HALF, TWO = B64_TWO;
   static constexpr uint32_t LN2H = H64_LN2, NEAR1H = H64_NEAR1;
@@ -483,9 +484,13 @@ template <> struct LogC<double> {
     return __longlong_as_double((ubits(v) & 0x800fffffffffffffull) | (1022ull << 52));
   }
   TF_DEV static double p2(int k) { return p2d_bf(k); }
+  // 2^k for k in [-1022, 1023] (normal), two integer ops
+  TF_DEV static double p2n(int k) { return __hiloint2double((k + 1023) << 20, 0); }
+  TF_DEV static double rcp(double x) { return rcp_nr(x); }
 };
 template <> struct LogC<float> {
-  static constexpr uint32_t NORM_SPAN = 254u;
+  static constexpr uint32_t NORM_SPAN = 252u;
+  static constexpr uint32_t DMAX = (127u - 21u) << 23;   // |d| < 2^-21
   static constexpr int SMALL = 21, EBIAS = 126;
   static constexpr uint32_t HALF = B32_HALF, TWO = B32_TWO;
   static constexpr uint32_t LN2H = B32_LN2 + 1u, NEAR1H = NEAR1_32 + 1u;
@@ -495,6 +500,8 @@ template <> struct LogC<float> {
     return __int_as_float((ubits(v) & 0x807fffffu) | (126u << 23));
   }
   TF_DEV static float p2(int k) { return p2f_bf(k); }
+  TF_DEV static float p2n(int k) { return __int_as_float((k + 127) << 23); }
+  TF_DEV static float rcp(float x) { return rcp_approx(x); }
 };
 
 template <class T, int VW>
@@ -506,17 +513,19 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
   TF<T> v[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    uint32_t eb0 = C::eb(y0i[e]);                     // sign|exponent
-    ok[e] = eb0 - 1u < C::NORM_SPAN &&                 // positive normal y0
-            (zbits(y1i[e]) || eexp(y1i[e]) + C::SMALL <= (int)eb0);
+    // positive normal y0 (below 2^1022 / 2^126) and finite y1; how small y1 is
+    // against y0 is checked on d = y1/y0 below, where it matters
+    ok[e] = C::eb(y0i[e]) - 1u < C::NORM_SPAN && is_finite(y1i[e]);
     y0[e] = ok[e] ? y0i[e] : T(1);
     y1[e] = ok[e] ? y1i[e] : T(0);
     v[e] = renorm_u(mk(y0[e], y1[e]));
+    ok[e] = ok[e] && C::eb(v[e].v) - 1u < C::NORM_SPAN;
+    if (!ok[e]) v[e] = mk(T(1), T(0));
     auto vb = ubits(v[e].v);
     bool band = vb >= C::HALF && vb <= C::TWO;
     n[e] = band ? 0 : C::n_of(v[e].v);
     zc0[e] = band ? v[e].v : C::mant(v[e].v);
-    zc1[e] = band ? v[e].e : (zbits(v[e].e) ? T(0) : mul(v[e].e, C::p2(-n[e])));
+    zc1[e] = band ? v[e].e : (zbits(v[e].e) ? T(0) : mul(v[e].e, C::p2n(-n[e])));
     r0[e] = seed_log1p_t(add(sub(zc0[e], T(1)), zc1[e]),      // explog.py:346-349
                          [&](int i) { return tb.SEED[i]; });
     ok[e] = ok[e] && ahi(r0[e]) < C::LN2H;
@@ -536,7 +545,8 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     // to d = y1/y0 (|d| <= 2^-50 |log y0|, 2^-17 in binary32), so
     // log(y0) = core - d to well below an ulp with d known to ~2^-22:
     // y1 * 2^-n over zc0 (= v0 * 2^-n, within an ulp of y0 * 2^-n).
-    T d0 = mul(mul(y1[e], C::p2(-n[e])), rcp_approx(zc0[e]));
+    T d0 = mul(mul(y1[e], C::p2n(-n[e])), C::rcp(zc0[e]));
+    ok[e] = ok[e] && ahi(d0) < C::DMAX;
     bool hard;
     T zz = rn_guard(core.v, sub(core.e, d0), hard);
     T dl = sub(y0[e], T(1));                          // exact near 1
@@ -571,11 +581,8 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
   TF<T> v[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    // |y1| << |y0| keeps d = y1/(1+y0) tiny; below 2^-54 the value part is y0
-    // itself and no correction is needed, so any finite y1 is fine there
-    bool tiny0 = ahi(y0i[e]) < (D ? H64_TINY54 : B32_TINY25);
-    ok[e] = is_finite(y0i[e]) && is_finite(y1i[e]) &&
-            (tiny0 || zbits(y1i[e]) || eexp(y1i[e]) + C::SMALL <= eexp(y0i[e]));
+    // finite inputs; the size of y1 is checked where it matters, on d below
+    ok[e] = is_finite(y0i[e]) && is_finite(y1i[e]);
     y0[e] = ok[e] ? y0i[e] : T(0);
     y1[e] = ok[e] ? y1i[e] : T(0);
     v[e] = renorm_u(mk(y0[e], y1[e]));
@@ -626,8 +633,10 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       T x1 = add(u.v, u.e);
       ok[e] = ok[e] && newton_quiet(x1, sd[e]);
       bool tiny = ahi(y0[e]) < (D ? H64_TINY54 : B32_TINY25);
-      // v - y0 == y1 exactly; |d| ~ 2^-53 |log1p(y0)|: ~2^-22 accuracy suffices
+      // v - y0 == y1 exactly; with |d| <= 2^-48 |log1p(y0)| (2^-21 binary32)
+      // ~2^-22 accuracy of d suffices; below 2^-54 the value part is y0 itself
       T d = mul(y1[e], rcp_approx(add(T(1), y0[e])));
+      ok[e] = ok[e] && (tiny || ahi(d) + ((uint32_t)(D ? 48 : 21) << (D ? 20 : 23)) <= ahi(sd[e]));
       bool hard;
       T zz = rn_guard(sd[e], sub(x1, d), hard);
       z0[e] = tiny ? y0[e] : zz;
