@@ -489,7 +489,7 @@ template <> struct LogC<double> {
   TF_DEV static double rcp(double x) { return rcp_nr(x); }
 };
 template <> struct LogC<float> {
-  static constexpr uint32_t NORM_SPAN = 252u;
+  static constexpr uint32_t NORM_SPAN = 254u;           // (2^-n may be subnormal: p2n = p2)
   static constexpr uint32_t DMAX = (127u - 21u) << 23;   // |d| < 2^-21
   static constexpr int SMALL = 21, EBIAS = 126;
   static constexpr uint32_t HALF = B32_HALF, TWO = B32_TWO;
@@ -500,7 +500,7 @@ template <> struct LogC<float> {
     return __int_as_float((ubits(v) & 0x807fffffu) | (126u << 23));
   }
   TF_DEV static float p2(int k) { return p2f_bf(k); }
-  TF_DEV static float p2n(int k) { return __int_as_float((k + 127) << 23); }
+  TF_DEV static float p2n(int k) { return p2f_bf(k); }
   TF_DEV static float rcp(float x) { return rcp_approx(x); }
 };
 
