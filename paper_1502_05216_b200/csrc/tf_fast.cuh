@@ -592,7 +592,7 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
     n[e] = 0;
     zc0[e] = T(1);
     zc1[e] = T(0);
-    if (UNIFIED) {
+    if (UNIFIED && !inb[e]) {
       // out-of-band prologue; v0 > -1 keeps w0 = 1 + v0 positive and normal
       ok[e] = ok[e] && (inb[e] || !sgn(v[e].v) || ahi(v[e].v) < B32_ONE);
       TF<T> w = renorm_u(t_add_d_u(v[e], T(1)));
@@ -670,12 +670,80 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
   }
 }
 
+// Per-warp exchange buffer for class-sorting the 32 x VW elements of a warp
+// iteration (binary32 tlog1p, whose in-band / out-of-band split is ~50/50).
+template <int VW> struct Xch {
+  float a[32 * VW], b[32 * VW];
+  unsigned char src[32 * VW], okb[32 * VW];
+};
+
+// binary32 tlog1p: sort the warp's elements by branch before evaluating, so
+// that every lane index except one holds a single class across the warp and
+// the in-band / out-of-band epilogues no longer run back to back under
+// divergence.  Element k = e*32 + lane goes to slot rank_A(k) (in-band) or
+// n_A + rank_B(k); results travel back through the same buffer.
+template <int VW>
+TF_DEV void tlog1p_sorted(const STab<float>& tb, Xch<VW>* xw, const float (&x0)[VW],
+                          const float (&x1)[VW], float (&z0)[VW], float (&z1)[VW],
+                          bool (&ok)[VW]) {
+  const int lane = threadIdx.x & 31;
+  unsigned m[VW];
+  int pre[VW], nA = 0;
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    bool fin = is_finite(x0[e]) && is_finite(x1[e]);
+    TF<float> v = renorm_u(mk(fin ? x0[e] : 0.0f, fin ? x1[e] : 0.0f));
+    bool inb = ahi(v.v) <= (sgn(v.v) ? B32_HALF : B32_ONE);
+    m[e] = __ballot_sync(0xffffffffu, inb);
+    pre[e] = nA;
+    nA += __popc(m[e]);
+  }
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    int k = e * 32 + lane;
+    int ra = pre[e] + __popc(m[e] & lt);
+    int dst = (m[e] >> lane & 1u) ? ra : nA + (k - ra);
+    xw->a[dst] = x0[e];
+    xw->b[dst] = x1[e];
+    xw->src[dst] = (unsigned char)k;
+  }
+  __syncwarp();
+  float p0[VW], p1[VW], q0[VW], q1[VW];
+  int sk[VW];
+  bool pok[VW];
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    p0[e] = xw->a[e * 32 + lane];
+    p1[e] = xw->b[e * 32 + lane];
+    sk[e] = xw->src[e * 32 + lane];
+  }
+  __syncwarp();
+  fast_tlog1p<float, VW>(tb, p0, p1, q0, q1, pok);
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    xw->a[sk[e]] = q0[e];
+    xw->b[sk[e]] = q1[e];
+    xw->okb[sk[e]] = pok[e];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    z0[e] = xw->a[e * 32 + lane];
+    z1[e] = xw->b[e * 32 + lane];
+    ok[e] = xw->okb[e * 32 + lane] != 0;
+  }
+  __syncwarp();
+}
+
 template <class T, int FN, int VW>
-TF_DEV void fast_eval(const STab<T>& tb, const T (&x0)[VW], const T (&x1)[VW], T (&z0)[VW],
-                      T (&z1)[VW], bool (&ok)[VW]) {
+TF_DEV void fast_eval(const STab<T>& tb, void* xch, const T (&x0)[VW], const T (&x1)[VW],
+                      T (&z0)[VW], T (&z1)[VW], bool (&ok)[VW]) {
   if constexpr (FN == FN_TEXP) fast_texp<VW>(tb, x0, x1, z0, z1, ok);
   else if constexpr (FN == FN_TEXPM1) fast_texpm1<VW>(tb, x0, x1, z0, z1, ok);
   else if constexpr (FN == FN_TLOG) fast_tlog<T, VW>(tb, x0, x1, z0, z1, ok);
+  else if constexpr (sizeof(T) == 4 && VW >= 2)
+    tlog1p_sorted<VW>(tb, static_cast<Xch<VW>*>(xch), x0, x1, z0, z1, ok);
   else fast_tlog1p<T, VW>(tb, x0, x1, z0, z1, ok);
 }
 

@@ -122,6 +122,8 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   __shared__ STab<T> tb;
   __shared__ uint32_t qs[WARPS][QCAP];
   __shared__ __align__(16) T stg[ASYNC ? STAGES : 1][2][BLOCK][VW];
+  constexpr bool XCH = FN == FN_TLOG1P && sizeof(T) == 4 && VW >= 2;
+  __shared__ Xch<VW> xch[XCH ? WARPS : 1];
   load_tables(tb);
   __syncthreads();
 
@@ -177,7 +179,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
       }
     }
     bool ok[VW];
-    fast_eval<T, FN, VW>(tb, a, b, r0, r1, ok);
+    fast_eval<T, FN, VW>(tb, &xch[XCH ? warp : 0], a, b, r0, r1, ok);
 #pragma unroll
     for (int e = 0; e < VW; ++e) rare[e] = valid && (!ok[e] || force);
     if (valid) {
