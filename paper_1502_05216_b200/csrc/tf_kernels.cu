@@ -30,6 +30,12 @@ namespace tf {
 #ifndef TF_VW64
 #define TF_VW64 2
 #endif
+#ifndef TF_VW32
+#define TF_VW32 4
+#endif
+#ifndef TF_MINB32W
+#define TF_MINB32W 2
+#endif
 
 __device__ unsigned long long g_rare_count = 0;
 
@@ -70,8 +76,9 @@ TF_DEV void st(T* p, uint64_t vi, const T (&a)[VW]) {
 // lanes per thread and occupancy per (width, vector width)
 template <class T, int VW> struct KCfg {
   static constexpr bool WIDE = sizeof(T) == 8 && VW == 4;   // 4 binary64 lanes per thread
-  static constexpr int BLOCK = WIDE ? 128 : 256;             // static smem stays < 48 KB
-  static constexpr int MINB = WIDE ? TF_MINB4 : TF_MINB;
+  static constexpr bool WIDE32 = sizeof(T) == 4 && VW == 8;  // 8 binary32 lanes per thread
+  static constexpr int BLOCK = (WIDE || WIDE32) ? 128 : 256; // static smem stays < 48 KB
+  static constexpr int MINB = WIDE ? TF_MINB4 : (WIDE32 ? TF_MINB32W : TF_MINB);
 };
 
 // ---- asynchronous global -> shared staging (LDGSTS), one 16 B vector per
@@ -115,6 +122,8 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   constexpr int BLOCK = KCfg<T, VW>::BLOCK;
   constexpr int WARPS = BLOCK / 32;
   constexpr int QCAP = 32 + 32 * VW;
+  static_assert(QCAP <= 160, "queue compaction below moves at most 4 x 32 entries");
+  static_assert(VW == 1 || VW * sizeof(T) % 16 == 0, "vector lanes must fill 16-byte chunks");
   constexpr int STAGES = 2;
   constexpr bool ASYNC = VW * sizeof(T) % 16 == 0;
   constexpr int NC = VW * (int)sizeof(T) / 16;        // 16-byte chunks per thread
@@ -446,7 +455,7 @@ int launch(const T* x0, const T* x1, T* z0, T* z1, int64_t n, void* stream, int 
   uintptr_t al = (uintptr_t)x0 | (uintptr_t)x1 | (uintptr_t)z0 | (uintptr_t)z1;
   if ((al & 15) == 0) {
     if constexpr (sizeof(T) == 8) return launch_one<T, FN, TF_VW64>(x0, x1, z0, z1, n, s, flags);
-    else return launch_one<T, FN, 4>(x0, x1, z0, z1, n, s, flags);
+    else return launch_one<T, FN, TF_VW32>(x0, x1, z0, z1, n, s, flags);
   }
   if ((al & (sizeof(T) - 1)) != 0) return fail(TF_ERR_ARG, "misaligned pointer%s");
   return launch_one<T, FN, 1>(x0, x1, z0, z1, n, s, flags);
