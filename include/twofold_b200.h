@@ -8,12 +8,12 @@
  *
  * Each entry point replaces, for a whole array, the per-element reference
  * call of the Python package (/root/reference/pkg/src/twofold):
- *   tf_texp_f64   <- ExpLog(64).texp(x)    explog.py:265-275
- *   tf_texpm1_f64 <- ExpLog(64).texpm1(x)  explog.py:299-310
- *   tf_tlog_f64   <- ExpLog(64).tlog(y)    explog.py:394-399
- *   tf_tlog1p_f64 <- ExpLog(64).tlog1p(y)  explog.py:464-467
+ *   tf_texp_f64   <- ExpLog(64).texp(x)    explog.py:115-125
+ *   tf_texpm1_f64 <- ExpLog(64).texpm1(x)  explog.py:149-160
+ *   tf_tlog_f64   <- ExpLog(64).tlog(y)    explog.py:244-249
+ *   tf_tlog1p_f64 <- ExpLog(64).tlog1p(y)  explog.py:314-317
  *   tf_*_f32      <- the same methods of ExpLog(32) (binary32 lane)
- * (api(width) / get_function(name, width), explog.py:483-499, resolve to them).
+ * (api(width) / get_function(name, width), explog.py:333-349, resolve to them).
  * The paper's scalar C form z0 = texp(x0, x1, &z1)
  * is the n == 1 case.
  *
@@ -50,11 +50,30 @@ extern "C" {
 #define TF_ERR_ARG (-1)  /* invalid argument (the reference raises ValueError) */
 #define TF_ERR_CUDA (-2) /* CUDA runtime / launch error */
 
-/* function codes for tf_eval (FUNCTION_NAMES subset TWOFOLD_ARG, explog.py:44-53) */
+/* function codes for tf_eval: the four TWOFOLD_ARG hot-path functions first,
+ * then the other sixteen names of FUNCTION_NAMES (explog.py:44-53).  Codes
+ * marked (dotted) take the plain argument x0 only; x1 may be NULL. */
 #define TF_FN_TEXP 0
 #define TF_FN_TEXPM1 1
 #define TF_FN_TLOG 2
 #define TF_FN_TLOG1P 3
+#define TF_FN_PEXP0 4    /* (dotted) */
+#define TF_FN_TEXP0 5    /* (dotted) */
+#define TF_FN_TEXPP 6
+#define TF_FN_PEXP 7
+#define TF_FN_PEXPM10 8  /* (dotted) */
+#define TF_FN_TEXPM10 9  /* (dotted) */
+#define TF_FN_TEXPM1P 10
+#define TF_FN_PEXPM1 11
+#define TF_FN_PLOG0 12   /* (dotted) */
+#define TF_FN_TLOG0 13   /* (dotted) */
+#define TF_FN_TLOGP 14
+#define TF_FN_PLOG 15
+#define TF_FN_PLOG1P0 16 /* (dotted) */
+#define TF_FN_TLOG1P0 17 /* (dotted) */
+#define TF_FN_TLOG1PP 18
+#define TF_FN_PLOG1P 19
+#define TF_FN_COUNT 20
 
 /* tf_eval flags */
 #define TF_FLAG_FORCE_EXACT 1 /* route every element through the exact path (testing) */

@@ -2,7 +2,7 @@
 
 TEST INFRASTRUCTURE ONLY.  Imported by tests/, __graft_entry__.smoke() and the
 cpu_baseline / --impl reference legs of bench.py -- never by the product
-package.  It evaluates the reference algorithm (pkg/src/twofold/explog.py:265-467)
+package.  It evaluates the reference algorithm (pkg/src/twofold/explog.py:115-317)
 op for op on the CPU:
 
   binary64: one C pass, libm = glibc (the library CPython's math calls);
@@ -26,7 +26,10 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "build", "libtforacle.so")
 
-FNS = {"texp": 0, "texpm1": 1, "tlog": 2, "tlog1p": 3}
+FNS = {"texp": 0, "texpm1": 1, "tlog": 2, "tlog1p": 3,
+       "pexp0": 4, "texp0": 5, "texpp": 6, "pexp": 7, "pexpm10": 8, "texpm10": 9,
+       "texpm1p": 10, "pexpm1": 11, "plog0": 12, "tlog0": 13, "tlogp": 14, "plog": 15,
+       "plog1p0": 16, "tlog1p0": 17, "tlog1pp": 18, "plog1p": 19}
 _LIBM32 = {0: np.exp, 1: np.expm1, 2: np.log, 3: np.log1p}
 
 

@@ -41,7 +41,15 @@ static const float TF32_E[] = {TF32_E_INIT};
 static const float TF32_C[] = {TF32_C_INIT};
 static const float TF32_CM1[] = {TF32_CM1_INIT};
 
-enum { FN_TEXP = 0, FN_TEXPM1 = 1, FN_TLOG = 2, FN_TLOG1P = 3 };
+enum {
+    FN_TEXP = 0, FN_TEXPM1 = 1, FN_TLOG = 2, FN_TLOG1P = 3,
+    /* the other sixteen functions of FUNCTION_NAMES (explog.py:44-50) */
+    FN_PEXP0 = 4, FN_TEXP0 = 5, FN_TEXPP = 6, FN_PEXP = 7,
+    FN_PEXPM10 = 8, FN_TEXPM10 = 9, FN_TEXPM1P = 10, FN_PEXPM1 = 11,
+    FN_PLOG0 = 12, FN_TLOG0 = 13, FN_TLOGP = 14, FN_PLOG = 15,
+    FN_PLOG1P0 = 16, FN_TLOG1P0 = 17, FN_TLOG1PP = 18, FN_PLOG1P = 19,
+    FN_COUNT = 20
+};
 enum { LM_EXP = 0, LM_EXPM1 = 1, LM_LOG = 2, LM_LOG1P = 3, LM_NONE = -1 };
 #define MAXCALLS 4
 
@@ -155,7 +163,7 @@ static tf64 t_mul_d64(int dv, tf64 x, double b) {
     return mk64(v, x.e * b + e);
 }
 
-/* params.py:276-293 */
+/* params.py:62-79 */
 #define LO64 (-0x1.74385446d71c4p+9)
 #define HI64 (0x1.62e42fefa39f0p+9)
 static const tf64 LN2_64 = {TF64_LN2_V, TF64_LN2_E};
@@ -268,7 +276,7 @@ static double lm64(L64* L, int f, double x) {
     }
 }
 
-/* ExpLog.texp (explog.py:265-275) */
+/* ExpLog.texp (explog.py:115-125) */
 static tf64 texp64(int dv, L64* L, double x0, double x1) {
     tf64 v = pexp0_raw64(dv, x0);
     double z0 = lm64(L, LM_EXP, x0);
@@ -277,7 +285,7 @@ static tf64 texp64(int dv, L64* L, double x0, double x1) {
     return mk64(z0, (z0 * t1) + (v.e + (v.v - z0)));
 }
 
-/* ExpLog.texpm1 (explog.py:299-310) */
+/* ExpLog.texpm1 (explog.py:149-160) */
 static tf64 texpm1_64(int dv, L64* L, double x0, double x1) {
     tf64 w = pexpm10_raw64(dv, x0);
     double z0 = lm64(L, LM_EXPM1, x0);
@@ -287,9 +295,9 @@ static tf64 texpm1_64(int dv, L64* L, double x0, double x1) {
     return mk64(z0, ((z0 + 1.0) * t1) + tail);
 }
 
-#define NEWTON_TOL 0x1p-20 /* explog.py:205 */
+#define NEWTON_TOL 0x1p-20 /* explog.py:55 */
 
-/* _newton_log_z (explog.py:320-336) */
+/* _newton_log_z (explog.py:170-186) */
 static double newton_log_z64(int dv, double z0, double z1, double r0) {
     tf64 s = pexpm10_raw64(dv, -r0);
     double zm1 = z0 - 1.0;
@@ -303,7 +311,7 @@ static double newton_log_z64(int dv, double z0, double z1, double r0) {
     return u.v + u.e;
 }
 
-/* _log_core (explog.py:338-358) */
+/* _log_core (explog.py:188-208) */
 static tf64 log_core64(int dv, L64* L, double y0, double y1) {
     double z0, z1;
     int n = 0;
@@ -327,26 +335,26 @@ static tf64 log_core64(int dv, L64* L, double y0, double y1) {
     return t_add64(mk64(r0, r1), nl);
 }
 
-/* _correct (explog.py:366-373) */
+/* _correct (explog.py:216-223) */
 static tf64 correct64(tf64 core, double lib0) {
     if (isinf(lib0) && core.v == lib0) return mk64(lib0, lib0);
     return mk64(lib0, core.e + (core.v - lib0));
 }
 
-/* ExpLog.tlog (explog.py:394-399) */
+/* ExpLog.tlog (explog.py:244-249) */
 static tf64 tlog64(int dv, L64* L, double y0, double y1) {
     tf64 v = renorm64(mk64(y0, y1));
     tf64 core = log_core64(dv, L, v.v, v.e);
     return correct64(core, lm64(L, LM_LOG, y0));
 }
 
-/* ExpLog.tlogp (explog.py:389-392) */
+/* ExpLog.tlogp (explog.py:239-242) */
 static tf64 tlogp64(int dv, L64* L, tf64 y) {
     tf64 core = log_core64(dv, L, y.v, y.e);
     return correct64(core, lm64(L, LM_LOG, y.v));
 }
 
-/* _newton_log1p_in_band (explog.py:410-424) */
+/* _newton_log1p_in_band (explog.py:260-274) */
 static double newton_log1p64(int dv, double y0, double y1, double x0) {
     tf64 s = pexpm10_raw64(dv, -x0);
     tf64 u;
@@ -360,7 +368,7 @@ static double newton_log1p64(int dv, double y0, double y1, double x0) {
     return u.v + u.e;
 }
 
-/* _log1p_core (explog.py:426-432) */
+/* _log1p_core (explog.py:276-282) */
 static tf64 log1p_core64(int dv, L64* L, double y0, double y1) {
     double x0 = lm64(L, LM_LOG1P, y0);
     double x1 = newton_log1p64(dv, y0, y1, x0);
@@ -371,7 +379,7 @@ static tf64 log1p_core64(int dv, L64* L, double y0, double y1) {
     return mk64(x0, x1);
 }
 
-/* _plog1p_raw (explog.py:440-444) */
+/* _plog1p_raw (explog.py:290-294) */
 static tf64 plog1p_raw64(int dv, L64* L, tf64 y) {
     if (y.v < -0.5 || y.v > 1.0) {
         tf64 w = renorm64(t_add_d64(y, 1.0));
@@ -380,19 +388,89 @@ static tf64 plog1p_raw64(int dv, L64* L, tf64 y) {
     return log1p_core64(dv, L, y.v, y.e);
 }
 
-/* ExpLog.tlog1p (explog.py:464-467) */
+/* ExpLog.tlog1p (explog.py:314-317) */
 static tf64 tlog1p64(int dv, L64* L, double y0, double y1) {
     tf64 v = renorm64(mk64(y0, y1));
     tf64 core = plog1p_raw64(dv, L, v);
     return correct64(core, lm64(L, LM_LOG1P, y0));
 }
 
+/* ---- the sixteen sibling functions (explog.py:101-325) ---- */
+
+/* texp0 (explog.py:105-113) */
+static tf64 texp0_64(int dv, L64* L, double x0) {
+    tf64 v = pexp0_raw64(dv, x0);
+    double z0 = lm64(L, LM_EXP, x0);
+    if (z0 == v.v && isinf(z0)) return mk64(z0, z0);
+    return mk64(z0, (v.v - z0) + v.e);
+}
+
+/* texpm10 (explog.py:139-147) */
+static tf64 texpm10_64(int dv, L64* L, double x0) {
+    tf64 w = pexpm10_raw64(dv, x0);
+    double z0 = lm64(L, LM_EXPM1, x0);
+    if (z0 == w.v && isinf(z0)) return mk64(z0, z0);
+    return mk64(z0, (w.v - z0) + w.e);
+}
+
+/* _plog1p0_raw (explog.py:284-288) */
+static tf64 plog1p0_raw64(int dv, L64* L, double y0) {
+    if (y0 < -0.5 || y0 > 1.0) {
+        tf64 v = renorm64(mk64(1.0, y0));
+        return log_core64(dv, L, v.v, v.e);
+    }
+    return log1p_core64(dv, L, y0, 0.0);
+}
+
 static tf64 eval64(int fn, int dv, L64* L, double x0, double x1) {
     switch (fn) {
-        case FN_TEXP: return texp64(dv, L, x0, x1);
-        case FN_TEXPM1: return texpm1_64(dv, L, x0, x1);
+        case FN_TEXP: case FN_TEXPP: return texp64(dv, L, x0, x1);
+        case FN_TEXPM1: case FN_TEXPM1P: return texpm1_64(dv, L, x0, x1);
         case FN_TLOG: return tlog64(dv, L, x0, x1);
-        default: return tlog1p64(dv, L, x0, x1);
+        case FN_TLOG1P: return tlog1p64(dv, L, x0, x1);
+        case FN_PEXP0: { tf64 r = pexp0_raw64(dv, x0); return fast_two_sum64(r.v, r.e); }
+        case FN_TEXP0: return texp0_64(dv, L, x0);
+        case FN_PEXP: { tf64 r = texp64(dv, L, x0, x1); return fast_two_sum64(r.v, r.e); }
+        case FN_PEXPM10: { tf64 r = pexpm10_raw64(dv, x0); return fast_two_sum64(r.v, r.e); }
+        case FN_TEXPM10: return texpm10_64(dv, L, x0);
+        case FN_PEXPM1: { tf64 r = texpm1_64(dv, L, x0, x1); return fast_two_sum64(r.v, r.e); }
+        case FN_PLOG0: {                                  /* explog.py:225-232 */
+            if (x0 == 0.0) return mk64(-INFINITY, -INFINITY);
+            if (x0 == INFINITY) return mk64(INFINITY, INFINITY);
+            tf64 r = log_core64(dv, L, x0, 0.0);
+            return fast_two_sum64(r.v, r.e);
+        }
+        case FN_TLOG0: {                                  /* explog.py:234-237 */
+            tf64 core = log_core64(dv, L, x0, 0.0);
+            return correct64(core, lm64(L, LM_LOG, x0));
+        }
+        case FN_TLOGP: return tlogp64(dv, L, mk64(x0, x1));  /* explog.py:239-242 */
+        case FN_PLOG: {                                   /* explog.py:251-258 */
+            if (x0 == 0.0) return mk64(-INFINITY, -INFINITY);
+            if (x0 == INFINITY) return mk64(INFINITY, INFINITY);
+            tf64 r = log_core64(dv, L, x0, x1);
+            return fast_two_sum64(r.v, r.e);
+        }
+        case FN_PLOG1P0: {                                /* explog.py:296-303 */
+            if (x0 == -1.0) return mk64(-INFINITY, -INFINITY);
+            if (x0 == INFINITY) return mk64(INFINITY, INFINITY);
+            tf64 r = plog1p0_raw64(dv, L, x0);
+            return fast_two_sum64(r.v, r.e);
+        }
+        case FN_TLOG1P0: {                                /* explog.py:305-308 */
+            tf64 core = plog1p0_raw64(dv, L, x0);
+            return correct64(core, lm64(L, LM_LOG1P, x0));
+        }
+        case FN_TLOG1PP: {                                /* explog.py:310-312 */
+            tf64 core = plog1p_raw64(dv, L, mk64(x0, x1));
+            return correct64(core, lm64(L, LM_LOG1P, x0));
+        }
+        default: {                                        /* plog1p, explog.py:319-325 */
+            if (x0 == -1.0 && x1 == 0.0) return mk64(-INFINITY, -INFINITY);
+            if (x0 == INFINITY) return mk64(INFINITY, INFINITY);
+            tf64 r = plog1p_raw64(dv, L, mk64(x0, x1));
+            return fast_two_sum64(r.v, r.e);
+        }
     }
 }
 
@@ -502,7 +580,7 @@ static tf32 t_mul_d32(int dv, tf32 x, float b) {
     return mk32(v, (x.e * b) + e);
 }
 
-/* params.py:295-312 */
+/* params.py:81-98 */
 #define LO32 (-0x1.9d1da0p+6f)
 #define HI32 (0x1.62e430p+6f)
 static const tf32 LN2_32 = {TF32_LN2_V, TF32_LN2_E};
@@ -628,7 +706,7 @@ static float newton_log_z32(int dv, float z0, float z1, float r0) {
 }
 
 /* the Newton-tolerance test runs in binary64 in the reference (plain Python
- * float arithmetic, explog.py:351 and 429) */
+ * float arithmetic, explog.py:201 and 429) */
 static inline int newton_again32(float r1, float r0) {
     return fabs((double)r1) > NEWTON_TOL * fabs((double)r0) + NEWTON_TOL;
 }
@@ -709,12 +787,77 @@ static tf32 tlog1p32(int dv, L32* L, float y0, float y1) {
     return correct32(core, lm32(L, LM_LOG1P, y0));
 }
 
+static tf32 texp0_32(int dv, L32* L, float x0) {
+    tf32 v = pexp0_raw32(dv, x0);
+    float z0 = lm32(L, LM_EXP, x0);
+    if (z0 == v.v && isinf(z0)) return mk32(z0, z0);
+    return mk32(z0, (v.v - z0) + v.e);
+}
+
+static tf32 texpm10_32(int dv, L32* L, float x0) {
+    tf32 w = pexpm10_raw32(dv, x0);
+    float z0 = lm32(L, LM_EXPM1, x0);
+    if (z0 == w.v && isinf(z0)) return mk32(z0, z0);
+    return mk32(z0, (w.v - z0) + w.e);
+}
+
+static tf32 plog1p0_raw32(int dv, L32* L, float y0) {
+    if (y0 < -0.5f || y0 > 1.0f) {
+        tf32 v = renorm32(mk32(1.0f, y0));
+        return log_core32(dv, L, v.v, v.e);
+    }
+    return log1p_core32(dv, L, y0, 0.0f);
+}
+
 static tf32 eval32(int fn, int dv, L32* L, float x0, float x1) {
     switch (fn) {
-        case FN_TEXP: return texp32(dv, L, x0, x1);
-        case FN_TEXPM1: return texpm1_32(dv, L, x0, x1);
+        case FN_TEXP: case FN_TEXPP: return texp32(dv, L, x0, x1);
+        case FN_TEXPM1: case FN_TEXPM1P: return texpm1_32(dv, L, x0, x1);
         case FN_TLOG: return tlog32(dv, L, x0, x1);
-        default: return tlog1p32(dv, L, x0, x1);
+        case FN_TLOG1P: return tlog1p32(dv, L, x0, x1);
+        case FN_PEXP0: { tf32 r = pexp0_raw32(dv, x0); return fast_two_sum32(r.v, r.e); }
+        case FN_TEXP0: return texp0_32(dv, L, x0);
+        case FN_PEXP: { tf32 r = texp32(dv, L, x0, x1); return fast_two_sum32(r.v, r.e); }
+        case FN_PEXPM10: { tf32 r = pexpm10_raw32(dv, x0); return fast_two_sum32(r.v, r.e); }
+        case FN_TEXPM10: return texpm10_32(dv, L, x0);
+        case FN_PEXPM1: { tf32 r = texpm1_32(dv, L, x0, x1); return fast_two_sum32(r.v, r.e); }
+        case FN_PLOG0: {
+            if (x0 == 0.0f) return mk32(-INFINITY, -INFINITY);
+            if (x0 == INFINITY) return mk32(INFINITY, INFINITY);
+            tf32 r = log_core32(dv, L, x0, 0.0f);
+            return fast_two_sum32(r.v, r.e);
+        }
+        case FN_TLOG0: {
+            tf32 core = log_core32(dv, L, x0, 0.0f);
+            return correct32(core, lm32(L, LM_LOG, x0));
+        }
+        case FN_TLOGP: return tlogp32(dv, L, mk32(x0, x1));
+        case FN_PLOG: {
+            if (x0 == 0.0f) return mk32(-INFINITY, -INFINITY);
+            if (x0 == INFINITY) return mk32(INFINITY, INFINITY);
+            tf32 r = log_core32(dv, L, x0, x1);
+            return fast_two_sum32(r.v, r.e);
+        }
+        case FN_PLOG1P0: {
+            if (x0 == -1.0f) return mk32(-INFINITY, -INFINITY);
+            if (x0 == INFINITY) return mk32(INFINITY, INFINITY);
+            tf32 r = plog1p0_raw32(dv, L, x0);
+            return fast_two_sum32(r.v, r.e);
+        }
+        case FN_TLOG1P0: {
+            tf32 core = plog1p0_raw32(dv, L, x0);
+            return correct32(core, lm32(L, LM_LOG1P, x0));
+        }
+        case FN_TLOG1PP: {
+            tf32 core = plog1p_raw32(dv, L, mk32(x0, x1));
+            return correct32(core, lm32(L, LM_LOG1P, x0));
+        }
+        default: {
+            if (x0 == -1.0f && x1 == 0.0f) return mk32(-INFINITY, -INFINITY);
+            if (x0 == INFINITY) return mk32(INFINITY, INFINITY);
+            tf32 r = plog1p_raw32(dv, L, mk32(x0, x1));
+            return fast_two_sum32(r.v, r.e);
+        }
     }
 }
 
@@ -778,7 +921,7 @@ static void body64(void* p, int64_t lo, int64_t hi, int64_t* acc) {
 
 EXPORT int tfo_eval_f64(int fn, int dv, const double* x0, const double* x1,
                         double* z0, double* z1, int64_t n, int nthreads) {
-    if (fn < 0 || fn > 3 || n < 0) return -1;
+    if (fn < 0 || fn >= FN_COUNT || n < 0) return -1;
     job64_t j = {fn, dv, x0, x1, z0, z1};
     parallel_for(n, nthreads, body64, &j);
     return 0;
@@ -810,7 +953,7 @@ static void body64r(void* p, int64_t lo, int64_t hi, int64_t* acc) {
 EXPORT int64_t tfo_eval_f64_pass(int fn, int dv, const double* x0, const double* x1,
                                  double* z0, double* z1, int64_t n, const double* ans,
                                  int n_known, double* req_arg, int8_t* req_fn, int nthreads) {
-    if (fn < 0 || fn > 3 || n < 0 || n_known < 0 || n_known > MAXCALLS) return -1;
+    if (fn < 0 || fn >= FN_COUNT || n < 0 || n_known < 0 || n_known > MAXCALLS) return -1;
     job64r_t j = {fn, dv, n_known, x0, x1, ans, z0, z1, req_arg, req_fn};
     return parallel_for(n, nthreads, body64r, &j);
 }
@@ -843,7 +986,7 @@ EXPORT int64_t tfo_eval_f32_pass(int fn, int dv, const float* x0, const float* x
                                  float* z0, float* z1, int64_t n, const float* ans,
                                  int n_known, float* req_arg, int8_t* req_fn,
                                  int nthreads) {
-    if (fn < 0 || fn > 3 || n < 0 || n_known < 0 || n_known > MAXCALLS) return -1;
+    if (fn < 0 || fn >= FN_COUNT || n < 0 || n_known < 0 || n_known > MAXCALLS) return -1;
     job32_t j = {fn, dv, n_known, x0, x1, ans, z0, z1, req_arg, req_fn};
     return parallel_for(n, nthreads, body32, &j);
 }

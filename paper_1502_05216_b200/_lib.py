@@ -16,7 +16,11 @@ LIB_PATH = os.environ.get("TWOFOLD_B200_LIB") or os.path.join(HERE, "lib", "libt
 CSRC = os.path.join(HERE, "csrc")
 
 TF_OK, TF_ERR_ARG, TF_ERR_CUDA = 0, -1, -2
-FN_CODES = {"texp": 0, "texpm1": 1, "tlog": 2, "tlog1p": 3}
+# tf_eval function codes (include/twofold_b200.h TF_FN_*)
+FN_CODES = {"texp": 0, "texpm1": 1, "tlog": 2, "tlog1p": 3, "pexp0": 4, "texp0": 5, "texpp": 6,
+            "pexp": 7, "pexpm10": 8, "texpm10": 9, "texpm1p": 10, "pexpm1": 11, "plog0": 12,
+            "tlog0": 13, "tlogp": 14, "plog": 15, "plog1p0": 16, "tlog1p0": 17, "tlog1pp": 18,
+            "plog1p": 19}
 FLAG_FORCE_EXACT = 1
 FLAG_COUNT_EXACT = 2
 FLAG_MARK_EXACT = 4

@@ -196,7 +196,7 @@ template <class T> TF_DEV TF<T> t_mul_d_c(TF<T> x, T b) {
 }
 
 // ------------------------------------------------------ method parameters
-// params.py:276-312
+// params.py:62-98
 template <class T> struct P;
 template <> struct P<double> {
   static constexpr double LO = -0x1.74385446d71c4p+9;

@@ -325,7 +325,7 @@ TF_DEV float p2f_bf(int k) {  // k in [-149, 127]
 }
 
 // "second Newton iteration cannot fire": |r1| < 2^-21 * max(|r0|, 1), a
-// conservative integer form of explog.py:351/429 (binary64 arithmetic there).
+// conservative integer form of explog.py:201/429 (binary64 arithmetic there).
 TF_DEV bool newton_quiet(double r1, double r0) {
   int e1 = bexp(r1), e0 = bexp(r0);
   return e1 + 22 <= max(e0, 1023);
@@ -383,7 +383,7 @@ TF_DEV void fast_texp(const STab<double>& tb, const double (&x0)[VW], const doub
       zz = mul(add(vs.v, vs.e), 0x1p-128);
     }
     z0[e] = zz;
-    z1[e] = add(mul(zz, t1_tiny(x1[e])), add(v.e, sub(v.v, zz)));  // explog.py:275
+    z1[e] = add(mul(zz, t1_tiny(x1[e])), add(v.e, sub(v.v, zz)));  // explog.py:125
   }
 }
 
@@ -434,7 +434,7 @@ TF_DEV void fast_texpm1(const STab<double>& tb, const double (&x0)[VW], const do
   for (int e = 0; e < VW; ++e) {
     z0[e] = ahi(xs[e]) < H64_TINY54 ? xs[e] : add(w[e].v, w[e].e);   // CR expm1(x0)
     double tail = add(w[e].e, sub(w[e].v, z0[e]));
-    z1[e] = add(mul(add(z0[e], 1.0), t1_tiny(x1[e])), tail);          // explog.py:309-310
+    z1[e] = add(mul(add(z0[e], 1.0), t1_tiny(x1[e])), tail);          // explog.py:159-160
   }
 }
 
@@ -467,7 +467,7 @@ TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const floa
 }
 
 // ================================================================= tlog
-// explog.py:394-399 -> _log_core (338-358) -> _newton_log_z (320-336),
+// explog.py:244-249 -> _log_core (338-358) -> _newton_log_z (320-336),
 // with the value part replaced by a correctly rounded log(y0):
 //   log(y0) = log(v) - log1p(d),  d = y1 / y0  (renorm is error-free: v - y0 == y1),
 // and near 1 by the exact-d series (log_near1).
@@ -526,7 +526,7 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     n[e] = band ? 0 : C::n_of(v[e].v);
     zc0[e] = band ? v[e].v : C::mant(v[e].v);
     zc1[e] = band ? v[e].e : (zbits(v[e].e) ? T(0) : mul(v[e].e, C::p2n(-n[e])));
-    r0[e] = seed_log1p_t(add(sub(zc0[e], T(1)), zc1[e]),      // explog.py:346-349
+    r0[e] = seed_log1p_t(add(sub(zc0[e], T(1)), zc1[e]),      // explog.py:196-199
                          [&](int i) { return tb.SEED[i]; });
     ok[e] = ok[e] && ahi(r0[e]) < C::LN2H;
     mr0[e] = -r0[e];
@@ -558,7 +558,7 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
 }
 
 // =============================================================== tlog1p
-// _plog1p_raw (explog.py:440-444) with both branches sharing ONE in-band
+// _plog1p_raw (explog.py:290-294) with both branches sharing ONE in-band
 // pexpm10 evaluation (the Taylor core is ~3/4 of the work):
 //   in-band  (-1/2 <= v0 <= 1): _log1p_core (426-432) -> _newton_log1p_in_band
 //            (410-424), seed log1p(v0);
@@ -613,7 +613,7 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       ok[e] = ok[e] && inb[e];
     }
     if (!ok[e]) { arg = T(0); inb[e] = true; }
-    sd[e] = seed_log1p_t(arg, [&](int i) { return tb.SEED[i]; });  // explog.py:347-349, 427
+    sd[e] = seed_log1p_t(arg, [&](int i) { return tb.SEED[i]; });  // explog.py:197-199, 277
     ok[e] = ok[e] && (inb[e] || ahi(sd[e]) < C::LN2H);
     ms[e] = -sd[e];
   }
@@ -623,10 +623,10 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
   for (int e = 0; e < VW; ++e) {
     if (inb[e]) {
       TF<T> u;
-      if (v[e].e == T(0)) {                              // explog.py:418-420
+      if (v[e].e == T(0)) {                              // explog.py:268-270
         TF<T> w = fast_two_sum_u(T(1), v[e].v);
         u = t_add_d_u(t_mul_u(w, s[e]), v[e].v);
-      } else {                                           // explog.py:421-423
+      } else {                                           // explog.py:271-273
         TF<T> ys = t_mul_u(v[e], s[e]);
         u = t_add_u(t_add_u(ys, v[e]), s[e]);
       }
@@ -741,6 +741,17 @@ TF_DEV void fast_eval(const STab<T>& tb, void* xch, const T (&x0)[VW], const T (
                       T (&z0)[VW], T (&z1)[VW], bool (&ok)[VW]) {
   if constexpr (FN == FN_TEXP) fast_texp<VW>(tb, x0, x1, z0, z1, ok);
   else if constexpr (FN == FN_TEXPM1) fast_texpm1<VW>(tb, x0, x1, z0, z1, ok);
+  else if constexpr (FN == FN_PEXP || FN == FN_PEXPM1) {
+    // pexp / pexpm1 = renorm_fast(texpp / texpm1p) (explog.py:131-133, 165-166)
+    if constexpr (FN == FN_PEXP) fast_texp<VW>(tb, x0, x1, z0, z1, ok);
+    else fast_texpm1<VW>(tb, x0, x1, z0, z1, ok);
+#pragma unroll
+    for (int e = 0; e < VW; ++e) {
+      TF<T> r = fast_two_sum_u(z0[e], z1[e]);
+      z0[e] = r.v;
+      z1[e] = r.e;
+    }
+  }
   else if constexpr (FN == FN_TLOG) fast_tlog<T, VW>(tb, x0, x1, z0, z1, ok);
   else if constexpr (sizeof(T) == 4 && VW >= 2)
     tlog1p_sorted<VW>(tb, static_cast<Xch<VW>*>(xch), x0, x1, z0, z1, ok);

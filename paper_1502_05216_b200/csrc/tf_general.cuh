@@ -1,5 +1,5 @@
 // tf_general.cuh -- the exact ("rare") path: a complete device restatement of
-// the reference texp/texpm1/tlog/tlog1p (pkg/src/twofold/explog.py:265-467,
+// the reference texp/texpm1/tlog/tlog1p (pkg/src/twofold/explog.py:115-317,
 // expcore.py:35-147) with every _special check, for ANY input: NaN/inf,
 // out-of-domain, subnormal, under/overflowing intermediates, non-coupled
 // twofolds, second Newton iterations.  The fast kernels divert every element
@@ -282,7 +282,7 @@ TF_DEV float expm1_cr(float x) {
   return rn32_twofold(w.v, w.e);
 }
 
-// t1 = expm1(x1) (explog.py:273, 307): the tail of a coupled input is tiny
+// t1 = expm1(x1) (explog.py:123, 157): the tail of a coupled input is tiny
 TF_DEV double expm1_t1(double x) {
   return ((uint32_t)hi32(x) & 0x7fffffffu) < 0x3e400000u ? t1_tiny(x) : expm1_cr(x);
 }
@@ -291,7 +291,7 @@ TF_DEV float expm1_t1(float x) {
 }
 
 // ------------------------------------------------------------ log cores
-// Newton seeds: the reference calls libm log / log1p (explog.py:347-349,427);
+// Newton seeds: the reference calls libm log / log1p (explog.py:197-199,277);
 // CUDA's are within 1 ulp and the Newton step absorbs the difference.
 //
 // The seed is a compact table-driven log1p (relative error ~2^-52 / 2^-23,
@@ -352,12 +352,12 @@ TF_DEV float seed_log1p(float x) {
 }
 
 // The Newton tolerance test is plain binary64 Python arithmetic in both lanes
-// (explog.py:351, 429).
+// (explog.py:201, 279).
 template <class T> TF_DEV bool newton_again(T r1, T r0) {
   return fabs((double)r1) > 0x1p-20 * fabs((double)r0) + 0x1p-20;
 }
 
-// _newton_log_z (explog.py:320-336)
+// _newton_log_z (explog.py:170-186)
 template <class T> TF_DEV T newton_log_z_c(T z0, T z1, T r0) {
   TF<T> s = pexpm10_raw_c(T(-r0));
   T zm1 = sub(z0, T(1));
@@ -371,7 +371,7 @@ template <class T> TF_DEV T newton_log_z_c(T z0, T z1, T r0) {
   return add(u.v, u.e);
 }
 
-// _log_core (explog.py:338-358)
+// _log_core (explog.py:188-208)
 template <class T> TF_DEV TF<T> log_core_c(T y0, T y1) {
   T z0, z1;
   int n = 0;
@@ -383,7 +383,7 @@ template <class T> TF_DEV TF<T> log_core_c(T y0, T y1) {
     z0 = y0;
     z1 = y1;
   }
-  // explog.py:346-349 seeds with log(z0) when y1 == z1 == 0, else with
+  // explog.py:196-199 seeds with log(z0) when y1 == z1 == 0, else with
   // log1p((z0 - 1) + z1); z0 - 1 is exact, so one log1p covers both (the seed
   // only needs to be within an ulp: the Newton step absorbs it).
   T r0 = seed_log1p(add(sub(z0, T(1)), z1));
@@ -397,7 +397,7 @@ template <class T> TF_DEV TF<T> log_core_c(T y0, T y1) {
   return t_add_c(mk(r0, r1), nl);
 }
 
-// _newton_log1p_in_band (explog.py:410-424)
+// _newton_log1p_in_band (explog.py:260-274)
 template <class T> TF_DEV T newton_log1p_c(T y0, T y1, T x0) {
   TF<T> s = pexpm10_raw_c(T(-x0));
   TF<T> u;
@@ -411,7 +411,7 @@ template <class T> TF_DEV T newton_log1p_c(T y0, T y1, T x0) {
   return add(u.v, u.e);
 }
 
-// _log1p_core (explog.py:426-432)
+// _log1p_core (explog.py:276-282)
 template <class T> TF_DEV TF<T> log1p_core_c(T y0, T y1) {
   T x0 = seed_log1p(y0);
   T x1 = newton_log1p_c(y0, y1, x0);
@@ -496,7 +496,7 @@ TF_DEV float log1p_cr(float y) {
 }
 
 // ------------------------------------------------------ public functions
-// ExpLog.texp (explog.py:265-275)
+// ExpLog.texp (explog.py:115-125)
 template <class T> TF_DEV TF<T> texp_gen(T x0, T x1) {
   TF<T> v = pexp0_raw_c(x0);
   T z0;
@@ -514,7 +514,7 @@ template <class T> TF_DEV TF<T> texp_gen(T x0, T x1) {
   return mk(z0, add(mul(z0, t1), add(v.e, sub(v.v, z0))));
 }
 
-// ExpLog.texpm1 (explog.py:299-310)
+// ExpLog.texpm1 (explog.py:149-160)
 template <class T> TF_DEV TF<T> texpm1_gen(T x0, T x1) {
   TF<T> w = pexpm10_raw_c(x0);
   T z0;
@@ -531,13 +531,13 @@ template <class T> TF_DEV TF<T> texpm1_gen(T x0, T x1) {
   return mk(z0, add(mul(add(z0, T(1)), t1), tail));
 }
 
-// _correct (explog.py:366-373)
+// _correct (explog.py:216-223)
 template <class T> TF_DEV TF<T> correct_c(TF<T> core, T lib0) {
   if (is_inf(lib0) && core.v == lib0) return mk(lib0, lib0);
   return mk(lib0, add(core.e, sub(core.v, lib0)));
 }
 
-// ExpLog.tlog (explog.py:394-399)
+// ExpLog.tlog (explog.py:244-249)
 template <class T> TF_DEV TF<T> tlog_gen(T y0, T y1) {
   TF<T> v = renorm_c(mk(y0, y1));
   TF<T> core = log_core_c(v.v, v.e);
@@ -552,7 +552,7 @@ template <class T> TF_DEV TF<T> tlog_gen(T y0, T y1) {
   return correct_c(core, lib0);
 }
 
-// ExpLog.tlog1p (explog.py:440-467) incl. tlogp for the out-of-band branch
+// ExpLog.tlog1p (explog.py:290-317) incl. tlogp for the out-of-band branch
 template <class T> TF_DEV TF<T> tlog1p_gen(T y0, T y1) {
   TF<T> v = renorm_c(mk(y0, y1));
   TF<T> core, raw;
@@ -590,13 +590,103 @@ template <class T> TF_DEV TF<T> tlog1p_gen(T y0, T y1) {
   return correct_c(core, lib0);
 }
 
-enum Fn { FN_TEXP = 0, FN_TEXPM1 = 1, FN_TLOG = 2, FN_TLOG1P = 3 };
+// ------------------------------------------------ the sixteen siblings
+// explog.py:101-325: the same cores with other arguments and finishing steps.
+// renorm_fast = fast_two_sum (eft.py:163-165).
+template <class T> TF_DEV TF<T> renorm_fast_c(TF<T> x) { return fast_two_sum_c(x.v, x.e); }
+
+// texp0 / texpm10 (explog.py:105-113, 139-147): value = libm(x0), error =
+// (core0 - z0) + core1
+template <class T> TF_DEV TF<T> texp0_gen(T x0) {
+  TF<T> v = pexp0_raw_c(x0);
+  T z0;
+  if constexpr (sizeof(T) == 8) {
+    uint32_t h = (uint32_t)hi32(x0);
+    bool band = (h & 0x7fffffffu) <= ((int)h < 0 ? 0x40857800u : 0x40862e14u);
+    z0 = band ? add(v.v, v.e) : exp_cr(x0);
+  } else {
+    z0 = exp_cr(x0);
+  }
+  if (z0 == v.v && is_inf(z0)) return mk(z0, z0);
+  return mk(z0, add(sub(v.v, z0), v.e));
+}
+template <class T> TF_DEV TF<T> texpm10_gen(T x0) {
+  TF<T> w = pexpm10_raw_c(x0);
+  T z0 = expm1_cr(x0);
+  if (z0 == w.v && is_inf(z0)) return mk(z0, z0);
+  return mk(z0, add(sub(w.v, z0), w.e));
+}
+
+// _plog1p0_raw (explog.py:284-288)
+template <class T> TF_DEV TF<T> plog1p0_raw_c(T y0) {
+  if (y0 < T(-0.5) || y0 > T(1)) {
+    TF<T> v = renorm_c(mk(T(1), y0));
+    return log_core_c(v.v, v.e);
+  }
+  return log1p_core_c(y0, T(0));
+}
+
+// _plog1p_raw (explog.py:290-294) incl. tlogp for the out-of-band branch
+template <class T> TF_DEV TF<T> plog1p_raw_c(TF<T> y) {
+  if (y.v < T(-0.5) || y.v > T(1)) {
+    TF<T> w = renorm_c(t_add_d_c(y, T(1)));
+    return correct_c(log_core_c(w.v, w.e), log_cr(w.v));
+  }
+  return log1p_core_c(y.v, y.e);
+}
+
+enum Fn {
+  FN_TEXP = 0, FN_TEXPM1 = 1, FN_TLOG = 2, FN_TLOG1P = 3,
+  FN_PEXP0 = 4, FN_TEXP0 = 5, FN_TEXPP = 6, FN_PEXP = 7,
+  FN_PEXPM10 = 8, FN_TEXPM10 = 9, FN_TEXPM1P = 10, FN_PEXPM1 = 11,
+  FN_PLOG0 = 12, FN_TLOG0 = 13, FN_TLOGP = 14, FN_PLOG = 15,
+  FN_PLOG1P0 = 16, FN_TLOG1P0 = 17, FN_TLOG1PP = 18, FN_PLOG1P = 19,
+  FN_COUNT = 20
+};
+
+// functions of a plain ("dotted") argument: x1 is not read
+__host__ __device__ constexpr bool dotted_fn(int fn) {
+  return fn == FN_PEXP0 || fn == FN_TEXP0 || fn == FN_PEXPM10 || fn == FN_TEXPM10 ||
+         fn == FN_PLOG0 || fn == FN_TLOG0 || fn == FN_PLOG1P0 || fn == FN_TLOG1P0;
+}
 
 template <class T, int FN> __device__ __noinline__ TF<T> eval_gen(T x0, T x1) {
-  if (FN == FN_TEXP) return texp_gen(x0, x1);
-  if (FN == FN_TEXPM1) return texpm1_gen(x0, x1);
-  if (FN == FN_TLOG) return tlog_gen(x0, x1);
-  return tlog1p_gen(x0, x1);
+  const T INF = Lim<T>::inf();
+  if constexpr (FN == FN_TEXP || FN == FN_TEXPP) return texp_gen(x0, x1);
+  else if constexpr (FN == FN_TEXPM1 || FN == FN_TEXPM1P) return texpm1_gen(x0, x1);
+  else if constexpr (FN == FN_TLOG) return tlog_gen(x0, x1);
+  else if constexpr (FN == FN_TLOG1P) return tlog1p_gen(x0, x1);
+  else if constexpr (FN == FN_PEXP0) return renorm_fast_c(pexp0_raw_c(x0));
+  else if constexpr (FN == FN_TEXP0) return texp0_gen(x0);
+  else if constexpr (FN == FN_PEXP) return renorm_fast_c(texp_gen(x0, x1));
+  else if constexpr (FN == FN_PEXPM10) return renorm_fast_c(pexpm10_raw_c(x0));
+  else if constexpr (FN == FN_TEXPM10) return texpm10_gen(x0);
+  else if constexpr (FN == FN_PEXPM1) return renorm_fast_c(texpm1_gen(x0, x1));
+  else if constexpr (FN == FN_PLOG0) {                       // explog.py:225-232
+    if (x0 == T(0)) return mk(-INF, -INF);
+    if (x0 == INF) return mk(INF, INF);
+    return renorm_fast_c(log_core_c(x0, T(0)));
+  } else if constexpr (FN == FN_TLOG0) {                     // explog.py:234-237
+    return correct_c(log_core_c(x0, T(0)), log_cr(x0));
+  } else if constexpr (FN == FN_TLOGP) {                     // explog.py:239-242
+    return correct_c(log_core_c(x0, x1), log_cr(x0));
+  } else if constexpr (FN == FN_PLOG) {                      // explog.py:251-258
+    if (x0 == T(0)) return mk(-INF, -INF);
+    if (x0 == INF) return mk(INF, INF);
+    return renorm_fast_c(log_core_c(x0, x1));
+  } else if constexpr (FN == FN_PLOG1P0) {                   // explog.py:296-303
+    if (x0 == T(-1)) return mk(-INF, -INF);
+    if (x0 == INF) return mk(INF, INF);
+    return renorm_fast_c(plog1p0_raw_c(x0));
+  } else if constexpr (FN == FN_TLOG1P0) {                   // explog.py:305-308
+    return correct_c(plog1p0_raw_c(x0), log1p_cr(x0));
+  } else if constexpr (FN == FN_TLOG1PP) {                   // explog.py:310-312
+    return correct_c(plog1p_raw_c(mk(x0, x1)), log1p_cr(x0));
+  } else {                                                   // plog1p, explog.py:319-325
+    if (x0 == T(-1) && x1 == T(0)) return mk(-INF, -INF);
+    if (x0 == INF) return mk(INF, INF);
+    return renorm_fast_c(plog1p_raw_c(mk(x0, x1)));
+  }
 }
 
 }  // namespace tf

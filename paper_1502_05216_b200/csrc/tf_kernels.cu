@@ -248,6 +248,24 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   }
 }
 
+// ------------------------------------------------- sibling functions
+// The sixteen non-TWOFOLD_ARG functions (explog.py:101-325) run the exact path
+// element by element (grid-stride, scalar SoA access): correct for every input,
+// ~10x below the admission-band kernels.  texpp / texpm1p alias the fast texp /
+// texpm1 kernels and pexp / pexpm1 add a renorm_fast epilogue to them.
+template <class T, int FN>
+__global__ void __launch_bounds__(256) k_gen(const T* __restrict__ x0, const T* __restrict__ x1,
+                                             T* __restrict__ z0, T* __restrict__ z1, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    T a = x0[i];
+    T b = dotted_fn(FN) ? T(0) : x1[i];
+    TF<T> r = eval_gen<T, FN>(a, b);
+    z0[i] = r.v;
+    z1[i] = r.e;
+  }
+}
+
 // ------------------------------------------------------------ generator
 // Bit-identical twin of paper_1502_05216_b200/workloads.py:generate.
 TF_DEV uint64_t mix64(uint64_t z) {
@@ -447,11 +465,32 @@ int launch_one(const T* x0, const T* x1, T* z0, T* z1, int64_t n, cudaStream_t s
 }
 
 template <class T, int FN>
+int launch_gen(const T* x0, const T* x1, T* z0, T* z1, int64_t n, cudaStream_t s) {
+  static int occ = 0;
+  if (!occ) {
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, tf::k_gen<T, FN>, 256, 0);
+    occ = v > 0 ? v : 1;
+  }
+  int64_t grid = (int64_t)device_sms() * occ;
+  int64_t need = (n + 255) / 256;
+  if (need < grid) grid = need;
+  tf::k_gen<T, FN><<<(unsigned)grid, 256, 0, s>>>(x0, x1, z0, z1, (uint64_t)n);
+  return cuda_check("k_gen launch");
+}
+
+template <class T, int FN>
 int launch(const T* x0, const T* x1, T* z0, T* z1, int64_t n, void* stream, int flags) {
   if (n < 0) return fail(TF_ERR_ARG, "negative element count%s");
   if (n == 0) return TF_OK;
+  if (tf::dotted_fn(FN) && !x1) x1 = x0;  // plain-argument functions never read x1
   if (!x0 || !x1 || !z0 || !z1) return fail(TF_ERR_ARG, "null pointer%s");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  constexpr bool FAST = FN == tf::FN_TEXP || FN == tf::FN_TEXPM1 || FN == tf::FN_TLOG ||
+                        FN == tf::FN_TLOG1P || FN == tf::FN_PEXP || FN == tf::FN_PEXPM1;
+  if constexpr (!FAST) {
+    return launch_gen<T, FN>(x0, x1, z0, z1, n, s);
+  }
   uintptr_t al = (uintptr_t)x0 | (uintptr_t)x1 | (uintptr_t)z0 | (uintptr_t)z1;
   if ((al & 15) == 0) {
     if constexpr (sizeof(T) == 8) return launch_one<T, FN, TF_VW64>(x0, x1, z0, z1, n, s, flags);
@@ -502,6 +541,31 @@ uint64_t mix64h(uint64_t z) {
 
 }  // namespace
 
+template <class T>
+int eval_dispatch(int fn, const T* a, const T* b, T* c, T* d, int64_t n, void* st, int fl) {
+  switch (fn) {
+    case TF_FN_TEXP: case TF_FN_TEXPP: return launch<T, tf::FN_TEXP>(a, b, c, d, n, st, fl);
+    case TF_FN_TEXPM1: case TF_FN_TEXPM1P: return launch<T, tf::FN_TEXPM1>(a, b, c, d, n, st, fl);
+    case TF_FN_TLOG: return launch<T, tf::FN_TLOG>(a, b, c, d, n, st, fl);
+    case TF_FN_TLOG1P: return launch<T, tf::FN_TLOG1P>(a, b, c, d, n, st, fl);
+    case TF_FN_PEXP: return launch<T, tf::FN_PEXP>(a, b, c, d, n, st, fl);
+    case TF_FN_PEXPM1: return launch<T, tf::FN_PEXPM1>(a, b, c, d, n, st, fl);
+    case TF_FN_PEXP0: return launch<T, tf::FN_PEXP0>(a, b, c, d, n, st, fl);
+    case TF_FN_TEXP0: return launch<T, tf::FN_TEXP0>(a, b, c, d, n, st, fl);
+    case TF_FN_PEXPM10: return launch<T, tf::FN_PEXPM10>(a, b, c, d, n, st, fl);
+    case TF_FN_TEXPM10: return launch<T, tf::FN_TEXPM10>(a, b, c, d, n, st, fl);
+    case TF_FN_PLOG0: return launch<T, tf::FN_PLOG0>(a, b, c, d, n, st, fl);
+    case TF_FN_TLOG0: return launch<T, tf::FN_TLOG0>(a, b, c, d, n, st, fl);
+    case TF_FN_TLOGP: return launch<T, tf::FN_TLOGP>(a, b, c, d, n, st, fl);
+    case TF_FN_PLOG: return launch<T, tf::FN_PLOG>(a, b, c, d, n, st, fl);
+    case TF_FN_PLOG1P0: return launch<T, tf::FN_PLOG1P0>(a, b, c, d, n, st, fl);
+    case TF_FN_TLOG1P0: return launch<T, tf::FN_TLOG1P0>(a, b, c, d, n, st, fl);
+    case TF_FN_TLOG1PP: return launch<T, tf::FN_TLOG1PP>(a, b, c, d, n, st, fl);
+    case TF_FN_PLOG1P: return launch<T, tf::FN_PLOG1P>(a, b, c, d, n, st, fl);
+  }
+  return fail(TF_ERR_ARG, "unknown function code%s");
+}
+
 extern "C" {
 
 TF_API int tf_version(void) { return TF_ABI_VERSION; }
@@ -530,28 +594,13 @@ TF_DEF(tf_tlog1p_f32, float, tf::FN_TLOG1P)
 
 TF_API int tf_eval(int fn, int width, const void* x0, const void* x1, void* z0, void* z1,
                    int64_t n, void* stream, int flags) {
-  if (width == 64) {
-    auto a = static_cast<const double*>(x0), b = static_cast<const double*>(x1);
-    auto c = static_cast<double*>(z0), d = static_cast<double*>(z1);
-    switch (fn) {
-      case TF_FN_TEXP: return launch<double, tf::FN_TEXP>(a, b, c, d, n, stream, flags);
-      case TF_FN_TEXPM1: return launch<double, tf::FN_TEXPM1>(a, b, c, d, n, stream, flags);
-      case TF_FN_TLOG: return launch<double, tf::FN_TLOG>(a, b, c, d, n, stream, flags);
-      case TF_FN_TLOG1P: return launch<double, tf::FN_TLOG1P>(a, b, c, d, n, stream, flags);
-    }
-  } else if (width == 32) {
-    auto a = static_cast<const float*>(x0), b = static_cast<const float*>(x1);
-    auto c = static_cast<float*>(z0), d = static_cast<float*>(z1);
-    switch (fn) {
-      case TF_FN_TEXP: return launch<float, tf::FN_TEXP>(a, b, c, d, n, stream, flags);
-      case TF_FN_TEXPM1: return launch<float, tf::FN_TEXPM1>(a, b, c, d, n, stream, flags);
-      case TF_FN_TLOG: return launch<float, tf::FN_TLOG>(a, b, c, d, n, stream, flags);
-      case TF_FN_TLOG1P: return launch<float, tf::FN_TLOG1P>(a, b, c, d, n, stream, flags);
-    }
-  } else {
-    return fail(TF_ERR_ARG, "unsupported width (expected 32 or 64)%s");
-  }
-  return fail(TF_ERR_ARG, "unknown function code%s");
+  if (width == 64)
+    return eval_dispatch<double>(fn, static_cast<const double*>(x0), static_cast<const double*>(x1),
+                                 static_cast<double*>(z0), static_cast<double*>(z1), n, stream, flags);
+  if (width == 32)
+    return eval_dispatch<float>(fn, static_cast<const float*>(x0), static_cast<const float*>(x1),
+                                static_cast<float*>(z0), static_cast<float*>(z1), n, stream, flags);
+  return fail(TF_ERR_ARG, "unsupported width (expected 32 or 64)%s");
 }
 
 TF_API int tf_generate(int dist, uint64_t seed, int64_t start, int64_t n, void* x0, void* x1,

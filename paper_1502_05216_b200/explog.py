@@ -1,6 +1,6 @@
 """Drop-in twofold exp/log surface, B200 edition.
 
-Mirrors the reference public API (pkg/src/twofold/explog.py:44-62, 219-499;
+Mirrors the reference public API (pkg/src/twofold/explog.py:44-62, 69-349;
 __init__.py:19-57): ``api(width, backend=None) -> ExpLog``, ``ExpLog.texp /
 texpm1 / tlog / tlog1p``, ``ExpLog.function(name)``, ``get_function(name,
 width, backend=None)``, ``FAMILIES``, ``FUNCTION_NAMES``, ``DOTTED_ARG``,
@@ -14,9 +14,14 @@ and the current stream, results allocated there), CPU tensors or numpy arrays
 evaluation runs the hand-written sm_100a kernels of libtwofold_b200.so; there
 is no CPU fallback.
 
-Of the twenty reference functions the four twofold-argument ones
-(TWOFOLD_ARG) are implemented; the other sixteen (explog.py:251-475) are the
-next rows of the coverage plan and raise NotImplementedError here.
+All twenty reference functions are served.  The four twofold-argument ones
+(TWOFOLD_ARG) run the admission-band fast kernels; ``texpp``/``texpm1p`` are
+the same kernels and ``pexp``/``pexpm1`` add a renorm epilogue to them; the
+other twelve (explog.py:101-325) run the element-wise exact-path kernel.
+DOTTED_ARG functions take a plain argument (a scalar, array or tensor, not a
+pair).  COUPLED_ARG functions assume |x1| <= ulp(x0)/2 like the reference;
+where the reference raises OverflowError for a non-coupled argument
+(math.ldexp, explog.py:192) the GPU returns a value instead of raising.
 """
 
 from __future__ import annotations
@@ -78,7 +83,7 @@ class ExpLog:
         self.params = params
         self._np = np.float64 if width == 64 else np.float32
 
-    # ---- the four twofold-argument functions (explog.py:265, 299, 394, 464)
+    # ---- the four twofold-argument functions (explog.py:115, 149, 244, 314)
     def texp(self, x, out=None):
         """Twofold e**(x0+x1); value part = correctly rounded exp(x0)."""
         return self._call("texp", x, out)
@@ -95,23 +100,85 @@ class ExpLog:
         """Twofold ln(1 + y0 + y1); value part = correctly rounded log1p(y0)."""
         return self._call("tlog1p", y, out)
 
+    # ---- the sixteen siblings (explog.py:101-325)
+    def pexp0(self, x, out=None):
+        """Pair e**x of a plain x (pexp0, explog.py:101-103)."""
+        return self._call("pexp0", x, out)
+
+    def texp0(self, x, out=None):
+        """Twofold e**x of a plain x (texp0, explog.py:105-113)."""
+        return self._call("texp0", x, out)
+
+    def texpp(self, x, out=None):
+        """Twofold e**(x0+x1) of a coupled twofold (texpp, explog.py:127-129)."""
+        return self._call("texpp", x, out)
+
+    def pexp(self, x, out=None):
+        """Renormalised pair e**(x0+x1) of a coupled twofold (pexp, explog.py:131-133)."""
+        return self._call("pexp", x, out)
+
+    def pexpm10(self, x, out=None):
+        """Pair e**x - 1 of a plain x (pexpm10, explog.py:135-137)."""
+        return self._call("pexpm10", x, out)
+
+    def texpm10(self, x, out=None):
+        """Twofold e**x - 1 of a plain x (texpm10, explog.py:139-147)."""
+        return self._call("texpm10", x, out)
+
+    def texpm1p(self, x, out=None):
+        """Twofold e**(x0+x1) - 1 of a coupled twofold (texpm1p, explog.py:162-163)."""
+        return self._call("texpm1p", x, out)
+
+    def pexpm1(self, x, out=None):
+        """Renormalised pair e**(x0+x1) - 1 (pexpm1, explog.py:165-166)."""
+        return self._call("pexpm1", x, out)
+
+    def plog0(self, y, out=None):
+        """Pair ln y of a plain y (plog0, explog.py:225-232)."""
+        return self._call("plog0", y, out)
+
+    def tlog0(self, y, out=None):
+        """Twofold ln y of a plain y (tlog0, explog.py:234-237)."""
+        return self._call("tlog0", y, out)
+
+    def tlogp(self, y, out=None):
+        """Twofold ln(y0+y1) of a coupled twofold (tlogp, explog.py:239-242)."""
+        return self._call("tlogp", y, out)
+
+    def plog(self, y, out=None):
+        """Pair ln(y0+y1) of a coupled twofold (plog, explog.py:251-258)."""
+        return self._call("plog", y, out)
+
+    def plog1p0(self, y, out=None):
+        """Pair ln(1+y) of a plain y (plog1p0, explog.py:296-303)."""
+        return self._call("plog1p0", y, out)
+
+    def tlog1p0(self, y, out=None):
+        """Twofold ln(1+y) of a plain y (tlog1p0, explog.py:305-308)."""
+        return self._call("tlog1p0", y, out)
+
+    def tlog1pp(self, y, out=None):
+        """Twofold ln(1+y0+y1) of a coupled twofold (tlog1pp, explog.py:310-312)."""
+        return self._call("tlog1pp", y, out)
+
+    def plog1p(self, y, out=None):
+        """Pair ln(1+y0+y1) of a coupled twofold (plog1p, explog.py:319-325)."""
+        return self._call("plog1p", y, out)
+
     def function(self, name: str):
         if name not in FUNCTION_NAMES:
             raise ValueError(f"unknown function {name!r}")
-        if name not in TWOFOLD_ARG:
-            raise NotImplementedError(
-                f"{name!r} is not on the B200 hot path yet (implemented: "
-                f"{', '.join(sorted(TWOFOLD_ARG))})")
         return getattr(self, name)
-
-    def __getattr__(self, name):
-        if name in FUNCTION_NAMES:
-            return self.function(name)
-        raise AttributeError(name)
 
     # ---- dispatch
     def _call(self, fn: str, x, out=None):
-        x0, x1 = x[0], x[1]
+        if fn in DOTTED_ARG:
+            # plain argument: the kernel never reads x1, so alias it to x0
+            if isinstance(x, Twofold) or isinstance(x, tuple):
+                raise TypeError(f"{fn} takes a plain argument, not a twofold")
+            x0 = x1 = x
+        else:
+            x0, x1 = x[0], x[1]
         if _is_torch(x0) or _is_torch(x1):
             if not (_is_torch(x0) and _is_torch(x1)):
                 raise TypeError("both twofold parts must be torch tensors")
@@ -208,6 +275,7 @@ def _pipeline(lib: ExpLog, fn: str, h0, h1, device=None, chunk: int = HOST_CHUNK
                            "(sm_100a); there is no CPU fallback")
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     n = h0.numel()
+    dotted = fn in DOTTED_ARG
     pinned = h0.is_pinned() and h1.is_pinned()
     if out is not None:
         z0, z1 = out
@@ -218,7 +286,7 @@ def _pipeline(lib: ExpLog, fn: str, h0, h1, device=None, chunk: int = HOST_CHUNK
         return z0, z1
     if not pinned:
         h0 = h0.pin_memory()
-        h1 = h1.pin_memory()
+        h1 = h0 if dotted else h1.pin_memory()
     c = min(chunk, n)
     streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
     bufs = [[torch.empty(c, dtype=h0.dtype, device=dev) for _ in range(4)] for _ in range(2)]
@@ -231,7 +299,10 @@ def _pipeline(lib: ExpLog, fn: str, h0, h1, device=None, chunk: int = HOST_CHUNK
         d0, d1, e0, e1 = (b[:m] for b in bufs[k & 1])
         with torch.cuda.stream(s):
             d0.copy_(h0[off:off + m], non_blocking=True)
-            d1.copy_(h1[off:off + m], non_blocking=True)
+            if dotted:
+                d1 = d0
+            else:
+                d1.copy_(h1[off:off + m], non_blocking=True)
             lib._launch(fn, d0, d1, e0, e1, m, s.cuda_stream)
             z0[off:off + m].copy_(e0, non_blocking=True)
             z1[off:off + m].copy_(e1, non_blocking=True)
@@ -246,7 +317,7 @@ def _api_cached(width: int, backend: str) -> ExpLog:
 
 
 def api(width: int, backend: str | None = None) -> ExpLog:
-    """Cached function surface for (width, backend) (explog.py:488-494)."""
+    """Cached function surface for (width, backend) (explog.py:338-344)."""
     if backend is None:
         backend = get_default_backend()
     elif backend not in ("fma", "dv"):
@@ -255,6 +326,6 @@ def api(width: int, backend: str | None = None) -> ExpLog:
 
 
 def get_function(name: str, width: int, backend: str | None = None):
-    """Resolve one of the twenty function names for a width (explog.py:497-499)."""
+    """Resolve one of the twenty function names for a width (explog.py:347-349)."""
     return api(width, backend).function(name)
 

@@ -9,6 +9,10 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 FNS = ("texp", "texpm1", "tlog", "tlog1p")
+# the other sixteen names of FUNCTION_NAMES (reference explog.py:44-53)
+SIBLINGS = ("pexp0", "texp0", "texpp", "pexp", "pexpm10", "texpm10", "texpm1p", "pexpm1",
+            "plog0", "tlog0", "tlogp", "plog", "plog1p0", "tlog1p0", "tlog1pp", "plog1p")
+ALL_FNS = FNS + SIBLINGS
 
 
 def pytest_configure(config):

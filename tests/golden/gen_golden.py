@@ -3,7 +3,7 @@
     PYTHONPATH=/root/reference/pkg/src python tests/golden/gen_golden.py
 
 For each (function, width) it evaluates the reference's own public API
-(``twofold.api(width).<fn>((x0, x1))``, explog.py:265-467) element by element on
+(``twofold.api(width).<fn>((x0, x1))``, explog.py:115-317) element by element on
 
   * a seeded sample of the BASELINE.json config distribution
     (paper_1502_05216_b200.workloads.generate, global indices [0, N_CFG)),
@@ -109,10 +109,21 @@ def edge_x0(fn: str, width: int, rng: np.random.Generator, n: int) -> np.ndarray
     return x0.astype(np.float32 if width == 32 else np.float64)
 
 
-def build_inputs(fn: str, width: int):
+# the sixteen sibling functions (explog.py:101-325), keyed to their family's
+# hot-path function for inputs; smaller samples
+FAMILY_OF = {
+    "pexp0": "texp", "texp0": "texp", "texpp": "texp", "pexp": "texp",
+    "pexpm10": "texpm1", "texpm10": "texpm1", "texpm1p": "texpm1", "pexpm1": "texpm1",
+    "plog0": "tlog", "tlog0": "tlog", "tlogp": "tlog", "plog": "tlog",
+    "plog1p0": "tlog1p", "tlog1p0": "tlog1p", "tlog1pp": "tlog1p", "plog1p": "tlog1p",
+}
+N_SIB = 1000
+
+
+def build_inputs(fn: str, width: int, n_cfg: int = N_CFG, n_edge: int = N_EDGE):
     dt = np.float32 if width == 32 else np.float64
     p = 53 if width == 64 else 24
-    x0c, x1c = generate(DIST[(fn, width)], 0, N_CFG, seed=SEED)
+    x0c, x1c = generate(DIST[(fn, width)], 0, n_cfg, seed=SEED)
     sx0, sx1 = [], []
     for a in special_x0(fn, width):
         a = float(dt(a))
@@ -120,8 +131,8 @@ def build_inputs(fn: str, width: int):
             sx0.append(a)
             sx1.append(b)
     rng = np.random.default_rng(SEED + width + len(fn))
-    ex0 = edge_x0(fn, width, rng, N_EDGE)
-    u = rng.uniform(-1.0, 1.0, N_EDGE)
+    ex0 = edge_x0(fn, width, rng, n_edge)
+    u = rng.uniform(-1.0, 1.0, n_edge)
     ex1 = (ex0.astype(np.float64) * u * 2.0 ** -p).astype(dt)
     x0 = np.concatenate([x0c.astype(dt), np.array(sx0, dt), ex0])
     x1 = np.concatenate([x1c.astype(dt), np.array(sx1, dt), ex1])
@@ -159,6 +170,31 @@ def main():
                 z1[i] = dt(r.error)
             path = os.path.join(out_dir, f"golden_{fn}_f{width}.npz")
             np.savez_compressed(path, x0=x0, x1=x1, z0=z0, z1=z1, n_cfg=N_CFG,
+                                provenance=json.dumps(prov))
+            print(f"{path}: {x0.size} vectors", file=sys.stderr)
+        for fn, fam in FAMILY_OF.items():
+            x0, x1 = build_inputs(fam, width, N_SIB, N_EDGE // 3)
+            f = getattr(lib, fn)
+            dotted = fn.endswith("0")
+            if dotted:
+                x1 = np.zeros_like(x1)       # dotted argument: x0 only
+            z0 = np.empty_like(x0)
+            z1 = np.empty_like(x1)
+            keep = np.ones(x0.size, bool)
+            for i in range(x0.size):
+                try:
+                    r = f(float(x0[i])) if dotted else f((float(x0[i]), float(x1[i])))
+                except OverflowError:
+                    # coupled-argument functions (tlogp, plog, ...) given a
+                    # non-coupled special-grid input: math.ldexp raises in the
+                    # reference (explog.py:192); no golden value exists
+                    keep[i] = False
+                    continue
+                z0[i] = dt(r.value)
+                z1[i] = dt(r.error)
+            x0, x1, z0, z1 = x0[keep], x1[keep], z0[keep], z1[keep]
+            path = os.path.join(out_dir, f"golden_{fn}_f{width}.npz")
+            np.savez_compressed(path, x0=x0, x1=x1, z0=z0, z1=z1, n_cfg=N_SIB,
                                 provenance=json.dumps(prov))
             print(f"{path}: {x0.size} vectors", file=sys.stderr)
 

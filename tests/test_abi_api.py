@@ -1,7 +1,7 @@
 """CPU-side checks of the drop-in boundary: the C-ABI library loads and exports
 every symbol include/twofold_b200.h declares, argument errors come back as
 status codes without touching a GPU, and the Python surface mirrors the
-reference package (pkg/src/twofold/explog.py:44-62, 483-499; __init__.py)."""
+reference package (pkg/src/twofold/explog.py:44-62, 333-349; __init__.py)."""
 
 import ctypes
 import os
@@ -46,7 +46,11 @@ def test_abi_argument_errors_without_gpu():
     assert L.tf_eval(0, 64, None, None, None, None, 5, None, 0) == _lib.TF_ERR_ARG
     assert b"null" in L.tf_last_error()
     assert L.tf_eval(0, 16, 8, 8, 8, 8, 5, None, 0) == _lib.TF_ERR_ARG
-    assert L.tf_eval(9, 64, 8, 8, 8, 8, 5, None, 0) == _lib.TF_ERR_ARG
+    assert L.tf_eval(20, 64, 8, 8, 8, 8, 5, None, 0) == _lib.TF_ERR_ARG     # TF_FN_COUNT
+    assert L.tf_eval(-1, 32, 8, 8, 8, 8, 5, None, 0) == _lib.TF_ERR_ARG
+    assert b"unknown function" in L.tf_last_error()
+    # a plain-argument (dotted) function accepts x1 == NULL, the others do not
+    assert L.tf_eval(_lib.FN_CODES["tlog"], 64, 8, None, 8, 8, 5, None, 0) == _lib.TF_ERR_ARG
     assert L.tf_texp_f64(None, None, None, None, 0, None) == 0
     assert L.tf_generate(99, 0, 0, 10, 8, 8, None) == _lib.TF_ERR_ARG
     assert L.tf_exact_count(None, 0) == _lib.TF_ERR_ARG
@@ -79,11 +83,33 @@ def test_api_surface_matches_reference():
     with pytest.raises(ValueError):
         P.get_function("nope", 64)
     assert P.get_function("texp", 64) == f.texp
-    with pytest.raises(NotImplementedError):
-        P.get_function("pexp0", 64)
+    for name in P.FUNCTION_NAMES:                  # all twenty are served
+        assert P.get_function(name, 32) == getattr(P.api(32), name)
+    assert sorted(_codes()) == sorted(P.FUNCTION_NAMES)
     t = P.Twofold(1.0, 2.0)
     assert t.value == 1.0 and t.error == 2.0
     P.assert_round_to_nearest()
+
+
+def _codes():
+    from paper_1502_05216_b200 import _lib
+
+    assert sorted(_lib.FN_CODES.values()) == list(range(20))
+    return _lib.FN_CODES
+
+
+def test_function_codes_match_header():
+    """_lib.FN_CODES mirrors the TF_FN_* macros of include/twofold_b200.h."""
+    import os
+    import re
+
+    from paper_1502_05216_b200 import _lib
+
+    hdr = open(os.path.join(os.path.dirname(__file__), "..", "include", "twofold_b200.h")).read()
+    macros = {m.group(1).lower(): int(m.group(2))
+              for m in re.finditer(r"#define TF_FN_([A-Z0-9]+) (\d+)", hdr)}
+    assert macros.pop("count") == 20
+    assert macros == _lib.FN_CODES
 
 
 def test_backend_default_roundtrip():

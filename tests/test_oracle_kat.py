@@ -18,7 +18,7 @@ LN2 = float.fromhex("0x1.62e42fefa39efp-1")
 INF, NAN = math.inf, math.nan
 
 
-# ---- decomposition (test_expcore.py:73-141)
+# ---- decomposition (test_expcore.py:37-106)
 def test_decompose_exp_examples():
     assert O.decompose_exp(1.0) == (0, 32, 0.0)
     assert O.decompose_exp(0.0) == (0, 0, 0.0)
@@ -50,7 +50,7 @@ def test_decompose_exact_random():
         assert abs(y) <= 2.0 ** -6
 
 
-# ---- Taylor cores (test_expcore.py:144-185)
+# ---- Taylor cores (test_expcore.py:108-149)
 def test_taylor_at_zero():
     assert O.taylor_exp(0.0) == (F12, 0.0)
     assert O.taylor_expm1(0.0) == (0.0, 0.0)
@@ -65,7 +65,7 @@ def test_taylor_exp_accuracy(y):
     assert rel <= 2.0 ** -100
 
 
-# ---- pexp0 / pexpm10 (test_expcore.py:187-265)
+# ---- pexp0 / pexpm10 (test_expcore.py:151-230)
 def test_pexp0_saturation_and_one():
     assert O.pexp0_raw(0.0) == (1.0, 0.0)
     assert O.pexp0_raw(-745.0) == (0.0, 0.0)
