@@ -171,7 +171,7 @@ METRIC = "twofold evals/sec (cfg2: texpm1+tlog1p float64, N=2^24 each)"
 def run_ours(args):
     import torch
 
-    from paper_1502_05216_b200 import Twofold, _lib, api, workloads
+    from paper_1502_05216_b200 import DOTTED_ARG, FAMILIES, Twofold, _lib, api, family_of, workloads
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -271,7 +271,7 @@ def run_ours(args):
         peak[width] = max(peak_by_op[f"f{width}_{n}"] for n in ("fma", "add", "mul"))
 
     # ---- per-function kernel rates at their configs
-    per_fn = {}
+    per_fn, siblings = {}, {}
     if not args.headline_only:
         for (fn, width), cfg in PER_FN.items():
             _, _, dname, _ = workloads.CONFIGS[cfg]
@@ -280,16 +280,20 @@ def run_ours(args):
             a0, a1 = gen(dname, m, dt, rank * m)
             z0, z1 = torch.empty_like(a0), torch.empty_like(a1)
             lib = api(width)
-            for _ in range(max(3, args.warmup)):
-                lib._launch(fn, a0, a1, z0, z1, m, sp)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = max(5, min(args.steps, 50))
-            e0.record(stream)
-            for _ in range(reps):
-                lib._launch(fn, a0, a1, z0, z1, m, sp)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ms = max_over_ranks(e0.elapsed_time(e1) / reps)
+
+            def time_fn(name, reps):
+                b1 = a0 if name in DOTTED_ARG else a1      # plain argument: x1 unused
+                for _ in range(max(3, args.warmup)):
+                    lib._launch(name, a0, b1, z0, z1, m, sp)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(reps):
+                    lib._launch(name, a0, b1, z0, z1, m, sp)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                return max_over_ranks(e0.elapsed_time(e1) / reps)
+
+            ms = time_fn(fn, max(5, min(args.steps, 50)))
             rate = m * world / (ms * 1e-3)
             ops = ALG_OPS[(fn, width)] * m / (ms * 1e-3)
             gbs = (32 if width == 64 else 16) * m / (ms * 1e-3) / 1e9
@@ -297,6 +301,17 @@ def run_ours(args):
                 "config": cfg, "elements": m, "ms": ms, "elements_per_s": rate,
                 "alg_gops": ops / 1e9, "fp_pipe_frac": ops / peak[width],
                 "hbm_gbs": gbs, "hbm_frac": gbs / _peaks()["hbm_gbs"]}
+            if not args.no_siblings:
+                # the other four functions of the family, same inputs (a dotted
+                # function reads x0 only)
+                for name in FAMILIES[family_of(fn)]:
+                    if name == fn:
+                        continue
+                    sms = time_fn(name, 5)
+                    siblings[f"{name}_f{width}"] = {
+                        "config": cfg, "elements": m, "ms": sms,
+                        "elements_per_s": m * world / (sms * 1e-3),
+                        "vs_" + fn: ms / sms}
             del a0, a1, z0, z1
 
     # ---- end to end through the public API with pinned host buffers
@@ -372,6 +387,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "per_function": per_fn,
+            "siblings": siblings,
             "parity_sample": stats,
         }
         print(json.dumps(line), flush=True)
@@ -441,6 +457,7 @@ def main():
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-siblings", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -358,7 +358,8 @@ TF_DEV double rn_guard(double h, double l, bool& hard) {  // binary64 cores: ~2^
 }
 
 // ================================================================ texp
-template <int VW>
+// PM = true: pexp0 = renorm_fast(pexp0_raw(x0)) (explog.py:101-103), no libm value
+template <int VW, bool PM = false>
 TF_DEV void fast_texp(const STab<double>& tb, const double (&x0)[VW], const double (&x1)[VW],
                       double (&z0)[VW], double (&z1)[VW], bool (&ok)[VW]) {
   double y[VW];
@@ -375,6 +376,12 @@ TF_DEV void fast_texp(const STab<double>& tb, const double (&x0)[VW], const doub
   for (int e = 0; e < VW; ++e) {
     TF<double> ct = t_mul_u(tv<double>(tb.C[n[e] - P<double>::C_LO]), t[e]);
     TF<double> v = t_mul_u(tv<double>(tb.E[m[e] - P<double>::E_LO]), ct);
+    if constexpr (PM) {
+      TF<double> r = fast_two_sum_u(v.v, v.e);
+      z0[e] = r.v;
+      z1[e] = r.e;
+      continue;
+    }
     double zz = add(v.v, v.e);                                  // CR exp(x0)
     if (m[e] <= TF64_ESC_LO + TF64_ESC_COUNT - 1) {
       // e^x < 2^-987: the unscaled product's residuals underflow, so round the
@@ -387,7 +394,7 @@ TF_DEV void fast_texp(const STab<double>& tb, const double (&x0)[VW], const doub
   }
 }
 
-template <int VW>
+template <int VW, bool PM = false>
 TF_DEV void fast_texp(const STab<float>& tb, const float (&x0)[VW], const float (&x1)[VW],
                       float (&z0)[VW], float (&z1)[VW], bool (&ok)[VW]) {
   float y[VW];
@@ -405,6 +412,12 @@ TF_DEV void fast_texp(const STab<float>& tb, const float (&x0)[VW], const float 
     TF<float> ct = t_mul_u(tv<float>(tb.C[n[e] - P<float>::C_LO]), t[e]);
     TF<float> ev = tv<float>(tb.E[m[e] - P<float>::E_LO]);
     TF<float> v = t_mul_u(ev, ct);
+    if constexpr (PM) {
+      TF<float> r = fast_two_sum_u(v.v, v.e);
+      z0[e] = r.v;
+      z1[e] = r.e;
+      continue;
+    }
     // value part: near the subnormal range use the 2^64-scaled coarse table so
     // the twofold keeps full precision (result is normal: exact unscaling)
     bool scaled = m[e] <= -35;  // e^(2m) < 2^-100: residuals would underflow
@@ -419,7 +432,8 @@ TF_DEV void fast_texp(const STab<float>& tb, const float (&x0)[VW], const float 
 
 // ============================================================== texpm1
 // binary64: the in-band core is the bulk (cfg 2: 99.5%)
-template <int VW>
+// PM = true: pexpm10 = renorm_fast(pexpm10_raw(x0)) (explog.py:135-137)
+template <int VW, bool PM = false>
 TF_DEV void fast_texpm1(const STab<double>& tb, const double (&x0)[VW], const double (&x1)[VW],
                         double (&z0)[VW], double (&z1)[VW], bool (&ok)[VW]) {
   double xs[VW];
@@ -432,6 +446,12 @@ TF_DEV void fast_texpm1(const STab<double>& tb, const double (&x0)[VW], const do
   pexpm10_inband_v<double, VW>(tb, xs, w);
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
+    if constexpr (PM) {
+      TF<double> r = fast_two_sum_u(w[e].v, w[e].e);
+      z0[e] = r.v;
+      z1[e] = r.e;
+      continue;
+    }
     z0[e] = ahi(xs[e]) < H64_TINY54 ? xs[e] : add(w[e].v, w[e].e);   // CR expm1(x0)
     double tail = add(w[e].e, sub(w[e].v, z0[e]));
     z1[e] = add(mul(add(z0[e], 1.0), t1_tiny(x1[e])), tail);          // explog.py:159-160
@@ -439,7 +459,7 @@ TF_DEV void fast_texpm1(const STab<double>& tb, const double (&x0)[VW], const do
 }
 
 // binary32: the pexp0 - 1 fallback is the bulk (cfg 4: 99.2%)
-template <int VW>
+template <int VW, bool PM = false>
 TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const float (&x1)[VW],
                         float (&z0)[VW], float (&z1)[VW], bool (&ok)[VW]) {
   float y[VW];
@@ -458,6 +478,12 @@ TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const floa
     TF<float> v = t_mul_u(tv<float>(tb.E[m[e] - P<float>::E_LO]),
                           t_mul_u(tv<float>(tb.C[n[e] - P<float>::C_LO]), t[e]));
     TF<float> w = t_add_d_u(v, -1.0f);                          // expcore.py:147
+    if constexpr (PM) {
+      TF<float> r = fast_two_sum_u(w.v, w.e);
+      z0[e] = r.v;
+      z1[e] = r.e;
+      continue;
+    }
     bool hard;
     z0[e] = rn_guard<-35>(w.v, w.e, hard);
     ok[e] = ok[e] && !hard;
@@ -504,7 +530,11 @@ template <> struct LogC<float> {
   TF_DEV static float rcp(float x) { return rcp_approx(x); }
 };
 
-template <class T, int VW>
+// Variants (explog.py:225-258): RENORM = false evaluates the core on (y0, y1)
+// as given (tlogp, plog; tlog0 / plog0 have y1 = 0, where renorm is the
+// identity); PM = true returns renorm_fast(core) instead of the _correct'ed
+// value part (plog0, plog).
+template <class T, int VW, bool RENORM = true, bool PM = false>
 TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW], T (&z0)[VW],
                       T (&z1)[VW], bool (&ok)[VW]) {
   using C = LogC<T>;
@@ -518,7 +548,7 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     ok[e] = C::eb(y0i[e]) - 1u < C::NORM_SPAN && is_finite(y1i[e]);
     y0[e] = ok[e] ? y0i[e] : T(1);
     y1[e] = ok[e] ? y1i[e] : T(0);
-    v[e] = renorm_u(mk(y0[e], y1[e]));
+    v[e] = RENORM ? renorm_u(mk(y0[e], y1[e])) : mk(y0[e], y1[e]);
     ok[e] = ok[e] && C::eb(v[e].v) - 1u < C::NORM_SPAN;
     if (!ok[e]) v[e] = mk(T(1), T(0));
     auto vb = ubits(v[e].v);
@@ -529,7 +559,9 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     r0[e] = seed_log1p_t(add(sub(zc0[e], T(1)), zc1[e]),      // explog.py:196-199
                          [&](int i) { return tb.SEED[i]; });
     ok[e] = ok[e] && ahi(r0[e]) < C::LN2H;
-    mr0[e] = -r0[e];
+    // keeps the CM1 index in range for rejected lanes (tlogp / plog take y1
+    // unrenormalised, so the seed of a non-coupled input can be anything)
+    mr0[e] = ok[e] ? -r0[e] : T(0);
   }
   TF<T> s[VW];
   pexpm10_inband_v<T, VW>(tb, mr0, s);
@@ -541,6 +573,12 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     ok[e] = ok[e] && newton_quiet(r1, r0[e]);
     TF<T> nl = t_mul_d_u(mk(P<T>::LN2_V, P<T>::LN2_E), (T)n[e]);
     TF<T> core = t_add_u(mk(r0[e], r1), nl);
+    if constexpr (PM) {                                 // explog.py:205-208, 258
+      TF<T> r = n[e] == 0 ? fast_two_sum_u(r0[e], r1) : fast_two_sum_u(core.v, core.e);
+      z0[e] = r.v;
+      z1[e] = r.e;
+      continue;
+    }
     // Away from 1 (|y0 - 1| >= 2^-20, 2^-7 in binary32) |log y0| is large next
     // to d = y1/y0 (|d| <= 2^-50 |log y0|, 2^-17 in binary32), so
     // log(y0) = core - d to well below an ulp with d known to ~2^-22:
@@ -569,7 +607,12 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
 // evaluates them here with a lane-selected prologue/epilogue.
 // Value parts: log1p(y0) = log1p(v) - log1p(d), d = y1/(1 + y0) (renorm is
 // error-free); log(w0) = log(w) - log1p(w1/w0).
-template <class T, int VW>
+// Variants (explog.py:284-325): RENORM = false evaluates (y0, y1) as given
+// (tlog1pp, plog1p; the dotted ones have y1 = 0); INNER = false is
+// _plog1p0_raw's out-of-band branch, the raw _log_core of renorm(1 + y0)
+// without tlogp's inner _correct (tlog1p0, plog1p0); PM = true returns
+// renorm_fast of the raw result (plog1p0, plog1p).
+template <class T, int VW, bool RENORM = true, bool PM = false, bool INNER = true>
 TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW], T (&z0)[VW],
                         T (&z1)[VW], bool (&ok)[VW]) {
   constexpr bool D = sizeof(T) == 8;
@@ -585,7 +628,7 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
     ok[e] = is_finite(y0i[e]) && is_finite(y1i[e]);
     y0[e] = ok[e] ? y0i[e] : T(0);
     y1[e] = ok[e] ? y1i[e] : T(0);
-    v[e] = renorm_u(mk(y0[e], y1[e]));
+    v[e] = RENORM ? renorm_u(mk(y0[e], y1[e])) : mk(y0[e], y1[e]);
     if (D) inb[e] = ahi(v[e].v) < (sgn(v[e].v) ? H64_HALF : H64_ONE);
     else inb[e] = ahi(v[e].v) <= (sgn(v[e].v) ? B32_HALF : B32_ONE);
     T arg = v[e].v;
@@ -632,6 +675,12 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       }
       T x1 = add(u.v, u.e);
       ok[e] = ok[e] && newton_quiet(x1, sd[e]);
+      if constexpr (PM) {                                 // renorm_fast(_log1p_core)
+        TF<T> r = fast_two_sum_u(sd[e], x1);
+        z0[e] = r.v;
+        z1[e] = r.e;
+        continue;
+      }
       bool tiny = ahi(y0[e]) < (D ? H64_TINY54 : B32_TINY25);
       // v - y0 == y1 exactly; with |d| <= 2^-48 |log1p(y0)| (2^-21 binary32)
       // ~2^-22 accuracy of d suffices; below 2^-54 the value part is y0 itself
@@ -650,6 +699,12 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       ok[e] = ok[e] && newton_quiet(r1, sd[e]);
       TF<T> nl = t_mul_d_u(mk(P<T>::LN2_V, P<T>::LN2_E), (T)n[e]);
       TF<T> core = t_add_u(mk(sd[e], r1), nl);
+      if constexpr (PM && !INNER) {                       // renorm_fast(_log_core(w))
+        TF<T> r = n[e] == 0 ? fast_two_sum_u(sd[e], r1) : fast_two_sum_u(core.v, core.e);
+        z0[e] = r.v;
+        z1[e] = r.e;
+        continue;
+      }
       // tlogp's value part log(w0) (correct, 366-373): w1/w0 = zc1/zc0
       // (out-of-band: |log w0| >= ln 2 - tiny, |w1/w0| <= 2^-24)
       T rc = rcp_nr(zc0[e]);
@@ -657,6 +712,12 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       T t0 = rn_guard(core.v, sub(core.e, mul(zc1[e], rc)), hard0);
       ok[e] = ok[e] && !hard0;
       T t1 = add(core.e, sub(core.v, t0));
+      if constexpr (PM) {                                 // renorm_fast(tlogp(w))
+        TF<T> r = fast_two_sum_u(t0, t1);
+        z0[e] = r.v;
+        z1[e] = r.e;
+        continue;
+      }
       // final value part log1p(y0) = log(w) - log1p(y1 / (1 + y0))
       // 1 + y0 ~ w0 = zc0 * 2^n: divide in the scaled domain (1/(1 + y0) can
       // underflow the approximate reciprocal when y0 ~ FLT_MAX)
@@ -665,7 +726,8 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       T zz = rn_guard(core.v, sub(core.e, fmaop(mul(T(-0.5), dd), dd, dd)), hard);
       ok[e] = ok[e] && !hard;
       z0[e] = zz;
-      z1[e] = add(t1, sub(t0, zz));                      // _correct (372-373)
+      if constexpr (INNER) z1[e] = add(t1, sub(t0, zz));  // _correct (222-223)
+      else z1[e] = add(core.e, sub(core.v, zz));
     }
   }
 }
@@ -682,7 +744,7 @@ template <int VW> struct Xch {
 // the in-band / out-of-band epilogues no longer run back to back under
 // divergence.  Element k = e*32 + lane goes to slot rank_A(k) (in-band) or
 // n_A + rank_B(k); results travel back through the same buffer.
-template <int VW>
+template <int VW, bool RENORM, bool PM, bool INNER>
 TF_DEV void tlog1p_sorted(const STab<float>& tb, Xch<VW>* xw, const float (&x0)[VW],
                           const float (&x1)[VW], float (&z0)[VW], float (&z1)[VW],
                           bool (&ok)[VW]) {
@@ -692,7 +754,8 @@ TF_DEV void tlog1p_sorted(const STab<float>& tb, Xch<VW>* xw, const float (&x0)[
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
     bool fin = is_finite(x0[e]) && is_finite(x1[e]);
-    TF<float> v = renorm_u(mk(fin ? x0[e] : 0.0f, fin ? x1[e] : 0.0f));
+    TF<float> v = mk(fin ? x0[e] : 0.0f, fin ? x1[e] : 0.0f);
+    if (RENORM) v = renorm_u(v);
     bool inb = ahi(v.v) <= (sgn(v.v) ? B32_HALF : B32_ONE);
     m[e] = __ballot_sync(0xffffffffu, inb);
     pre[e] = nA;
@@ -719,7 +782,7 @@ TF_DEV void tlog1p_sorted(const STab<float>& tb, Xch<VW>* xw, const float (&x0)[
     sk[e] = xw->src[e * 32 + lane];
   }
   __syncwarp();
-  fast_tlog1p<float, VW>(tb, p0, p1, q0, q1, pok);
+  fast_tlog1p<float, VW, RENORM, PM, INNER>(tb, p0, p1, q0, q1, pok);
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
     xw->a[sk[e]] = q0[e];
@@ -736,15 +799,46 @@ TF_DEV void tlog1p_sorted(const STab<float>& tb, Xch<VW>* xw, const float (&x0)[
   __syncwarp();
 }
 
+// log1p-family functions (class-sorted in binary32)
+__host__ __device__ constexpr bool log1p_fn(int fn) {
+  return fn == FN_TLOG1P || fn == FN_TLOG1P0 || fn == FN_TLOG1PP || fn == FN_PLOG1P ||
+         fn == FN_PLOG1P0;
+}
+
+// All twenty functions (explog.py:101-325) on the admission-band cores.  The
+// dotted ones arrive with x1 = 0: texp0 / texpm10 / tlog0 are then bitwise the
+// twofold functions (t1 = expm1(0) = 0 adds +0 to a nonzero-or-+0 tail; renorm
+// of (y0, 0) is the identity), which tests/test_gpu_parity.py checks against
+// the exact path.
 template <class T, int FN, int VW>
 TF_DEV void fast_eval(const STab<T>& tb, void* xch, const T (&x0)[VW], const T (&x1)[VW],
                       T (&z0)[VW], T (&z1)[VW], bool (&ok)[VW]) {
-  if constexpr (FN == FN_TEXP) fast_texp<VW>(tb, x0, x1, z0, z1, ok);
-  else if constexpr (FN == FN_TEXPM1) fast_texpm1<VW>(tb, x0, x1, z0, z1, ok);
-  else if constexpr (FN == FN_PEXP || FN == FN_PEXPM1) {
-    // pexp / pexpm1 = renorm_fast(texpp / texpm1p) (explog.py:131-133, 165-166)
-    if constexpr (FN == FN_PEXP) fast_texp<VW>(tb, x0, x1, z0, z1, ok);
-    else fast_texpm1<VW>(tb, x0, x1, z0, z1, ok);
+  if constexpr (FN == FN_TEXP || FN == FN_TEXPP || FN == FN_TEXP0 || FN == FN_PEXP) {
+    fast_texp<VW>(tb, x0, x1, z0, z1, ok);
+  } else if constexpr (FN == FN_PEXP0) {
+    fast_texp<VW, true>(tb, x0, x1, z0, z1, ok);
+  } else if constexpr (FN == FN_TEXPM1 || FN == FN_TEXPM1P || FN == FN_TEXPM10 ||
+                       FN == FN_PEXPM1) {
+    fast_texpm1<VW>(tb, x0, x1, z0, z1, ok);
+  } else if constexpr (FN == FN_PEXPM10) {
+    fast_texpm1<VW, true>(tb, x0, x1, z0, z1, ok);
+  } else if constexpr (FN == FN_TLOG || FN == FN_TLOG0) {
+    fast_tlog<T, VW>(tb, x0, x1, z0, z1, ok);
+  } else if constexpr (FN == FN_TLOGP) {
+    fast_tlog<T, VW, false>(tb, x0, x1, z0, z1, ok);
+  } else if constexpr (FN == FN_PLOG0 || FN == FN_PLOG) {
+    fast_tlog<T, VW, false, true>(tb, x0, x1, z0, z1, ok);
+  } else {
+    constexpr bool RENORM = FN == FN_TLOG1P;
+    constexpr bool PM = FN == FN_PLOG1P0 || FN == FN_PLOG1P;
+    constexpr bool INNER = !(FN == FN_TLOG1P0 || FN == FN_PLOG1P0);
+    if constexpr (sizeof(T) == 4 && VW >= 2)
+      tlog1p_sorted<VW, RENORM, PM, INNER>(tb, static_cast<Xch<VW>*>(xch), x0, x1, z0, z1, ok);
+    else
+      fast_tlog1p<T, VW, RENORM, PM, INNER>(tb, x0, x1, z0, z1, ok);
+  }
+  if constexpr (FN == FN_PEXP || FN == FN_PEXPM1) {
+    // renorm_fast(texpp / texpm1p) (explog.py:131-133, 165-166)
 #pragma unroll
     for (int e = 0; e < VW; ++e) {
       TF<T> r = fast_two_sum_u(z0[e], z1[e]);
@@ -752,10 +846,6 @@ TF_DEV void fast_eval(const STab<T>& tb, void* xch, const T (&x0)[VW], const T (
       z1[e] = r.e;
     }
   }
-  else if constexpr (FN == FN_TLOG) fast_tlog<T, VW>(tb, x0, x1, z0, z1, ok);
-  else if constexpr (sizeof(T) == 4 && VW >= 2)
-    tlog1p_sorted<VW>(tb, static_cast<Xch<VW>*>(xch), x0, x1, z0, z1, ok);
-  else fast_tlog1p<T, VW>(tb, x0, x1, z0, z1, ok);
 }
 
 }  // namespace tf

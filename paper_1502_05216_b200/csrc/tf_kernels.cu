@@ -107,7 +107,7 @@ TF_DEV void drain(const uint32_t* q, int cnt, const T* __restrict__ x0, const T*
       z0[i] = Lim<T>::qnan();
       z1[i] = T(-12345);
     } else {
-      TF<T> r = eval_gen<T, FN>(x0[i], x1[i]);
+      TF<T> r = eval_gen<T, FN>(x0[i], dotted_fn(FN) ? T(0) : x1[i]);
       z0[i] = r.v;
       z1[i] = r.e;
     }
@@ -131,7 +131,8 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   __shared__ STab<T> tb;
   __shared__ uint32_t qs[WARPS][QCAP];
   __shared__ __align__(16) T stg[ASYNC ? STAGES : 1][2][BLOCK][VW];
-  constexpr bool XCH = FN == FN_TLOG1P && sizeof(T) == 4 && VW >= 2;
+  constexpr bool XCH = log1p_fn(FN) && sizeof(T) == 4 && VW >= 2;
+  constexpr bool DOT = dotted_fn(FN);  // plain argument: x1 is never read
   __shared__ Xch<VW> xch[XCH ? WARPS : 1];
   load_tables(tb);
   __syncthreads();
@@ -152,7 +153,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       cp_async16(&stg[0][0][threadIdx.x][c * EC], x0 + (v ? vi * VW + c * EC : 0u), v);
-      cp_async16(&stg[0][1][threadIdx.x][c * EC], x1 + (v ? vi * VW + c * EC : 0u), v);
+      if (!DOT) cp_async16(&stg[0][1][threadIdx.x][c * EC], x1 + (v ? vi * VW + c * EC : 0u), v);
     }
     cp_async_commit();
   }
@@ -168,20 +169,26 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         cp_async16(&stg[cs ^ 1][0][threadIdx.x][c * EC], x0 + (pvalid ? pv * VW + c * EC : 0u), pvalid);
-        cp_async16(&stg[cs ^ 1][1][threadIdx.x][c * EC], x1 + (pvalid ? pv * VW + c * EC : 0u), pvalid);
+        if (!DOT)
+          cp_async16(&stg[cs ^ 1][1][threadIdx.x][c * EC], x1 + (pvalid ? pv * VW + c * EC : 0u), pvalid);
       }
       cp_async_commit();
       cp_async_wait<1>();
 #pragma unroll
       for (int e = 0; e < VW; ++e) {
         a[e] = stg[cs][0][threadIdx.x][e];
-        b[e] = stg[cs][1][threadIdx.x][e];
+        b[e] = DOT ? T(0) : stg[cs][1][threadIdx.x][e];
       }
       cs ^= 1;
     } else {
       if (valid) {
         ld<T, VW>(x0, vi, a);
-        ld<T, VW>(x1, vi, b);
+        if (DOT) {
+#pragma unroll
+          for (int e = 0; e < VW; ++e) b[e] = T(0);
+        } else {
+          ld<T, VW>(x1, vi, b);
+        }
       } else {
 #pragma unroll
         for (int e = 0; e < VW; ++e) { a[e] = T(0); b[e] = T(0); }
@@ -245,24 +252,6 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
     if (lane + 96 < qn) q[lane + 64] = mv3;
     if (lane + 128 < qn) q[lane + 96] = mv4;
     qn -= c;
-  }
-}
-
-// ------------------------------------------------- sibling functions
-// The sixteen non-TWOFOLD_ARG functions (explog.py:101-325) run the exact path
-// element by element (grid-stride, scalar SoA access): correct for every input,
-// ~10x below the admission-band kernels.  texpp / texpm1p alias the fast texp /
-// texpm1 kernels and pexp / pexpm1 add a renorm_fast epilogue to them.
-template <class T, int FN>
-__global__ void __launch_bounds__(256) k_gen(const T* __restrict__ x0, const T* __restrict__ x1,
-                                             T* __restrict__ z0, T* __restrict__ z1, uint64_t n) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    T a = x0[i];
-    T b = dotted_fn(FN) ? T(0) : x1[i];
-    TF<T> r = eval_gen<T, FN>(a, b);
-    z0[i] = r.v;
-    z1[i] = r.e;
   }
 }
 
@@ -465,32 +454,12 @@ int launch_one(const T* x0, const T* x1, T* z0, T* z1, int64_t n, cudaStream_t s
 }
 
 template <class T, int FN>
-int launch_gen(const T* x0, const T* x1, T* z0, T* z1, int64_t n, cudaStream_t s) {
-  static int occ = 0;
-  if (!occ) {
-    int v = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, tf::k_gen<T, FN>, 256, 0);
-    occ = v > 0 ? v : 1;
-  }
-  int64_t grid = (int64_t)device_sms() * occ;
-  int64_t need = (n + 255) / 256;
-  if (need < grid) grid = need;
-  tf::k_gen<T, FN><<<(unsigned)grid, 256, 0, s>>>(x0, x1, z0, z1, (uint64_t)n);
-  return cuda_check("k_gen launch");
-}
-
-template <class T, int FN>
 int launch(const T* x0, const T* x1, T* z0, T* z1, int64_t n, void* stream, int flags) {
   if (n < 0) return fail(TF_ERR_ARG, "negative element count%s");
   if (n == 0) return TF_OK;
   if (tf::dotted_fn(FN) && !x1) x1 = x0;  // plain-argument functions never read x1
   if (!x0 || !x1 || !z0 || !z1) return fail(TF_ERR_ARG, "null pointer%s");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  constexpr bool FAST = FN == tf::FN_TEXP || FN == tf::FN_TEXPM1 || FN == tf::FN_TLOG ||
-                        FN == tf::FN_TLOG1P || FN == tf::FN_PEXP || FN == tf::FN_PEXPM1;
-  if constexpr (!FAST) {
-    return launch_gen<T, FN>(x0, x1, z0, z1, n, s);
-  }
   uintptr_t al = (uintptr_t)x0 | (uintptr_t)x1 | (uintptr_t)z0 | (uintptr_t)z1;
   if ((al & 15) == 0) {
     if constexpr (sizeof(T) == 8) return launch_one<T, FN, TF_VW64>(x0, x1, z0, z1, n, s, flags);
@@ -544,6 +513,7 @@ uint64_t mix64h(uint64_t z) {
 template <class T>
 int eval_dispatch(int fn, const T* a, const T* b, T* c, T* d, int64_t n, void* st, int fl) {
   switch (fn) {
+    // texpp / texpm1p are texp / texpm1 (explog.py:127-129, 162-163)
     case TF_FN_TEXP: case TF_FN_TEXPP: return launch<T, tf::FN_TEXP>(a, b, c, d, n, st, fl);
     case TF_FN_TEXPM1: case TF_FN_TEXPM1P: return launch<T, tf::FN_TEXPM1>(a, b, c, d, n, st, fl);
     case TF_FN_TLOG: return launch<T, tf::FN_TLOG>(a, b, c, d, n, st, fl);

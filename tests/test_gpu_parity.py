@@ -105,7 +105,7 @@ def test_golden_vectors(fn, width, golden, cuda):
 
 
 @pytest.mark.parametrize("width", WIDTHS)
-@pytest.mark.parametrize("fn", FNS + ("texpp", "pexp", "texpm1p", "pexpm1"))
+@pytest.mark.parametrize("fn", ALL_FNS)
 def test_fast_path_equals_exact_path(fn, width, golden, cuda):
     """Admission-band kernels and the exact path agree bit for bit."""
     from paper_1502_05216_b200 import _lib
@@ -237,3 +237,43 @@ def test_full_size_config(cfg, cuda):
     assert not bool(torch.isnan(z1[fin]).any())
     del x0, x1, z0, z1, z
     torch.cuda.empty_cache()
+
+
+SIB_DIST = {("exp", 64): "exp64s", ("expm1", 64): "pow10_64", ("log", 64): "logu64s",
+            ("log1p", 64): "pow10c_64", ("exp", 32): "exp32", ("expm1", 32): "exp32",
+            ("log", 32): "log32", ("log1p", 32): "log32"}
+
+
+@pytest.mark.parametrize("width", WIDTHS)
+@pytest.mark.parametrize("fn", SIBLINGS)
+def test_sibling_fast_equals_exact_on_config(fn, width, cuda):
+    """The sibling fast paths (admission-band cores + variant epilogues) against
+    the element-wise exact path, bitwise, on 2^20 config-distributed elements
+    (with specials for binary64), plus the CR-sim oracle on a subsample."""
+    import torch
+
+    from paper_1502_05216_b200 import _lib, api, family_of
+
+    L = _lib.ensure_device(cuda.index)
+    dist = SIB_DIST[(family_of(fn), width)]
+    dt = torch.float64 if width == 64 else torch.float32
+    n = (1 << 20) + 3                                        # ragged tail too
+    x0 = torch.empty(n, dtype=dt, device=cuda)
+    x1 = torch.empty(n, dtype=dt, device=cuda)
+    _lib.check(L.tf_generate(_lib.DIST_CODES[dist], 5, 0, n, x0.data_ptr(), x1.data_ptr(), None),
+               "gen")
+    if fn.endswith("0"):
+        x1 = x0
+    lib = api(width)
+    a = lib._device(fn, x0, x1)
+    b = lib._device(fn, x0, x1, flags=_lib.FLAG_FORCE_EXACT)
+    torch.cuda.synchronize()
+    r = compare(a.value.cpu().numpy(), a.error.cpu().numpy(), b.value.cpu().numpy(),
+                b.error.cpu().numpy(), width)
+    assert r["z0_mismatch"] == 0 and r["z1_bit_mismatch"] == 0, r
+    m = 1 << 14
+    h0 = x0[:m].cpu().numpy()
+    h1 = np.zeros_like(h0) if fn.endswith("0") else x1[:m].cpu().numpy()
+    s = compare(a.value[:m].cpu().numpy(), a.error[:m].cpu().numpy(),
+                *_crsim(fn, width, h0, h1, "fma"), width)
+    assert s["class_mismatch"] == 0 and s["tol_violations"] == 0, s

@@ -10,3 +10,10 @@ print("headline Gelem/s", round(d["value"] / 1e9, 2), {k: round(v, 4) for k, v i
 for k, v in d["per_function"].items():
     print(f'{k:12s} {v["elements_per_s"]/1e9:7.1f} Gelem/s  fp_frac {v["fp_pipe_frac"]:.3f}  hbm_frac {v["hbm_frac"]:.3f}')
 PY
+python - <<'PY'
+import json
+d = json.loads(open("gpurun_out/bench.log").read().strip().splitlines()[-1])
+for k, v in d.get("siblings", {}).items():
+    r = [x for x in v if x.startswith("vs_")][0]
+    print(f'{k:12s} {v["elements_per_s"]/1e9:7.1f} Gelem/s  {r} {v[r]:.3f}')
+PY
