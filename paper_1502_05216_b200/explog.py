@@ -14,10 +14,11 @@ and the current stream, results allocated there), CPU tensors or numpy arrays
 evaluation runs the hand-written sm_100a kernels of libtwofold_b200.so; there
 is no CPU fallback.
 
-All twenty reference functions are served.  The four twofold-argument ones
-(TWOFOLD_ARG) run the admission-band fast kernels; ``texpp``/``texpm1p`` are
-the same kernels and ``pexp``/``pexpm1`` add a renorm epilogue to them; the
-other twelve (explog.py:101-325) run the element-wise exact-path kernel.
+All twenty reference functions are served by the same admission-band kernels
+(tf_fast.cuh fast_eval): ``texpp``/``texpm1p`` are ``texp``/``texpm1``, the
+p-functions return renorm_fast of the cores, the dotted t-functions run their
+twofold twins with x1 = 0, and the coupled-argument log functions skip the
+renormalisation (explog.py:101-325).
 DOTTED_ARG functions take a plain argument (a scalar, array or tensor, not a
 pair).  COUPLED_ARG functions assume |x1| <= ulp(x0)/2 like the reference;
 where the reference raises OverflowError for a non-coupled argument
