@@ -132,6 +132,39 @@ TF_API int tf_fma_peak(int width, void* out_dev, int blocks, int iters, void* st
  * TF_FLAG_COUNT_EXACT on the counted calls); synchronous. */
 TF_API int tf_exact_count(unsigned long long* out, int reset);
 
+/* ---- accuracy audit (reference audit.py:207-286 run_accuracy; etalon
+ * oracle.py:37-167).  Families: 0 exp, 1 expm1, 2 log, 3 log1p
+ * (explog.py:44-49 FAMILIES). */
+#define TF_FAM_EXP 0
+#define TF_FAM_EXPM1 1
+#define TF_FAM_LOG 2
+#define TF_FAM_LOG1P 3
+#define TF_ETALON_ORACLE 0 /* triple-double high-precision etalon (~2^-140 relative) */
+#define TF_ETALON_LIB 1    /* binary64 library at x0 + x1 (binary32 audits only) */
+/* audit sample states: included, excluded (non-finite / below the error floor),
+ * etalon domain error, zero reference (absolute fallback) */
+#define TF_AUDIT_INCLUDED 0
+#define TF_AUDIT_FLOOR 1
+#define TF_AUDIT_DOMAIN 2
+#define TF_AUDIT_ABSOLUTE 3
+
+/* Per-sample relative error of the results (z0, z1) of a `family` function at
+ * the arguments (x0, x1), all device arrays of the lane type of `width`;
+ * err[] (double) and state[] (TF_AUDIT_*) are device outputs. */
+TF_API int tf_audit_errors(int family, int width, int etalon_kind, const void* x0, const void* x1,
+                           const void* z0, const void* z1, int64_t n, double* err,
+                           unsigned char* state, void* stream);
+
+/* The triple-double etalon itself at x0 + x1 (binary64 device arrays):
+ * value = (m[i] + m[n+i] + m[2n+i]) * 2^k[i]; NaN words outside the domain. */
+TF_API int tf_etalon(int family, const double* x0, const double* x1, int64_t n, double* m,
+                     int* k, void* stream);
+
+/* run_bench's checksum (audit.py:344-349): XOR over i of the binary64 bit
+ * pattern of (double) z0[i], written to *out (device). */
+TF_API int tf_checksum(int width, const void* z0, int64_t n, unsigned long long* out,
+                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,7 +31,10 @@ DIST_CODES = {"exp64": 0, "pow10_64": 1, "pow10c_64": 2, "log64": 3, "exp32": 4,
 EXPORTS = ("tf_version", "tf_last_error", "tf_init", "tf_texp_f64", "tf_texpm1_f64",
            "tf_tlog_f64", "tf_tlog1p_f64", "tf_texp_f32", "tf_texpm1_f32", "tf_tlog_f32",
            "tf_tlog1p_f32", "tf_eval", "tf_generate", "tf_compare", "tf_fma_peak",
-           "tf_exact_count")
+           "tf_exact_count", "tf_audit_errors", "tf_etalon", "tf_checksum")
+FAMILY_CODES = {"exp": 0, "expm1": 1, "log": 2, "log1p": 3}
+ETALON_CODES = {"oracle": 0, "lib": 1}
+AUDIT_INCLUDED, AUDIT_FLOOR, AUDIT_DOMAIN, AUDIT_ABSOLUTE = 0, 1, 2, 3
 
 _lib = None
 _lock = threading.Lock()
@@ -80,6 +83,12 @@ def load() -> ctypes.CDLL:
         L.tf_fma_peak.restype = i32
         L.tf_exact_count.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), i32]
         L.tf_exact_count.restype = i32
+        L.tf_audit_errors.argtypes = [i32, i32, i32, vp, vp, vp, vp, i64, vp, vp, vp]
+        L.tf_audit_errors.restype = i32
+        L.tf_etalon.argtypes = [i32, vp, vp, i64, vp, vp, vp]
+        L.tf_etalon.restype = i32
+        L.tf_checksum.argtypes = [i32, vp, i64, vp, vp]
+        L.tf_checksum.restype = i32
         _lib = L
         return L
 

@@ -17,7 +17,7 @@
 #include <mutex>
 
 #include "tf_fast.cuh"
-#include "../../include/twofold_b200.h"
+#include "tf_abi.h"
 
 namespace tf {
 
@@ -396,11 +396,11 @@ __global__ void __launch_bounds__(256) k_fma_peak(T* out, int iters, T a, T b) {
 }  // namespace tf
 
 // ===================================================================== ABI
-namespace {
+namespace tfabi {
 
 thread_local char g_err[512] = "";
 
-int fail(int code, const char* fmt, const char* detail = "") {
+int fail(int code, const char* fmt, const char* detail) {
   snprintf(g_err, sizeof g_err, fmt, detail);
   return code;
 }
@@ -432,6 +432,16 @@ int device_sms() {
   }
   return g_dev[d].sms;
 }
+
+}  // namespace tfabi
+
+namespace {
+using tfabi::cuda_check;
+using tfabi::device_sms;
+using tfabi::fail;
+using tfabi::g_const_ready;
+using tfabi::g_err;
+using tfabi::g_mu;
 
 template <class T, int FN, int VW>
 int launch_one(const T* x0, const T* x1, T* z0, T* z1, int64_t n, cudaStream_t s, int flags) {
