@@ -50,6 +50,11 @@ PER_FN = {
     ("texp", 32): "cfg4_texp_f32", ("texpm1", 32): "cfg4_texpm1_f32",
     ("tlog", 32): "cfg4_tlog_f32", ("tlog1p", 32): "cfg4_tlog1p_f32",
 }
+# input arrays each tf_eft op streams (a0 + a1/b0/b1 as the op needs them)
+EFT_ARRAYS_IN = {"fast_two_sum": 2, "two_sum": 2, "two_diff": 2, "two_prod": 2, "split": 1,
+                 "renorm_fast": 2, "renorm": 2, "t_add": 4, "t_add_d": 3, "t_mul": 4,
+                 "t_mul_d": 3, "t_div": 4, "t_sqrt": 2}
+EFT_BACKEND_OPS = ("two_prod", "t_mul", "t_mul_d", "t_div", "t_sqrt")
 N_HEAD = 1 << 24
 N_FN = {64: 1 << 24, 32: 1 << 26}
 SEED = 2024
@@ -314,6 +319,35 @@ def run_ours(args):
                         "vs_" + fn: ms / sms}
             del a0, a1, z0, z1
 
+    # ---- element-wise EFT / twofold arithmetic ops (HBM-bound streaming)
+    eft_rates = {}
+    if not args.headline_only and not args.no_eft:
+        m = 1 << 25
+        for width in (64, 32):
+            dt = torch.float64 if width == 64 else torch.float32
+            sz = 8 if width == 64 else 4
+            ops_in = [torch.empty(m, dtype=dt, device=dev).uniform_(1.0, 2.0) for _ in range(4)]
+            z0, z1 = torch.empty_like(ops_in[0]), torch.empty_like(ops_in[0])
+            ptrs = [a.data_ptr() for a in ops_in]
+            for op, code in _lib.OP_CODES.items():
+                for backend in ((0, 1) if op in EFT_BACKEND_OPS else (0,)):
+                    def go():
+                        _lib.check(L.tf_eft(code, width, backend, *ptrs, z0.data_ptr(),
+                                            z1.data_ptr(), m, sp), "tf_eft")
+                    for _ in range(3):
+                        go()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    for _ in range(10):
+                        go()
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ms = max_over_ranks(e0.elapsed_time(e1) / 10)
+                    gbs = (EFT_ARRAYS_IN[op] + 2) * sz * m / (ms * 1e-3) / 1e9
+                    name = f"{op}{'_dv' if backend else ''}_f{width}"
+                    eft_rates[name] = {"elements_per_s": m * world / (ms * 1e-3), "ms": ms,
+                                       "hbm_gbs": gbs, "hbm_frac": gbs / _peaks()["hbm_gbs"]}
+            del ops_in, z0, z1
     # ---- end to end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -388,6 +422,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "per_function": per_fn,
             "siblings": siblings,
+            "eft_ops": eft_rates,
             "parity_sample": stats,
         }
         print(json.dumps(line), flush=True)
@@ -458,6 +493,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-siblings", action="store_true")
+    ap.add_argument("--no-eft", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -165,6 +165,30 @@ TF_API int tf_etalon(int family, const double* x0, const double* x1, int64_t n, 
 TF_API int tf_checksum(int width, const void* z0, int64_t n, unsigned long long* out,
                        void* stream);
 
+/* ---- element-wise EFTs and twofold arithmetic over device arrays
+ * (reference eft.py:77-237 binary64, eft32.py:36-214 binary32), bit-exact
+ * including the _special non-finite policy.  Operands: a = (a0, a1),
+ * b = (b0, b1); scalar ops read a0 (and b0); results (z0, z1) = (value, error)
+ * or (hi, lo) for split.  backend: 0 = "fma" residual, 1 = "dv" (Dekker /
+ * Veltkamp, fma_sim remainders); it only matters for the ops marked [b]. */
+#define TF_OP_FAST_TWO_SUM 0 /* fast_two_sum(a0, b0)   eft.py:77-82   */
+#define TF_OP_TWO_SUM 1      /* two_sum(a0, b0)        eft.py:85-92   */
+#define TF_OP_TWO_DIFF 2     /* two_diff(a0, b0)       eft.py:95-104  */
+#define TF_OP_TWO_PROD 3     /* two_prod_*(a0, b0) [b] eft.py:131-149 */
+#define TF_OP_SPLIT 4        /* split(a0) -> (hi, lo)  eft.py:115-128 */
+#define TF_OP_RENORM_FAST 5  /* renorm_fast(a)         eft.py:163-165 */
+#define TF_OP_RENORM 6       /* renorm(a)              eft.py:168-171 */
+#define TF_OP_T_ADD 7        /* t_add(a, b)            eft.py:182-189 */
+#define TF_OP_T_ADD_D 8      /* t_add_d(a, b0)         eft.py:192-199 */
+#define TF_OP_T_MUL 9        /* t_mul(a, b) [b]        eft.py:207-212 */
+#define TF_OP_T_MUL_D 10     /* t_mul_d(a, b0) [b]     eft.py:214-219 */
+#define TF_OP_T_DIV 11       /* t_div(a, b) [b]        eft.py:221-226 */
+#define TF_OP_T_SQRT 12      /* t_sqrt(a) [b]          eft.py:228-235 */
+#define TF_OP_COUNT 13
+
+TF_API int tf_eft(int op, int width, int backend, const void* a0, const void* a1, const void* b0,
+                  const void* b1, void* z0, void* z1, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -155,6 +155,8 @@ def lib():
         L.tfo_decompose_exp32.argtypes = [ctypes.c_float, vp, vp]
         L.tfo_decompose_expm1_32.argtypes = [ctypes.c_float, vp, vp]
         L.tfo_eft64.argtypes = [i32, i32, vp, vp]
+        L.tfo_eft.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, ctypes.c_int64]
+        L.tfo_eft.restype = i32
         _lib = L
     return _lib
 
@@ -280,3 +282,22 @@ def eft64(op: str, *args: float, backend: str = "fma"):
     out = np.zeros(2, np.float64)
     lib().tfo_eft64(_EFT_OPS[op], 1 if backend == "dv" else 0, _ptr(a), _ptr(out))
     return float(out[0]), float(out[1])
+
+
+EFT_OPS = ("fast_two_sum", "two_sum", "two_diff", "two_prod", "split", "renorm_fast", "renorm",
+           "t_add", "t_add_d", "t_mul", "t_mul_d", "t_div", "t_sqrt")
+
+
+def eft_arrays(op: str, width: int, a0, a1=None, b0=None, b1=None, backend: str = "fma"):
+    """Element-wise EFT / twofold op over arrays (op codes = TF_OP_*), the C
+    restatement of eft.py:77-237 / eft32.py:36-214."""
+    dt = np.float64 if width == 64 else np.float32
+    a0 = np.ascontiguousarray(a0, dtype=dt)
+    arrs = [a0] + [None if v is None else np.ascontiguousarray(v, dtype=dt) for v in (a1, b0, b1)]
+    z0 = np.empty_like(a0)
+    z1 = np.empty_like(a0)
+    rc = lib().tfo_eft(EFT_OPS.index(op), width, 1 if backend == "dv" else 0,
+                       *[None if v is None else _ptr(v) for v in arrs], _ptr(z0), _ptr(z1), a0.size)
+    if rc:
+        raise ValueError(f"tfo_eft({op}) failed")
+    return z0, z1

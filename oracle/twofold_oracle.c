@@ -163,6 +163,52 @@ static tf64 t_mul_d64(int dv, tf64 x, double b) {
     return mk64(v, x.e * b + e);
 }
 
+/* two_diff (eft.py:95-104): the corrected six-step sequence */
+static tf64 two_diff64(double a, double b) {
+    double d = a - b;
+    if (!isfinite(d)) return special64(d, N2(a, b));
+    double bp = d - a;
+    double ap = d - bp;
+    double bs = b + bp;
+    double as = a - ap;
+    return mk64(d, as - bs);
+}
+
+/* two_prod_fma / two_prod_dv (eft.py:131-149) */
+static tf64 two_prod64(int dv, double x, double y) {
+    double v = x * y;
+    if (!isfinite(v)) return special64(v, N2(x, y));
+    return mk64(v, prod_err64(dv, x, y, v));
+}
+
+/* fma_sim (eft.py:152-160) without the debug precondition assert */
+static double fma_sim64(double x, double y, double z) {
+    tf64 p = two_prod64(1, x, y);
+    return (z + p.v) + p.e;
+}
+
+/* _rem_fma / _rem_dv (eft.py:267-272): a - q*b */
+static double rem64(int dv, double q, double b, double a) {
+    return dv ? fma_sim64(-q, b, a) : fma(-q, b, a);
+}
+
+/* t_div (eft.py:221-226); IEEE division == div64 (_fp.py:136-143) */
+static tf64 t_div64(int dv, tf64 x, tf64 y) {
+    double q = x.v / y.v;
+    if (!isfinite(q)) return special64(q, N4(x.v, x.e, y.v, y.e));
+    double r = rem64(dv, q, y.v, x.v);
+    return mk64(q, (r + (x.e - q * y.e)) / y.v);
+}
+
+/* t_sqrt (eft.py:228-235); sqrt of a negative is NaN like sqrt64 (_fp.py:156-160) */
+static tf64 t_sqrt64(int dv, tf64 x) {
+    double q = sqrt(x.v);
+    if (!isfinite(q)) return special64(q, N2(x.v, x.e));
+    if (x.v == 0.0) return mk64(q, 0.0);
+    double r = rem64(dv, q, q, x.v);
+    return mk64(q, (r + x.e) / (q + q));
+}
+
 /* params.py:62-79 */
 #define LO64 (-0x1.74385446d71c4p+9)
 #define HI64 (0x1.62e42fefa39f0p+9)
@@ -578,6 +624,51 @@ static tf32 t_mul_d32(int dv, tf32 x, float b) {
     if (!isfinite(v)) return special32(v, N3(x.v, x.e, b));
     float e = prod_err32(dv, x.v, b, v);
     return mk32(v, (x.e * b) + e);
+}
+
+/* two_diff (eft32.py:52-60) */
+static tf32 two_diff32(float a, float b) {
+    float d = a - b;
+    if (!isfinite(d)) return special32(d, N2(a, b));
+    float bp = d - a;
+    float ap = d - bp;
+    float bs = b + bp;
+    float as = a - ap;
+    return mk32(d, as - bs);
+}
+
+/* eft32.py:85-101 (two_prod_fma / two_prod_dv) */
+static tf32 two_prod32(int dv, float x, float y) {
+    float v = x * y;
+    if (!isfinite(v)) return special32(v, N2(x, y));
+    return mk32(v, prod_err32(dv, x, y, v));
+}
+
+/* fma_sim (eft32.py:104-110) */
+static float fma_sim32(float x, float y, float z) {
+    tf32 p = two_prod32(1, x, y);
+    return (z + p.v) + p.e;
+}
+
+static float rem32(int dv, float q, float b, float a) {
+    return dv ? fma_sim32(-q, b, a) : fmaf(-q, b, a);
+}
+
+/* eft32.py:161-166; div32 / sqrt32 (_fp.py:146-167) are correctly rounded */
+static tf32 t_div32(int dv, tf32 x, tf32 y) {
+    float q = x.v / y.v;
+    if (!isfinite(q)) return special32(q, N4(x.v, x.e, y.v, y.e));
+    float r = rem32(dv, q, y.v, x.v);
+    return mk32(q, (r + (x.e - q * y.e)) / y.v);
+}
+
+/* eft32.py:168-175 */
+static tf32 t_sqrt32(int dv, tf32 x) {
+    float q = sqrtf(x.v);
+    if (!isfinite(q)) return special32(q, N2(x.v, x.e));
+    if (x.v == 0.0f) return mk32(q, 0.0f);
+    float r = rem32(dv, q, q, x.v);
+    return mk32(q, (r + x.e) / (q + q));
 }
 
 /* params.py:81-98 */
@@ -1045,4 +1136,45 @@ EXPORT void tfo_eft64(int op, int dv, const double* a, double* out) {
     }
     out[0] = r.v;
     out[1] = r.e;
+}
+
+/* Element-wise EFT / twofold arithmetic over arrays:
+ * op codes = TF_OP_* of include/twofold_b200.h; operands a = (a0, a1),
+ * b = (b0, b1) as the op needs them. */
+#define EFT_BODY(W, T, MK)                                                          \
+    for (int64_t i = 0; i < n; ++i) {                                               \
+        T x0 = A0[i], x1 = A1 ? A1[i] : 0, y0 = B0 ? B0[i] : 0, y1 = B1 ? B1[i] : 0; \
+        tf##W r;                                                                    \
+        switch (op) {                                                               \
+            case 0: r = fast_two_sum##W(x0, y0); break;                             \
+            case 1: r = two_sum##W(x0, y0); break;                                  \
+            case 2: r = two_diff##W(x0, y0); break;                                 \
+            case 3: r = two_prod##W(dv, x0, y0); break;                             \
+            case 4: split##W(x0, &r.v, &r.e); break;                                \
+            case 5: r = fast_two_sum##W(x0, x1); break;                             \
+            case 6: r = renorm##W(MK(x0, x1)); break;                               \
+            case 7: r = t_add##W(MK(x0, x1), MK(y0, y1)); break;                    \
+            case 8: r = t_add_d##W(MK(x0, x1), y0); break;                          \
+            case 9: r = t_mul##W(dv, MK(x0, x1), MK(y0, y1)); break;                \
+            case 10: r = t_mul_d##W(dv, MK(x0, x1), y0); break;                     \
+            case 11: r = t_div##W(dv, MK(x0, x1), MK(y0, y1)); break;               \
+            default: r = t_sqrt##W(dv, MK(x0, x1)); break;                          \
+        }                                                                           \
+        Z0[i] = r.v;                                                                \
+        Z1[i] = r.e;                                                                \
+    }
+
+EXPORT int tfo_eft(int op, int width, int dv, const void* a0, const void* a1, const void* b0,
+                   const void* b1, void* z0, void* z1, int64_t n) {
+    if (op < 0 || op > 12) return -1;
+    if (width == 64) {
+        const double *A0 = a0, *A1 = a1, *B0 = b0, *B1 = b1;
+        double *Z0 = z0, *Z1 = z1;
+        EFT_BODY(64, double, mk64)
+    } else {
+        const float *A0 = a0, *A1 = a1, *B0 = b0, *B1 = b1;
+        float *Z0 = z0, *Z1 = z1;
+        EFT_BODY(32, float, mk32)
+    }
+    return 0;
 }
