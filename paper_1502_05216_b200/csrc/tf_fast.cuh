@@ -458,6 +458,41 @@ TF_DEV void fast_texpm1(const STab<double>& tb, const double (&x0)[VW], const do
   }
 }
 
+// binary64 fallback branch (|x0| >= ln2, expcore.py:147): pexp0_raw(x0) - 1.
+// Not the main path at the BASELINE configs (cfg 2: 0.5% of elements); the
+// rare-element drain runs it before resorting to the exact path.
+template <int VW, bool PM = false>
+TF_DEV void fast_texpm1_fb(const STab<double>& tb, const double (&x0)[VW],
+                           const double (&x1)[VW], double (&z0)[VW], double (&z1)[VW],
+                           bool (&ok)[VW]) {
+  double y[VW];
+  int m[VW], n[VW];
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    ok[e] = abits(x0[e]) > B64_LN2 &&                          // out of band (expcore.py:142)
+            ahi(x0[e]) <= (sgn(x0[e]) ? H64_TEXP_NEG : H64_TEXP_POS) &&
+            ahi(x1[e]) < H64_X1_TINY;
+    decomp_exp_u(ok[e] ? x0[e] : 1.0, m[e], n[e], y[e]);
+  }
+  TF<double> t[VW];
+  taylor_exp_v<VW>(y, t);
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    TF<double> v = t_mul_u(tv<double>(tb.E[m[e] - P<double>::E_LO]),
+                           t_mul_u(tv<double>(tb.C[n[e] - P<double>::C_LO]), t[e]));
+    TF<double> w = t_add_d_u(v, -1.0);                          // expcore.py:147
+    if constexpr (PM) {
+      TF<double> r = fast_two_sum_u(w.v, w.e);
+      z0[e] = r.v;
+      z1[e] = r.e;
+      continue;
+    }
+    z0[e] = add(w.v, w.e);                                      // CR expm1(x0)
+    double tail = add(w.e, sub(w.v, z0[e]));
+    z1[e] = add(mul(add(z0[e], 1.0), t1_tiny(x1[e])), tail);
+  }
+}
+
 // binary32: the pexp0 - 1 fallback is the bulk (cfg 4: 99.2%)
 template <int VW, bool PM = false>
 TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const float (&x1)[VW],
@@ -503,13 +538,16 @@ template <> struct LogC<double> {
   static constexpr uint32_t DMAX = (1023u - 40u) << 20;  // |d| < 2^-40 (tlog value part)
   static constexpr int SMALL = 50, EBIAS = 1022;
   static constexpr uint64_t HALF = B64_HALF, TWO = B64_TWO;
-  static constexpr uint32_t LN2H = H64_LN2, NEAR1H = H64_NEAR1;
+  static constexpr uint32_t NEAR1H = H64_NEAR1;
   TF_DEV static uint32_t eb(double x) { return (uint32_t)hi32(x) >> 20; }
   TF_DEV static int n_of(double v) { return (int)(ubits(v) >> 52) - 1022; }
   TF_DEV static double mant(double v) {
     return __longlong_as_double((ubits(v) & 0x800fffffffffffffull) | (1022ull << 52));
   }
   TF_DEV static double p2(int k) { return p2d_bf(k); }
+  // |r| <= LN2 (the table value): pexpm10_raw's in-band test (expcore.py:142),
+  // exact; a seed of exactly -LN2 (argument a power of two) stays in band
+  TF_DEV static bool in_ln2(double r) { return abits(r) <= B64_LN2; }
   // 2^k for k in [-1022, 1023] (normal), two integer ops
   TF_DEV static double p2n(int k) { return __hiloint2double((k + 1023) << 20, 0); }
   TF_DEV static double rcp(double x) { return rcp_nr(x); }
@@ -519,13 +557,14 @@ template <> struct LogC<float> {
   static constexpr uint32_t DMAX = (127u - 21u) << 23;   // |d| < 2^-21
   static constexpr int SMALL = 21, EBIAS = 126;
   static constexpr uint32_t HALF = B32_HALF, TWO = B32_TWO;
-  static constexpr uint32_t LN2H = B32_LN2 + 1u, NEAR1H = NEAR1_32 + 1u;
+  static constexpr uint32_t NEAR1H = NEAR1_32 + 1u;
   TF_DEV static uint32_t eb(float x) { return ubits(x) >> 23; }
   TF_DEV static int n_of(float v) { return (int)(ubits(v) >> 23) - 126; }
   TF_DEV static float mant(float v) {
     return __int_as_float((ubits(v) & 0x807fffffu) | (126u << 23));
   }
   TF_DEV static float p2(int k) { return p2f_bf(k); }
+  TF_DEV static bool in_ln2(float r) { return abits(r) <= B32_LN2; }
   TF_DEV static float p2n(int k) { return p2f_bf(k); }
   TF_DEV static float rcp(float x) { return rcp_approx(x); }
 };
@@ -558,7 +597,7 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     zc1[e] = band ? v[e].e : (zbits(v[e].e) ? T(0) : mul(v[e].e, C::p2n(-n[e])));
     r0[e] = seed_log1p_t(add(sub(zc0[e], T(1)), zc1[e]),      // explog.py:196-199
                          [&](int i) { return tb.SEED[i]; });
-    ok[e] = ok[e] && ahi(r0[e]) < C::LN2H;
+    ok[e] = ok[e] && C::in_ln2(r0[e]);
     // keeps the CM1 index in range for rejected lanes (tlogp / plog take y1
     // unrenormalised, so the seed of a non-coupled input can be anything)
     mr0[e] = ok[e] ? -r0[e] : T(0);
@@ -612,11 +651,14 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
 // _plog1p0_raw's out-of-band branch, the raw _log_core of renorm(1 + y0)
 // without tlogp's inner _correct (tlog1p0, plog1p0); PM = true returns
 // renorm_fast of the raw result (plog1p0, plog1p).
-template <class T, int VW, bool RENORM = true, bool PM = false, bool INNER = true>
+template <class T, int VW, bool RENORM = true, bool PM = false, bool INNER = true, int UNI = -1>
 TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW], T (&z0)[VW],
                         T (&z1)[VW], bool (&ok)[VW]) {
   constexpr bool D = sizeof(T) == 8;
-  constexpr bool UNIFIED = !D;
+  constexpr bool UNIFIED = UNI < 0 ? !D : UNI > 0;
+  // out-of-band value part: log1p(d) = d - d^2/2 to the lane's precision needs
+  // |d| = |y1 / (1 + y0)| <= 2^-13 (binary32) / 2^-36 (binary64)
+  constexpr int DSEP = D ? 37 : 14;
   using C = LogC<T>;
   T y0[VW], y1[VW], sd[VW], ms[VW], zc0[VW], zc1[VW];
   int n[VW];
@@ -629,7 +671,12 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
     y0[e] = ok[e] ? y0i[e] : T(0);
     y1[e] = ok[e] ? y1i[e] : T(0);
     v[e] = RENORM ? renorm_u(mk(y0[e], y1[e])) : mk(y0[e], y1[e]);
-    if (D) inb[e] = ahi(v[e].v) < (sgn(v[e].v) ? H64_HALF : H64_ONE);
+    // in band: -1/2 <= v0 <= 1 (explog.py:291).  The unified branch needs the
+    // exact test (v0 = 1 or -1/2 must not go out of band); without it, the
+    // binary64 high-word test keeps a margin inside the band (|log1p(v0)| then
+    // stays below LN2 whatever the seed's last bit) and sends the rest away.
+    if (D && !UNIFIED) inb[e] = ahi(v[e].v) < (sgn(v[e].v) ? H64_HALF : H64_ONE);
+    else if (D) inb[e] = abits(v[e].v) <= (sgn(v[e].v) ? B64_HALF : B64_ONE);
     else inb[e] = ahi(v[e].v) <= (sgn(v[e].v) ? B32_HALF : B32_ONE);
     T arg = v[e].v;
     n[e] = 0;
@@ -637,10 +684,10 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
     zc1[e] = T(0);
     if (UNIFIED && !inb[e]) {
       // out-of-band prologue; v0 > -1 keeps w0 = 1 + v0 positive and normal
-      ok[e] = ok[e] && (inb[e] || !sgn(v[e].v) || ahi(v[e].v) < B32_ONE);
+      ok[e] = ok[e] && (inb[e] || !sgn(v[e].v) || ahi(v[e].v) < (D ? H64_ONE : B32_ONE));
       TF<T> w = renorm_u(t_add_d_u(v[e], T(1)));
       // |d| = |y1 / (1 + y0)| <= ~2^-13 so log1p(d) = d - d^2/2 suffices below
-      ok[e] = ok[e] && (inb[e] || zbits(y1[e]) || bexp(y1[e]) + 14 <= bexp(w.v));
+      ok[e] = ok[e] && (inb[e] || zbits(y1[e]) || bexp(y1[e]) + DSEP <= bexp(w.v));
       auto wb = ubits(w.v);
       bool band = wb >= C::HALF && wb <= C::TWO;
       int nn = band ? 0 : C::n_of(w.v);
@@ -657,7 +704,10 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
     }
     if (!ok[e]) { arg = T(0); inb[e] = true; }
     sd[e] = seed_log1p_t(arg, [&](int i) { return tb.SEED[i]; });  // explog.py:197-199, 277
-    ok[e] = ok[e] && (inb[e] || ahi(sd[e]) < C::LN2H);
+    // pexpm10_raw(-sd) must take its in-band branch (|sd| <= LN2); in band this
+    // can fail only at v0 = -1/2 or 1 with a seed one ulp beyond ln 2
+    if (D && !UNIFIED) ok[e] = ok[e] && (inb[e] || C::in_ln2(sd[e]));
+    else ok[e] = ok[e] && C::in_ln2(sd[e]);
     ms[e] = -sd[e];
   }
   TF<T> s[VW];
@@ -797,6 +847,41 @@ TF_DEV void tlog1p_sorted(const STab<float>& tb, Xch<VW>* xw, const float (&x0)[
     ok[e] = xw->okb[e * 32 + lane] != 0;
   }
   __syncwarp();
+}
+
+// Second-chance evaluator of the rare-element drain (binary64): the branch the
+// main fast path leaves out -- texpm1's pexp0 - 1 fallback, tlog1p's
+// out-of-band tlogp(renorm(1 + y)) -- run lane-scalar on the queued elements;
+// elements it does not admit go on to the exact path.  Exact-path cost per
+// element is ~10x this, and these branches are most of cfg 2's rare elements.
+template <class T, int FN> struct HasAlt {
+  static constexpr bool value =
+      sizeof(T) == 8 && (FN == FN_TEXPM1 || FN == FN_TEXPM10 || FN == FN_PEXPM10 ||
+                         FN == FN_PEXPM1 || FN == FN_TLOG1P || FN == FN_TLOG1P0 ||
+                         FN == FN_TLOG1PP || FN == FN_PLOG1P || FN == FN_PLOG1P0);
+};
+template <class T, int FN>
+TF_DEV bool fast_alt(const STab<T>& tb, T x0, T x1, T& z0, T& z1) {
+  T a[1] = {x0}, b[1] = {x1}, r0[1], r1[1];
+  bool ok[1];
+  if constexpr (FN == FN_TEXPM1 || FN == FN_TEXPM10 || FN == FN_PEXPM1) {
+    fast_texpm1_fb<1>(tb, a, b, r0, r1, ok);
+    if constexpr (FN == FN_PEXPM1) {
+      TF<T> r = fast_two_sum_u(r0[0], r1[0]);
+      r0[0] = r.v;
+      r1[0] = r.e;
+    }
+  } else if constexpr (FN == FN_PEXPM10) {
+    fast_texpm1_fb<1, true>(tb, a, b, r0, r1, ok);
+  } else {
+    constexpr bool RENORM = FN == FN_TLOG1P;
+    constexpr bool PM = FN == FN_PLOG1P0 || FN == FN_PLOG1P;
+    constexpr bool INNER = !(FN == FN_TLOG1P0 || FN == FN_PLOG1P0);
+    fast_tlog1p<T, 1, RENORM, PM, INNER, 1>(tb, a, b, r0, r1, ok);
+  }
+  z0 = r0[0];
+  z1 = r1[0];
+  return ok[0];
 }
 
 // log1p-family functions (class-sorted in binary32)

@@ -21,23 +21,29 @@
 
 namespace tf {
 
-#ifndef TF_MINB
-#define TF_MINB 4
-#endif
-#ifndef TF_MINB4
-#define TF_MINB4 2
-#endif
 #ifndef TF_VW64
 #define TF_VW64 2
 #endif
 #ifndef TF_VW32
 #define TF_VW32 4
 #endif
-#ifndef TF_MINB32W
-#define TF_MINB32W 2
-#endif
 
 __device__ unsigned long long g_rare_count = 0;
+
+
+#ifndef TF_TIMELINE
+#define TF_TIMELINE 0
+#endif
+#if TF_TIMELINE
+constexpr unsigned TL_MAX = 1u << 16;
+__device__ unsigned long long g_tl[4 * TL_MAX];
+__device__ unsigned g_tl_smid[TL_MAX];
+TF_DEV unsigned tl_smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+#endif
 
 template <class T, int VW> struct Vec;
 template <> struct Vec<double, 2> { typedef double2 t; };
@@ -74,11 +80,36 @@ TF_DEV void st(T* p, uint64_t vi, const T (&a)[VW]) {
 }
 
 // lanes per thread and occupancy per (width, vector width)
+// One CTA of TF_BLOCK threads per SM (TF_BLOCK / 32 warps) by default.  With
+// several smaller CTAs per SM the warp schedulers favour the older CTAs, which
+// then finish far ahead of the younger ones: a persistent grid-stride loop ends
+// in a staircase of shrinking occupancy (tools/timeline_probe.py measured
+// 4 CTAs/SM finishing at 40/60/80/100% of the span).  Warps of one CTA advance
+// together, so a single CTA per SM keeps every warp busy to the end.
+#ifndef TF_BLOCK
+#define TF_BLOCK 1024
+#endif
 template <class T, int VW> struct KCfg {
   static constexpr bool WIDE = sizeof(T) == 8 && VW == 4;   // 4 binary64 lanes per thread
   static constexpr bool WIDE32 = sizeof(T) == 4 && VW == 8;  // 8 binary32 lanes per thread
-  static constexpr int BLOCK = (WIDE || WIDE32) ? 128 : 256; // static smem stays < 48 KB
-  static constexpr int MINB = WIDE ? TF_MINB4 : (WIDE32 ? TF_MINB32W : TF_MINB);
+  static constexpr int BLOCK = (WIDE || WIDE32) ? TF_BLOCK / 2 : TF_BLOCK;
+  static constexpr int MINB = (WIDE || WIDE32) ? 1 : 1024 / TF_BLOCK;
+};
+
+// shared-memory layout of one k_eval CTA (dynamic: > 48 KB)
+template <class T, int VW, int BLOCK, bool ASYNC, bool XCH> struct EvalSmem {
+  static constexpr int WARPS = BLOCK / 32;
+  static constexpr int QCAP = 32 + 32 * VW;
+  STab<T> tb;
+  uint32_t qs[WARPS][QCAP];
+  __align__(16) T stg[ASYNC ? 2 : 1][2][BLOCK][VW];
+  Xch<VW> xch[XCH ? WARPS : 1];
+};
+template <class T, int FN, int VW> struct EvalCfg {
+  static constexpr int BLOCK = KCfg<T, VW>::BLOCK;
+  static constexpr bool ASYNC = VW * sizeof(T) % 16 == 0;
+  static constexpr bool XCH = log1p_fn(FN) && sizeof(T) == 4 && VW >= 2;
+  typedef EvalSmem<T, VW, BLOCK, ASYNC, XCH> Smem;
 };
 
 // ---- asynchronous global -> shared staging (LDGSTS), one 16 B vector per
@@ -99,20 +130,34 @@ template <int N> TF_DEV void cp_async_wait() {
 
 // Evaluate the queued rare elements q[0..cnt) (cnt <= 32) with the exact path.
 template <class T, int FN>
-TF_DEV void drain(const uint32_t* q, int cnt, const T* __restrict__ x0, const T* __restrict__ x1,
-                  T* __restrict__ z0, T* __restrict__ z1, int lane, bool count, bool mark) {
+TF_DEV void drain(const STab<T>& tb, const uint32_t* q, int cnt, const T* __restrict__ x0,
+                  const T* __restrict__ x1, T* __restrict__ z0, T* __restrict__ z1, int lane,
+                  bool count, bool mark, bool force) {
+  bool exact = false;
   if (lane < cnt) {
     uint32_t i = q[lane];
+    T a = x0[i], b = dotted_fn(FN) ? T(0) : x1[i];
     if (mark) {  // diagnostics: tag exact-path elements instead of evaluating them
       z0[i] = Lim<T>::qnan();
       z1[i] = T(-12345);
     } else {
-      TF<T> r = eval_gen<T, FN>(x0[i], dotted_fn(FN) ? T(0) : x1[i]);
-      z0[i] = r.v;
-      z1[i] = r.e;
+      T r0, r1;
+      bool done = false;
+      if constexpr (HasAlt<T, FN>::value) done = !force && fast_alt<T, FN>(tb, a, b, r0, r1);
+      if (!done) {
+        TF<T> r = eval_gen<T, FN>(a, b);
+        r0 = r.v;
+        r1 = r.e;
+        exact = true;
+      }
+      z0[i] = r0;
+      z1[i] = r1;
     }
   }
-  if (count && lane == 0) atomicAdd(&g_rare_count, (unsigned long long)cnt);
+  if (count) {
+    unsigned m = __ballot_sync(0xffffffffu, exact || (mark && lane < cnt));
+    if (lane == 0) atomicAdd(&g_rare_count, (unsigned long long)__popc(m));
+  }
 }
 
 template <class T, int FN, int VW>
@@ -128,17 +173,30 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   constexpr bool ASYNC = VW * sizeof(T) % 16 == 0;
   constexpr int NC = VW * (int)sizeof(T) / 16;        // 16-byte chunks per thread
   constexpr int EC = 16 / (int)sizeof(T);             // elements per chunk
-  __shared__ STab<T> tb;
-  __shared__ uint32_t qs[WARPS][QCAP];
-  __shared__ __align__(16) T stg[ASYNC ? STAGES : 1][2][BLOCK][VW];
-  constexpr bool XCH = log1p_fn(FN) && sizeof(T) == 4 && VW >= 2;
+  typedef typename EvalCfg<T, FN, VW>::Smem Smem;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  STab<T>& tb = S.tb;
+  auto& qs = S.qs;
+  auto& stg = S.stg;
+  auto& xch = S.xch;
+  constexpr bool XCH = EvalCfg<T, FN, VW>::XCH;
   constexpr bool DOT = dotted_fn(FN);  // plain argument: x1 is never read
-  __shared__ Xch<VW> xch[XCH ? WARPS : 1];
+  static_assert(STAGES == 2 || !ASYNC, "two-stage staging");
+#if TF_TIMELINE
+  unsigned long long tl0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl0));
+#endif
   load_tables(tb);
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* q = qs[warp];
+#if TF_TIMELINE
+  unsigned long long tl1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl1));
+  unsigned tl_drains = 0, tl_iters = 0;
+#endif
   const bool force = flags & TF_FLAG_FORCE_EXACT;
   const bool count = flags & TF_FLAG_COUNT_EXACT;
   const bool mark = flags & TF_FLAG_MARK_EXACT;
@@ -147,8 +205,13 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   const uint32_t nvec = n / VW;
   const uint32_t stride = gridDim.x * BLOCK;
   const uint32_t first = blockIdx.x * BLOCK + warp * 32;
+  // warp-iteration bases (vector index of lane 0): current and next.  (A
+  // dynamic claim scheme -- per-warp atomic counters over 16 interleaved
+  // partitions -- evened out the finish times but cost more than it saved:
+  // 93.7 vs 95.7 G elem/s on the headline step.)
+  uint32_t base = first, nbase = first + stride;
   if constexpr (ASYNC) {
-    uint32_t vi = first + lane;
+    uint32_t vi = base + lane;
     bool v = vi < nvec;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -158,13 +221,13 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
     cp_async_commit();
   }
   int cs = 0;
-  for (uint32_t base = first; base < nvec; base += stride) {
+  while (base < nvec) {
     const uint32_t vi = base + lane;
     const bool valid = vi < nvec;
     T a[VW], b[VW], r0[VW], r1[VW];
     bool rare[VW];
     if constexpr (ASYNC) {
-      uint32_t pv = vi + stride;
+      uint32_t pv = nbase + lane;
       bool pvalid = pv < nvec;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
@@ -215,7 +278,10 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
     }
     while (qn >= 32) {
       __syncwarp();
-      drain<T, FN>(q, 32, x0, x1, z0, z1, lane, count, mark);
+#if TF_TIMELINE
+      ++tl_drains;
+#endif
+      drain<T, FN>(tb, q, 32, x0, x1, z0, z1, lane, count, mark, force);
       __syncwarp();
       uint32_t mv = (lane + 32 < qn) ? q[lane + 32] : 0u;
       uint32_t mv2 = (lane + 64 < qn) ? q[lane + 64] : 0u;
@@ -229,8 +295,14 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
       qn -= 32;
       __syncwarp();
     }
+    base = nbase;
+    nbase += stride;
   }
   if constexpr (ASYNC) cp_async_wait<0>();
+#if TF_TIMELINE
+  unsigned long long tl2;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl2));
+#endif
   // ragged tail (n % VW elements): exact path, first warp of block 0
   const uint32_t tail = n - nvec * VW;
   if (blockIdx.x == 0 && warp == 0 && tail) {
@@ -240,7 +312,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   while (qn > 0) {
     __syncwarp();
     int c = qn < 32 ? qn : 32;
-    drain<T, FN>(q, c, x0, x1, z0, z1, lane, count, mark);
+    drain<T, FN>(tb, q, c, x0, x1, z0, z1, lane, count, mark, force);
     __syncwarp();
     uint32_t mv = (lane + 32 < qn) ? q[lane + 32] : 0u;
     uint32_t mv2 = (lane + 64 < qn) ? q[lane + 64] : 0u;
@@ -253,6 +325,19 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
     if (lane + 128 < qn) q[lane + 96] = mv4;
     qn -= c;
   }
+#if TF_TIMELINE
+  // diagnostics build only: per-warp start / tables-staged / loop-end / end times
+  unsigned long long tl3;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl3));
+  unsigned gw = blockIdx.x * WARPS + warp;
+  if (lane == 0 && gw < TL_MAX) {
+    g_tl[4 * gw] = tl0;
+    g_tl[4 * gw + 1] = tl1;
+    g_tl[4 * gw + 2] = tl2;
+    g_tl[4 * gw + 3] = tl3;
+    g_tl_smid[gw] = tl_smid() | (tl_drains << 16);
+  }
+#endif
 }
 
 // ------------------------------------------------------------ generator
@@ -446,9 +531,13 @@ using tfabi::g_mu;
 template <class T, int FN, int VW>
 int launch_one(const T* x0, const T* x1, T* z0, T* z1, int64_t n, cudaStream_t s, int flags) {
   static int occ = 0;
+  constexpr size_t SMEM = sizeof(typename tf::EvalCfg<T, FN, VW>::Smem);
   if (!occ) {
+    cudaFuncSetAttribute(tf::k_eval<T, FN, VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SMEM);
     int v = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, tf::k_eval<T, FN, VW>, tf::KCfg<T, VW>::BLOCK, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, tf::k_eval<T, FN, VW>,
+                                                  tf::KCfg<T, VW>::BLOCK, SMEM);
     occ = v > 0 ? v : 1;
   }
   const int64_t CHUNK = (int64_t)1 << 31;  // queue indices are 32-bit
@@ -457,8 +546,8 @@ int launch_one(const T* x0, const T* x1, T* z0, T* z1, int64_t n, cudaStream_t s
     int64_t vecs = (m / VW + tf::KCfg<T, VW>::BLOCK - 1) / tf::KCfg<T, VW>::BLOCK;
     int64_t grid = (int64_t)device_sms() * occ;
     if (vecs < grid) grid = vecs > 0 ? vecs : 1;
-    tf::k_eval<T, FN, VW><<<(unsigned)grid, tf::KCfg<T, VW>::BLOCK, 0, s>>>(x0 + off, x1 + off, z0 + off,
-                                                              z1 + off, (uint32_t)m, flags);
+    tf::k_eval<T, FN, VW><<<(unsigned)grid, tf::KCfg<T, VW>::BLOCK, SMEM, s>>>(
+        x0 + off, x1 + off, z0 + off, z1 + off, (uint32_t)m, flags);
   }
   return cuda_check("k_eval launch");
 }
@@ -643,6 +732,16 @@ TF_API int tf_fma_peak(int width, void* out_dev, int blocks, int iters, void* st
   }
   return cuda_check("k_fma_peak launch");
 }
+
+#if TF_TIMELINE
+TF_API int tf_timeline(unsigned long long* host_t, unsigned* host_sm, int n) {
+  if (cudaMemcpyFromSymbol(host_t, tf::g_tl, sizeof(unsigned long long) * 4 * n) != cudaSuccess)
+    return cuda_check("timeline copy");
+  if (cudaMemcpyFromSymbol(host_sm, tf::g_tl_smid, sizeof(unsigned) * n) != cudaSuccess)
+    return cuda_check("timeline copy");
+  return TF_OK;
+}
+#endif
 
 TF_API int tf_exact_count(unsigned long long* out, int reset) {
   if (!out) return fail(TF_ERR_ARG, "null pointer%s");
