@@ -21,8 +21,17 @@
 
 namespace tf {
 
+// binary64 lanes per thread: 4 for the exponential families (512-thread CTAs,
+// 112 registers: +6% texp, +3% texpm1), 2 for the logarithms (1024-thread CTAs;
+// 4 lanes cost them ~2%).  TF_VW64 forces one width for all.
 #ifndef TF_VW64
-#define TF_VW64 2
+#define TF_VW64 0
+#endif
+#ifndef TF_VW64_EXP
+#define TF_VW64_EXP 4
+#endif
+#ifndef TF_VW64_LOG
+#define TF_VW64_LOG 2
 #endif
 #ifndef TF_VW32
 #define TF_VW32 4
@@ -561,7 +570,13 @@ int launch(const T* x0, const T* x1, T* z0, T* z1, int64_t n, void* stream, int 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uintptr_t al = (uintptr_t)x0 | (uintptr_t)x1 | (uintptr_t)z0 | (uintptr_t)z1;
   if ((al & 15) == 0) {
-    if constexpr (sizeof(T) == 8) return launch_one<T, FN, TF_VW64>(x0, x1, z0, z1, n, s, flags);
+    if constexpr (sizeof(T) == 8) {
+      constexpr bool EXPF = FN == tf::FN_TEXP || FN == tf::FN_TEXPM1 || FN == tf::FN_PEXP0 ||
+                            FN == tf::FN_TEXP0 || FN == tf::FN_PEXP || FN == tf::FN_PEXPM10 ||
+                            FN == tf::FN_TEXPM10 || FN == tf::FN_PEXPM1;
+      constexpr int VW = TF_VW64 ? TF_VW64 : (EXPF ? TF_VW64_EXP : TF_VW64_LOG);
+      return launch_one<T, FN, VW>(x0, x1, z0, z1, n, s, flags);
+    }
     else return launch_one<T, FN, TF_VW32>(x0, x1, z0, z1, n, s, flags);
   }
   if ((al & (sizeof(T) - 1)) != 0) return fail(TF_ERR_ARG, "misaligned pointer%s");
