@@ -319,6 +319,44 @@ def run_ours(args):
                         "vs_" + fn: ms / sms}
             del a0, a1, z0, z1
 
+    # ---- config 1 at its own size (2^20 texp f64): the launch-overhead regime,
+    # eager launches vs one CUDA graph of 100 launches
+    small = None
+    if not args.headline_only:
+        m = 1 << 20
+        a0, a1 = gen("exp64", m, torch.float64, rank * m)
+        z0, z1 = torch.empty_like(a0), torch.empty_like(a0)
+        f = api(64)
+        for _ in range(5):
+            f._launch("texp", a0, a1, z0, z1, m, sp)
+        reps = 100
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            f._launch("texp", a0, a1, z0, z1, m, sp)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        eager_ms = max_over_ranks(e0.elapsed_time(e1) / reps)
+        g = torch.cuda.CUDAGraph()
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        with torch.cuda.stream(gs):
+            with torch.cuda.graph(g, stream=gs):
+                for _ in range(reps):
+                    f._launch("texp", a0, a1, z0, z1, m, gs.cuda_stream)
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        graph_ms = max_over_ranks(e0.elapsed_time(e1) / reps)
+        small = {"config": "cfg1_texp_f64", "elements": m,
+                 "eager_ms": eager_ms, "eager_elements_per_s": m * world / (eager_ms * 1e-3),
+                 "graph_ms": graph_ms, "graph_elements_per_s": m * world / (graph_ms * 1e-3),
+                 "graph_launches": reps}
+        del a0, a1, z0, z1, g
+
     # ---- element-wise EFT / twofold arithmetic ops (HBM-bound streaming)
     eft_rates = {}
     if not args.headline_only and not args.no_eft:
@@ -423,6 +461,7 @@ def run_ours(args):
             "per_function": per_fn,
             "siblings": siblings,
             "eft_ops": eft_rates,
+            "cfg1_small": small,
             "parity_sample": stats,
         }
         print(json.dumps(line), flush=True)

@@ -23,3 +23,8 @@ d = json.loads(open("gpurun_out/bench.log").read().strip().splitlines()[-1])
 for k, v in d.get("eft_ops", {}).items():
     print(f'{k:18s} {v["elements_per_s"]/1e9:7.1f} Gelem/s  {v["hbm_gbs"]:7.0f} GB/s  hbm_frac {v["hbm_frac"]:.3f}')
 PY
+python - <<'PY'
+import json
+d = json.loads(open("gpurun_out/bench.log").read().strip().splitlines()[-1])
+print("cfg1_small", d.get("cfg1_small"))
+PY
