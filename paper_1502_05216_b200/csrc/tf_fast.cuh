@@ -604,6 +604,8 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
   }
   TF<T> s[VW];
   pexpm10_inband_v<T, VW>(tb, mr0, s);
+  T dl[VW], cv[VW], ce[VW];
+  unsigned near = 0;
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
     TF<T> w = fast_two_sum_u(sub(zc0[e], T(1)), zc1[e]);
@@ -625,12 +627,31 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     T d0 = mul(mul(y1[e], C::p2n(-n[e])), C::rcp(zc0[e]));
     ok[e] = ok[e] && ahi(d0) < C::DMAX;
     bool hard;
-    T zz = rn_guard(core.v, sub(core.e, d0), hard);
-    T dl = sub(y0[e], T(1));                          // exact near 1
-    if (ahi(dl) < C::NEAR1H) zz = log_near1(dl);
+    z0[e] = rn_guard(core.v, sub(core.e, d0), hard);
+    dl[e] = sub(y0[e], T(1));                         // exact near 1
+    if (ahi(dl[e]) < C::NEAR1H) near |= 1u << e;
     else ok[e] = ok[e] && !hard;
-    z0[e] = zz;
-    z1[e] = add(core.e, sub(core.v, zz));            // _correct (372-373)
+    cv[e] = core.v;
+    ce[e] = core.e;
+  }
+  // near-1 value parts (cfg 3: 5% of elements): one log_near1 per pass for the
+  // lowest flagged lane, so a warp pays for one series, not one per lane
+  while (near) {
+    T d = dl[0];
+#pragma unroll
+    for (int e = VW - 1; e > 0; --e)
+      if (near >> e & 1u) d = dl[e];
+    if (near & 1u) d = dl[0];
+    const unsigned low = near & (0u - near);
+    T r = log_near1(d);
+#pragma unroll
+    for (int e = 0; e < VW; ++e)
+      if (low == 1u << e) z0[e] = r;
+    near &= near - 1u;
+  }
+  if constexpr (!PM) {
+#pragma unroll
+    for (int e = 0; e < VW; ++e) z1[e] = add(ce[e], sub(cv[e], z0[e]));  // _correct (222-223)
   }
 }
 
