@@ -881,8 +881,46 @@ template <class T, int FN> struct HasAlt {
                          FN == FN_PEXPM1 || FN == FN_TLOG1P || FN == FN_TLOG1P0 ||
                          FN == FN_TLOG1PP || FN == FN_PLOG1P || FN == FN_PLOG1P0);
 };
+// binary64 out-of-band tlog1p / tlog1pp / plog1p when 1 + y0 is exact (e.g.
+// cfg 2's clamp value y0 = -1 + 2^-52, whose tail y1 is O(1 + y0), so the
+// unified branch's d = y1 / (1 + y0) is not small): tlogp(w), w = renorm(1 + v)
+// (explog.py:290-294, 239-242), and the value part CR log1p(y0) = CR log(1 + y0)
+// from a second tlog core on the exact argument.
+template <int FN>
+TF_DEV bool alt_log1p_exact1p(const STab<double>& tb, double y0, double y1, double& z0,
+                              double& z1) {
+  constexpr bool RENORM = FN == FN_TLOG1P;
+  constexpr bool PM = FN == FN_PLOG1P;
+  if (!is_finite(y0) || !is_finite(y1)) return false;
+  TF<double> v = RENORM ? renorm_u(mk(y0, y1)) : mk(y0, y1);
+  if (!(v.v < -0.5 || v.v > 1.0) || !(v.v > -1.0)) return false;
+  TF<double> w = renorm_u(t_add_d_u(v, 1.0));
+  double a[1] = {w.v}, b[1] = {w.e}, t0[1], t1[1];
+  bool ok[1];
+  fast_tlog<double, 1, false>(tb, a, b, t0, t1, ok);         // tlogp(w)
+  if (!ok[0]) return false;
+  if constexpr (PM) {                                          // renorm_fast(tlogp(w))
+    TF<double> r = fast_two_sum_u(t0[0], t1[0]);
+    z0 = r.v;
+    z1 = r.e;
+    return true;
+  } else {
+    TF<double> u = two_sum_u(1.0, y0);
+    if (!zbits(u.e)) return false;                             // 1 + y0 not exact
+    double c[1] = {u.v}, d[1] = {0.0}, l0[1], l1[1];
+    fast_tlog<double, 1, false>(tb, c, d, l0, l1, ok);       // CR log(1 + y0)
+    if (!ok[0]) return false;
+    z0 = l0[0];
+    z1 = add(t1[0], sub(t0[0], z0));                          // _correct (222-223)
+    return true;
+  }
+}
+
 template <class T, int FN>
 TF_DEV bool fast_alt(const STab<T>& tb, T x0, T x1, T& z0, T& z1) {
+  if constexpr (sizeof(T) == 8 && (FN == FN_TLOG1P || FN == FN_TLOG1PP || FN == FN_PLOG1P)) {
+    if (alt_log1p_exact1p<FN>(tb, x0, x1, z0, z1)) return true;
+  }
   T a[1] = {x0}, b[1] = {x1}, r0[1], r1[1];
   bool ok[1];
   if constexpr (FN == FN_TEXPM1 || FN == FN_TEXPM10 || FN == FN_PEXPM1) {
