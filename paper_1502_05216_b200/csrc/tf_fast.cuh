@@ -357,6 +357,25 @@ TF_DEV double rn_guard(double h, double l, bool& hard) {  // binary64 cores: ~2^
   return add(h, l);
 }
 
+// binary32 value part from the binary64 library (rare-element drain only):
+// CUDA's binary64 exp/expm1/log/log1p are within 1 ulp, so RN32 of the result
+// is the correctly rounded binary32 value unless it lies within 2 binary64
+// ulps of a binary32 rounding midpoint (hard: exact path).  Normal binary32
+// results only (29 dropped bits).
+TF_DEV float cr32_of(double v, bool& hard) {
+  const long long b = (long long)(ubits(v) & ((1ull << 29) - 1));
+  const long long dm = b - (1ll << 28);
+  hard = dm <= 2 && dm >= -2;
+  return __double2float_rn(v);
+}
+enum DFn { DF_EXP = 0, DF_EXPM1 = 1, DF_LOG = 2, DF_LOG1P = 3 };
+template <int F> TF_DEV float cr32_lib(float x, bool& hard) {
+  const double d = (double)x;
+  const double v = F == DF_EXP ? exp(d) : F == DF_EXPM1 ? expm1(d) : F == DF_LOG ? log(d)
+                                                                        : log1p(d);
+  return cr32_of(v, hard);
+}
+
 // ================================================================ texp
 // PM = true: pexp0 = renorm_fast(pexp0_raw(x0)) (explog.py:101-103), no libm value
 template <int VW, bool PM = false>
@@ -394,7 +413,8 @@ TF_DEV void fast_texp(const STab<double>& tb, const double (&x0)[VW], const doub
   }
 }
 
-template <int VW, bool PM = false>
+// DBLV: value part from the binary64 library (cr32_lib), rare-element drain
+template <int VW, bool PM = false, bool DBLV = false>
 TF_DEV void fast_texp(const STab<float>& tb, const float (&x0)[VW], const float (&x1)[VW],
                       float (&z0)[VW], float (&z1)[VW], bool (&ok)[VW]) {
   float y[VW];
@@ -424,7 +444,8 @@ TF_DEV void fast_texp(const STab<float>& tb, const float (&x0)[VW], const float 
     TF<float> es = tv<float>(tb.ESC[scaled ? m[e] - TF32_ESC_LO : 0]);
     TF<float> vs = t_mul_u(scaled ? es : ev, ct);
     bool hard;
-    z0[e] = mul(rn_guard<-35>(vs.v, vs.e, hard), scaled ? 0x1p-64f : 1.0f);
+    if constexpr (DBLV) z0[e] = cr32_lib<DF_EXP>(x0[e], hard);
+    else z0[e] = mul(rn_guard<-35>(vs.v, vs.e, hard), scaled ? 0x1p-64f : 1.0f);
     ok[e] = ok[e] && !hard;
     z1[e] = add(mul(z0[e], t1_tiny(x1[e])), add(v.e, sub(v.v, z0[e])));
   }
@@ -494,7 +515,7 @@ TF_DEV void fast_texpm1_fb(const STab<double>& tb, const double (&x0)[VW],
 }
 
 // binary32: the pexp0 - 1 fallback is the bulk (cfg 4: 99.2%)
-template <int VW, bool PM = false>
+template <int VW, bool PM = false, bool DBLV = false>
 TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const float (&x1)[VW],
                         float (&z0)[VW], float (&z1)[VW], bool (&ok)[VW]) {
   float y[VW];
@@ -520,11 +541,34 @@ TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const floa
       continue;
     }
     bool hard;
-    z0[e] = rn_guard<-35>(w.v, w.e, hard);
+    if constexpr (DBLV) z0[e] = cr32_lib<DF_EXPM1>(x0[e], hard);
+    else z0[e] = rn_guard<-35>(w.v, w.e, hard);
     ok[e] = ok[e] && !hard;
     float tail = add(w.e, sub(w.v, z0[e]));
     z1[e] = add(mul(add(z0[e], 1.0f), t1_tiny(x1[e])), tail);
   }
+}
+
+// binary32 in-band branch (|x0| <= LN2, expcore.py:142-146), drain only: the
+// main binary32 kernel takes the fallback branch (cfg 4: 99.2% of elements)
+template <bool PM = false>
+TF_DEV void fast_texpm1_inb32(const STab<float>& tb, float x0, float x1, float& z0, float& z1,
+                              bool& ok) {
+  ok = abits(x0) <= B32_LN2 && ahi(x1) < B32_X1_TINY;
+  float xs[1] = {ok ? x0 : 0.0f};
+  TF<float> w[1];
+  pexpm10_inband_v<float, 1>(tb, xs, w);
+  if constexpr (PM) {
+    TF<float> r = fast_two_sum_u(w[0].v, w[0].e);
+    z0 = r.v;
+    z1 = r.e;
+    return;
+  }
+  bool hard;
+  z0 = cr32_lib<DF_EXPM1>(xs[0], hard);
+  ok = ok && !hard;
+  float tail = add(w[0].e, sub(w[0].v, z0));
+  z1 = add(mul(add(z0, 1.0f), t1_tiny(x1)), tail);
 }
 
 // ================================================================= tlog
@@ -573,7 +617,7 @@ template <> struct LogC<float> {
 // as given (tlogp, plog; tlog0 / plog0 have y1 = 0, where renorm is the
 // identity); PM = true returns renorm_fast(core) instead of the _correct'ed
 // value part (plog0, plog).
-template <class T, int VW, bool RENORM = true, bool PM = false>
+template <class T, int VW, bool RENORM = true, bool PM = false, bool DBLV = false>
 TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW], T (&z0)[VW],
                       T (&z1)[VW], bool (&ok)[VW]) {
   using C = LogC<T>;
@@ -627,10 +671,15 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     T d0 = mul(mul(y1[e], C::p2n(-n[e])), C::rcp(zc0[e]));
     ok[e] = ok[e] && ahi(d0) < C::DMAX;
     bool hard;
-    z0[e] = rn_guard(core.v, sub(core.e, d0), hard);
     dl[e] = sub(y0[e], T(1));                         // exact near 1
-    if (ahi(dl[e]) < C::NEAR1H) near |= 1u << e;
-    else ok[e] = ok[e] && !hard;
+    if constexpr (DBLV && sizeof(T) == 4) {
+      z0[e] = cr32_lib<DF_LOG>(y0[e], hard);
+      ok[e] = ok[e] && !hard;
+    } else {
+      z0[e] = rn_guard(core.v, sub(core.e, d0), hard);
+      if (ahi(dl[e]) < C::NEAR1H) near |= 1u << e;
+      else ok[e] = ok[e] && !hard;
+    }
     cv[e] = core.v;
     ce[e] = core.e;
   }
@@ -672,7 +721,8 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
 // _plog1p0_raw's out-of-band branch, the raw _log_core of renorm(1 + y0)
 // without tlogp's inner _correct (tlog1p0, plog1p0); PM = true returns
 // renorm_fast of the raw result (plog1p0, plog1p).
-template <class T, int VW, bool RENORM = true, bool PM = false, bool INNER = true, int UNI = -1>
+template <class T, int VW, bool RENORM = true, bool PM = false, bool INNER = true, int UNI = -1,
+          bool DBLV = false>
 TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW], T (&z0)[VW],
                         T (&z1)[VW], bool (&ok)[VW]) {
   constexpr bool D = sizeof(T) == 8;
@@ -682,6 +732,7 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
   constexpr int DSEP = D ? 37 : 14;
   using C = LogC<T>;
   T y0[VW], y1[VW], sd[VW], ms[VW], zc0[VW], zc1[VW];
+  T wv[DBLV ? VW : 1];
   int n[VW];
   bool inb[VW];
   TF<T> v[VW];
@@ -707,6 +758,7 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       // out-of-band prologue; v0 > -1 keeps w0 = 1 + v0 positive and normal
       ok[e] = ok[e] && (inb[e] || !sgn(v[e].v) || ahi(v[e].v) < (D ? H64_ONE : B32_ONE));
       TF<T> w = renorm_u(t_add_d_u(v[e], T(1)));
+      if constexpr (DBLV) wv[e] = w.v;
       // |d| = |y1 / (1 + y0)| <= ~2^-13 so log1p(d) = d - d^2/2 suffices below
       ok[e] = ok[e] && (inb[e] || zbits(y1[e]) || bexp(y1[e]) + DSEP <= bexp(w.v));
       auto wb = ubits(w.v);
@@ -758,7 +810,9 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       T d = mul(y1[e], rcp_approx(add(T(1), y0[e])));
       ok[e] = ok[e] && (tiny || ahi(d) + ((uint32_t)(D ? 48 : 21) << (D ? 20 : 23)) <= ahi(sd[e]));
       bool hard;
-      T zz = rn_guard(sd[e], sub(x1, d), hard);
+      T zz;
+      if constexpr (DBLV && !D) zz = cr32_lib<DF_LOG1P>(y0[e], hard);
+      else zz = rn_guard(sd[e], sub(x1, d), hard);
       z0[e] = tiny ? y0[e] : zz;
       ok[e] = ok[e] && (tiny || !hard);
       z1[e] = add(x1, sub(sd[e], z0[e]));               // _correct (372-373)
@@ -780,7 +834,12 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       // (out-of-band: |log w0| >= ln 2 - tiny, |w1/w0| <= 2^-24)
       T rc = rcp_nr(zc0[e]);
       bool hard0;
-      T t0 = rn_guard(core.v, sub(core.e, mul(zc1[e], rc)), hard0);
+      T t0;
+      if constexpr (DBLV && !D) {
+        t0 = cr32_lib<DF_LOG>(wv[e], hard0);                 // log(w0)
+      } else {
+        t0 = rn_guard(core.v, sub(core.e, mul(zc1[e], rc)), hard0);
+      }
       ok[e] = ok[e] && !hard0;
       T t1 = add(core.e, sub(core.v, t0));
       if constexpr (PM) {                                 // renorm_fast(tlogp(w))
@@ -794,7 +853,9 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       // underflow the approximate reciprocal when y0 ~ FLT_MAX)
       T dd = mul(mul(y1[e], C::p2(-n[e])), rc);
       bool hard;
-      T zz = rn_guard(core.v, sub(core.e, fmaop(mul(T(-0.5), dd), dd, dd)), hard);
+      T zz;
+      if constexpr (DBLV && !D) zz = cr32_lib<DF_LOG1P>(y0[e], hard);
+      else zz = rn_guard(core.v, sub(core.e, fmaop(mul(T(-0.5), dd), dd, dd)), hard);
       ok[e] = ok[e] && !hard;
       z0[e] = zz;
       if constexpr (INNER) z1[e] = add(t1, sub(t0, zz));  // _correct (222-223)
@@ -877,10 +938,50 @@ TF_DEV void tlog1p_sorted(const STab<float>& tb, Xch<VW>* xw, const float (&x0)[
 // element is ~10x this, and these branches are most of cfg 2's rare elements.
 template <class T, int FN> struct HasAlt {
   static constexpr bool value =
-      sizeof(T) == 8 && (FN == FN_TEXPM1 || FN == FN_TEXPM10 || FN == FN_PEXPM10 ||
-                         FN == FN_PEXPM1 || FN == FN_TLOG1P || FN == FN_TLOG1P0 ||
-                         FN == FN_TLOG1PP || FN == FN_PLOG1P || FN == FN_PLOG1P0);
+      sizeof(T) == 4 ||
+      (FN == FN_TEXPM1 || FN == FN_TEXPM10 || FN == FN_PEXPM10 || FN == FN_PEXPM1 ||
+       FN == FN_TLOG1P || FN == FN_TLOG1P0 || FN == FN_TLOG1PP || FN == FN_PLOG1P ||
+       FN == FN_PLOG1P0);
 };
+
+// binary32 second chance: the same fast cores with the value part from the
+// binary64 library instead of the 2^-32 rounding guard (which sends ~0.5% of
+// elements away), and texpm1's in-band branch
+template <int FN>
+TF_DEV bool fast_alt32(const STab<float>& tb, float x0, float x1, float& z0, float& z1) {
+  float a[1] = {x0}, b[1] = {x1}, r0[1], r1[1];
+  bool ok[1];
+  if constexpr (FN == FN_TEXP || FN == FN_TEXPP || FN == FN_TEXP0 || FN == FN_PEXP) {
+    fast_texp<1, false, true>(tb, a, b, r0, r1, ok);
+  } else if constexpr (FN == FN_PEXP0) {
+    return false;                                  // no value part to guard
+  } else if constexpr (FN == FN_TEXPM1 || FN == FN_TEXPM1P || FN == FN_TEXPM10 ||
+                       FN == FN_PEXPM1 || FN == FN_PEXPM10) {
+    constexpr bool PM = FN == FN_PEXPM10;
+    if (abits(x0) <= B32_LN2) fast_texpm1_inb32<PM>(tb, x0, x1, r0[0], r1[0], ok[0]);
+    else if constexpr (PM) return false;
+    else fast_texpm1<1, false, true>(tb, a, b, r0, r1, ok);
+  } else if constexpr (FN == FN_TLOG || FN == FN_TLOG0) {
+    fast_tlog<float, 1, true, false, true>(tb, a, b, r0, r1, ok);
+  } else if constexpr (FN == FN_TLOGP) {
+    fast_tlog<float, 1, false, false, true>(tb, a, b, r0, r1, ok);
+  } else if constexpr (FN == FN_PLOG0 || FN == FN_PLOG) {
+    return false;
+  } else {
+    constexpr bool RENORM = FN == FN_TLOG1P;
+    constexpr bool PM = FN == FN_PLOG1P0 || FN == FN_PLOG1P;
+    constexpr bool INNER = !(FN == FN_TLOG1P0 || FN == FN_PLOG1P0);
+    fast_tlog1p<float, 1, RENORM, PM, INNER, 1, true>(tb, a, b, r0, r1, ok);
+  }
+  if constexpr (FN == FN_PEXP || FN == FN_PEXPM1) {
+    TF<float> r = fast_two_sum_u(r0[0], r1[0]);
+    r0[0] = r.v;
+    r1[0] = r.e;
+  }
+  z0 = r0[0];
+  z1 = r1[0];
+  return ok[0];
+}
 // binary64 out-of-band tlog1p / tlog1pp / plog1p when 1 + y0 is exact (e.g.
 // cfg 2's clamp value y0 = -1 + 2^-52, whose tail y1 is O(1 + y0), so the
 // unified branch's d = y1 / (1 + y0) is not small): tlogp(w), w = renorm(1 + v)
@@ -916,8 +1017,9 @@ TF_DEV bool alt_log1p_exact1p(const STab<double>& tb, double y0, double y1, doub
   }
 }
 
-template <class T, int FN>
-TF_DEV bool fast_alt(const STab<T>& tb, T x0, T x1, T& z0, T& z1) {
+template <int FN>
+TF_DEV bool fast_alt64(const STab<double>& tb, double x0, double x1, double& z0, double& z1) {
+  using T = double;
   if constexpr (sizeof(T) == 8 && (FN == FN_TLOG1P || FN == FN_TLOG1PP || FN == FN_PLOG1P)) {
     if (alt_log1p_exact1p<FN>(tb, x0, x1, z0, z1)) return true;
   }
@@ -941,6 +1043,15 @@ TF_DEV bool fast_alt(const STab<T>& tb, T x0, T x1, T& z0, T& z1) {
   z0 = r0[0];
   z1 = r1[0];
   return ok[0];
+}
+
+template <class T, int FN>
+TF_DEV bool fast_alt(const STab<T>& tb, T x0, T x1, T& z0, T& z1) {
+  if constexpr (sizeof(T) == 4) {
+    return fast_alt32<FN>(tb, x0, x1, z0, z1);
+  } else {
+    return fast_alt64<FN>(tb, x0, x1, z0, z1);
+  }
 }
 
 // log1p-family functions (class-sorted in binary32)
