@@ -617,10 +617,15 @@ template <> struct LogC<float> {
 // as given (tlogp, plog; tlog0 / plog0 have y1 = 0, where renorm is the
 // identity); PM = true returns renorm_fast(core) instead of the _correct'ed
 // value part (plog0, plog).
-template <class T, int VW, bool RENORM = true, bool PM = false, bool DBLV = false>
+// FULLR (binary64 drain only): the top binade y0 >= 2^1022 too, scaling by a
+// possibly subnormal 2^-n (p2 instead of the two-op p2n)
+template <class T, int VW, bool RENORM = true, bool PM = false, bool DBLV = false,
+          bool FULLR = false>
 TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW], T (&z0)[VW],
                       T (&z1)[VW], bool (&ok)[VW]) {
   using C = LogC<T>;
+  constexpr uint32_t SPAN = FULLR ? C::NORM_SPAN + 2u : C::NORM_SPAN;
+  auto p2s = [](int k) { return FULLR ? C::p2(k) : C::p2n(k); };
   T y0[VW], y1[VW], zc0[VW], zc1[VW], r0[VW], mr0[VW];
   int n[VW];
   TF<T> v[VW];
@@ -628,17 +633,17 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
   for (int e = 0; e < VW; ++e) {
     // positive normal y0 (below 2^1022 / 2^126) and finite y1; how small y1 is
     // against y0 is checked on d = y1/y0 below, where it matters
-    ok[e] = C::eb(y0i[e]) - 1u < C::NORM_SPAN && is_finite(y1i[e]);
+    ok[e] = C::eb(y0i[e]) - 1u < SPAN && is_finite(y1i[e]);
     y0[e] = ok[e] ? y0i[e] : T(1);
     y1[e] = ok[e] ? y1i[e] : T(0);
     v[e] = RENORM ? renorm_u(mk(y0[e], y1[e])) : mk(y0[e], y1[e]);
-    ok[e] = ok[e] && C::eb(v[e].v) - 1u < C::NORM_SPAN;
+    ok[e] = ok[e] && C::eb(v[e].v) - 1u < SPAN;
     if (!ok[e]) v[e] = mk(T(1), T(0));
     auto vb = ubits(v[e].v);
     bool band = vb >= C::HALF && vb <= C::TWO;
     n[e] = band ? 0 : C::n_of(v[e].v);
     zc0[e] = band ? v[e].v : C::mant(v[e].v);
-    zc1[e] = band ? v[e].e : (zbits(v[e].e) ? T(0) : mul(v[e].e, C::p2n(-n[e])));
+    zc1[e] = band ? v[e].e : (zbits(v[e].e) ? T(0) : mul(v[e].e, p2s(-n[e])));
     r0[e] = seed_log1p_t(add(sub(zc0[e], T(1)), zc1[e]),      // explog.py:196-199
                          [&](int i) { return tb.SEED[i]; });
     ok[e] = ok[e] && C::in_ln2(r0[e]);
@@ -668,7 +673,7 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     // to d = y1/y0 (|d| <= 2^-50 |log y0|, 2^-17 in binary32), so
     // log(y0) = core - d to well below an ulp with d known to ~2^-22:
     // y1 * 2^-n over zc0 (= v0 * 2^-n, within an ulp of y0 * 2^-n).
-    T d0 = mul(mul(y1[e], C::p2n(-n[e])), C::rcp(zc0[e]));
+    T d0 = mul(mul(y1[e], p2s(-n[e])), C::rcp(zc0[e]));
     ok[e] = ok[e] && ahi(d0) < C::DMAX;
     bool hard;
     dl[e] = sub(y0[e], T(1));                         // exact near 1
@@ -941,7 +946,8 @@ template <class T, int FN> struct HasAlt {
       sizeof(T) == 4 ||
       (FN == FN_TEXPM1 || FN == FN_TEXPM10 || FN == FN_PEXPM10 || FN == FN_PEXPM1 ||
        FN == FN_TLOG1P || FN == FN_TLOG1P0 || FN == FN_TLOG1PP || FN == FN_PLOG1P ||
-       FN == FN_PLOG1P0);
+       FN == FN_PLOG1P0 || FN == FN_TLOG || FN == FN_TLOG0 || FN == FN_TLOGP ||
+       FN == FN_PLOG || FN == FN_PLOG0);
 };
 
 // binary32 second chance: the same fast cores with the value part from the
@@ -1034,6 +1040,12 @@ TF_DEV bool fast_alt64(const STab<double>& tb, double x0, double x1, double& z0,
     }
   } else if constexpr (FN == FN_PEXPM10) {
     fast_texpm1_fb<1, true>(tb, a, b, r0, r1, ok);
+  } else if constexpr (FN == FN_TLOG || FN == FN_TLOG0) {       // top binade
+    fast_tlog<T, 1, true, false, false, true>(tb, a, b, r0, r1, ok);
+  } else if constexpr (FN == FN_TLOGP) {
+    fast_tlog<T, 1, false, false, false, true>(tb, a, b, r0, r1, ok);
+  } else if constexpr (FN == FN_PLOG0 || FN == FN_PLOG) {
+    fast_tlog<T, 1, false, true, false, true>(tb, a, b, r0, r1, ok);
   } else {
     constexpr bool RENORM = FN == FN_TLOG1P;
     constexpr bool PM = FN == FN_PLOG1P0 || FN == FN_PLOG1P;
