@@ -27,10 +27,12 @@ template <class T> struct STab {
   typename V2<T>::t C[P<T>::C_N];
   typename V2<T>::t CM1[P<T>::CM1_N];
   typename V2<T>::t ESC[sizeof(T) == 8 ? TF64_ESC_COUNT : TF32_ESC_COUNT];
-  typename V2<T>::t SEED[TF64_SEED_COUNT];
+  typename V2<T>::t SEED[sizeof(T) == 8 ? TF64_SEED_COUNT : TF32_SEED_COUNT];
 };
 
-template <class T> __device__ void load_tables(STab<T>& s) {
+// SEED (the log seed table, 32 KB in binary64) is staged only by the
+// logarithm kernels
+template <class T> __device__ void load_tables(STab<T>& s, bool seed) {
   const T* srcE = sizeof(T) == 8 ? (const T*)g_E64 : (const T*)g_E32;
   const T* srcC = sizeof(T) == 8 ? (const T*)g_C64 : (const T*)g_C32;
   const T* srcM = sizeof(T) == 8 ? (const T*)g_CM164 : (const T*)g_CM132;
@@ -42,7 +44,9 @@ template <class T> __device__ void load_tables(STab<T>& s) {
   for (int i = threadIdx.x; i < NS; i += blockDim.x) { s.ESC[i].x = srcS[2 * i]; s.ESC[i].y = srcS[2 * i + 1]; }
   const typename V2<T>::t* srcD =
       sizeof(T) == 8 ? (const typename V2<T>::t*)g_SEED64 : (const typename V2<T>::t*)g_SEED32;
-  for (int i = threadIdx.x; i < TF64_SEED_COUNT; i += blockDim.x) s.SEED[i] = srcD[i];
+  constexpr int ND = sizeof(T) == 8 ? TF64_SEED_COUNT : TF32_SEED_COUNT;
+  if (seed)
+    for (int i = threadIdx.x; i < ND; i += blockDim.x) s.SEED[i] = srcD[i];
 }
 
 template <class T, class V> TF_DEV TF<T> tv(V a) { return mk(a.x, a.y); }

@@ -295,17 +295,16 @@ TF_DEV float expm1_t1(float x) {
 // CUDA's are within 1 ulp and the Newton step absorbs the difference.
 //
 // The seed is a compact table-driven log1p (relative error ~2^-52 / 2^-23,
-// 13 FP64 ops, no branches) over a in [-1/2, 1], where every caller's argument
+// 10 FP64 ops, no branches) over a in [-1/2, 1], where every caller's argument
 // lies: f = 1 + a split exactly as f + clo, bucket (invc, logc) from the
-// exponent and 7 leading mantissa bits of f, r = f * invc - 1 (|r| <= 2^-8),
-// log1p(a) = logc + log1p(r) + clo/f; |a| < 2^-8 uses r = a directly.  The
+// exponent and 10 (binary32: 7) leading mantissa bits of f, r = f * invc - 1
+// (|r| <= 2^-11, resp. 2^-8), log1p(a) = logc + log1p(r) + clo/f; |a| below
+// that uses r = a directly.  The
 // fast kernels read the table from shared memory, the exact path through the
 // read-only cache, so both produce the same seed bits.
-TF_DEV double seed_poly(double r) {  // log1p(r), |r| <= 2^-8 (+slack), degree 7
+TF_DEV double seed_poly(double r) {  // log1p(r), |r| <= 2^-11 (+slack), degree 5
   double q = mul(r, r);
-  double p = fmaop(r, 0x1.2492492492492p-3, -0x1.5555555555555p-3);
-  p = fmaop(r, p, 0x1.999999999999ap-3);
-  p = fmaop(r, p, -0.25);
+  double p = fmaop(r, 0x1.999999999999ap-3, -0.25);
   p = fmaop(r, p, 0x1.5555555555555p-2);
   p = fmaop(r, p, -0.5);
   return fmaop(q, p, r);
@@ -317,12 +316,13 @@ TF_DEV float seed_poly(float r) {   // degree 4
   return fmaop(q, p, r);
 }
 template <class Get> TF_DEV double seed_log1p_t(double a, Get get) {
+  constexpr int B = TF64_SEED_BITS, NB = 1 << B;
   double f = add(1.0, a);
   double clo = sub(a, sub(f, 1.0));                    // 1 + a == f + clo exactly
   uint32_t h = (uint32_t)hi32(f);
-  int idx = (((int)(h >> 20) - 1022) << 7) | (int)((h >> 13) & 127u);
-  bool small = ahi(a) < 0x3f700000u;                  // |a| < 2^-8
-  idx = small ? 128 : min(max(idx, 0), 256);
+  int idx = (((int)(h >> 20) - 1022) << B) | (int)((h >> (20 - B)) & (NB - 1u));
+  bool small = ahi(a) < 0x3f400000u;                  // |a| < 2^-11
+  idx = small ? NB : min(max(idx, 0), 2 * NB);
   double2 t = get(idx);
   double r = small ? a : fmaop(f, t.x, -1.0);
   double p = seed_poly(r);
@@ -332,9 +332,10 @@ template <class Get> TF_DEV float seed_log1p_t(float a, Get get) {
   float f = add(1.0f, a);
   float clo = sub(a, sub(f, 1.0f));
   uint32_t h = ubits(f);
-  int idx = (((int)(h >> 23) - 126) << 7) | (int)((h >> 16) & 127u);
+  constexpr int B = TF32_SEED_BITS, NB = 1 << B;
+  int idx = (((int)(h >> 23) - 126) << B) | (int)((h >> (23 - B)) & (NB - 1u));
   bool small = ahi(a) < 0x3b800000u;                  // |a| < 2^-8
-  idx = small ? 128 : min(max(idx, 0), 256);
+  idx = small ? NB : min(max(idx, 0), 2 * NB);
   float2 t = get(idx);
   float r = small ? a : fmaop(f, t.x, -1.0f);
   float p = seed_poly(r);

@@ -196,7 +196,11 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   unsigned long long tl0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl0));
 #endif
-  load_tables(tb);
+  constexpr bool LOGF = FN == FN_TLOG || FN == FN_TLOG1P || FN == FN_PLOG0 ||
+                        FN == FN_TLOG0 || FN == FN_TLOGP || FN == FN_PLOG ||
+                        FN == FN_PLOG1P0 || FN == FN_TLOG1P0 || FN == FN_TLOG1PP ||
+                        FN == FN_PLOG1P;
+  load_tables(tb, LOGF);
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
