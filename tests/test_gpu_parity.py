@@ -277,3 +277,34 @@ def test_sibling_fast_equals_exact_on_config(fn, width, cuda):
     s = compare(a.value[:m].cpu().numpy(), a.error[:m].cpu().numpy(),
                 *_crsim(fn, width, h0, h1, "fma"), width)
     assert s["class_mismatch"] == 0 and s["tol_violations"] == 0, s
+
+
+@pytest.mark.parametrize("width", WIDTHS)
+@pytest.mark.parametrize("fn", ("texp", "texpm1", "tlog", "tlog1p", "texp0", "plog1p"))
+def test_unaligned_arrays_use_scalar_kernel_same_bits(fn, width, cuda):
+    """Arrays that are element- but not 16-byte-aligned run the one-lane kernel;
+    results equal the vector kernel's bit for bit."""
+    import torch
+
+    from paper_1502_05216_b200 import _lib, api, family_of
+
+    L = _lib.ensure_device(cuda.index)
+    dist = SIB_DIST[(family_of(fn), width)]
+    dt = torch.float64 if width == 64 else torch.float32
+    n = (1 << 18) + 7
+    x0 = torch.empty(n + 1, dtype=dt, device=cuda)
+    x1 = torch.empty_like(x0)
+    _lib.check(L.tf_generate(_lib.DIST_CODES[dist], 9, 0, n + 1, x0.data_ptr(), x1.data_ptr(),
+                             None), "gen")
+    lib = api(width)
+    a0, a1 = x0[1:], x1[1:]                       # offset by one element
+    assert a0.data_ptr() % 16 != 0
+    b0, b1 = a0.clone(), a1.clone()               # aligned copies
+    dotted = fn.endswith("0")
+    za = lib._device(fn, a0, a0 if dotted else a1)
+    zb = lib._device(fn, b0, b0 if dotted else b1)
+    torch.cuda.synchronize()
+    assert torch.equal(za.value.view(torch.int64 if width == 64 else torch.int32),
+                       zb.value.view(torch.int64 if width == 64 else torch.int32))
+    assert torch.equal(za.error.view(torch.int64 if width == 64 else torch.int32),
+                       zb.error.view(torch.int64 if width == 64 else torch.int32))
