@@ -47,7 +47,7 @@ _inited: set[int] = set()
 
 def build(force: bool = False) -> str:
     """Compile the CUDA library in-tree for sm_100a (nvcc; see csrc/Makefile)."""
-    args = ["make", "-s", "-C", CSRC]
+    args = ["make", "-s", f"-j{min(4, os.cpu_count() or 1)}", "-C", CSRC]
     if force:
         args.insert(1, "-B")
     subprocess.run(args, check=True)
