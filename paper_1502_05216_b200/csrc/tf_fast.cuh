@@ -816,7 +816,9 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       bool tiny = ahi(y0[e]) < (D ? H64_TINY54 : B32_TINY25);
       // v - y0 == y1 exactly; with |d| <= 2^-48 |log1p(y0)| (2^-21 binary32)
       // ~2^-22 accuracy of d suffices; below 2^-54 the value part is y0 itself
-      T d = mul(y1[e], rcp_approx(add(T(1), y0[e])));
+      // binary64 needs the refined reciprocal: MUFU alone is 2^-19.9
+      // (tools/micro/rcp_acc.cu), which would misround ~1e-6 of the z0
+      T d = mul(y1[e], C::rcp(add(T(1), y0[e])));
       ok[e] = ok[e] && (tiny || ahi(d) + ((uint32_t)(D ? 48 : 21) << (D ? 20 : 23)) <= ahi(sd[e]));
       bool hard;
       T zz;

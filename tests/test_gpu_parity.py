@@ -245,6 +245,36 @@ SIB_DIST = {("exp", 64): "exp64s", ("expm1", 64): "pow10_64", ("log", 64): "logu
 
 
 @pytest.mark.parametrize("width", WIDTHS)
+@pytest.mark.parametrize("fn", FNS)
+def test_fast_equals_exact_on_config_large(fn, width, cuda):
+    """The four hot-path kernels against the exact path, bitwise, on 2^22
+    config-distributed elements: a value-part shortcut that misrounds even
+    1e-6 of the elements shows up here."""
+    import torch
+
+    from paper_1502_05216_b200 import _lib, api, family_of
+
+    L = _lib.ensure_device(cuda.index)
+    dist = {("texp", 64): "exp64", ("texpm1", 64): "pow10_64", ("tlog", 64): "log64",
+            ("tlog1p", 64): "pow10c_64", ("texp", 32): "exp32", ("texpm1", 32): "exp32",
+            ("tlog", 32): "log32", ("tlog1p", 32): "log32"}[(fn, width)]
+    dt = torch.float64 if width == 64 else torch.float32
+    n = 1 << 22
+    x0 = torch.empty(n, dtype=dt, device=cuda)
+    x1 = torch.empty_like(x0)
+    _lib.check(L.tf_generate(_lib.DIST_CODES[dist], 77, 0, n, x0.data_ptr(), x1.data_ptr(), None),
+               "gen")
+    lib = api(width)
+    a = lib._device(fn, x0, x1)
+    b = lib._device(fn, x0, x1, flags=_lib.FLAG_FORCE_EXACT)
+    torch.cuda.synchronize()
+    iv = torch.int64 if width == 64 else torch.int32
+    bad = (a.value.view(iv) != b.value.view(iv)) | (a.error.view(iv) != b.error.view(iv))
+    idx = torch.nonzero(bad).flatten()[:5].tolist()
+    assert not bad.any(), [(float(x0[i]), float(x1[i])) for i in idx]
+
+
+@pytest.mark.parametrize("width", WIDTHS)
 @pytest.mark.parametrize("fn", SIBLINGS)
 def test_sibling_fast_equals_exact_on_config(fn, width, cuda):
     """The sibling fast paths (admission-band cores + variant epilogues) against
