@@ -583,7 +583,9 @@ TF_DEV void fast_texpm1_inb32(const STab<float>& tb, float x0, float x1, float& 
 template <class T> struct LogC;
 template <> struct LogC<double> {
   static constexpr uint32_t NORM_SPAN = 2044u;   // positive normal and < 2^1022: 2^-n normal
-  static constexpr uint32_t DMAX = (1023u - 40u) << 20;  // |d| < 2^-40 (tlog value part)
+  // |d| < 2^-50 (tlog value part): log(y0) = core - d drops d^2/2, which must
+  // stay far below an ulp of |log y0| >= 2^-20 (coupled inputs have |d| <= 2^-53)
+  static constexpr uint32_t DMAX = (1023u - 50u) << 20;
   static constexpr int SMALL = 50, EBIAS = 1022;
   static constexpr uint64_t HALF = B64_HALF, TWO = B64_TWO;
   static constexpr uint32_t NEAR1H = H64_NEAR1;
