@@ -569,7 +569,12 @@ TF_DEV void fast_texpm1_inb32(const STab<float>& tb, float x0, float x1, float& 
     return;
   }
   bool hard;
-  z0 = cr32_lib<DF_EXPM1>(xs[0], hard);
+  z0 = rn_guard<-35>(w[0].v, w[0].e, hard);        // binary64 library only when
+  if (hard) z0 = cr32_lib<DF_EXPM1>(xs[0], hard);  // the core cannot decide
+  if (ahi(xs[0]) < B32_TINY25) {                    // expm1(x) rounds to x (keeps -0)
+    z0 = xs[0];
+    hard = false;
+  }
   ok = ok && !hard;
   float tail = add(w[0].e, sub(w[0].v, z0));
   z1 = add(mul(add(z0, 1.0f), t1_tiny(x1)), tail);

@@ -98,6 +98,17 @@ TF_DEV void st(T* p, uint64_t vi, const T (&a)[VW]) {
 #ifndef TF_BLOCK
 #define TF_BLOCK 1024
 #endif
+// cp.async stages: the binary32 exponentials move the most bytes per FP op
+// and gain from a third stage in flight (+2% texpm1); the logarithms do not
+#ifndef TF_STAGES32
+#define TF_STAGES32 3
+#endif
+#ifndef TF_STAGES32_LOG
+#define TF_STAGES32_LOG 2
+#endif
+#ifndef TF_STAGES64
+#define TF_STAGES64 2
+#endif
 template <class T, int VW> struct KCfg {
   static constexpr bool WIDE = sizeof(T) == 8 && VW == 4;   // 4 binary64 lanes per thread
   static constexpr bool WIDE32 = sizeof(T) == 4 && VW == 8;  // 8 binary32 lanes per thread
@@ -106,19 +117,25 @@ template <class T, int VW> struct KCfg {
 };
 
 // shared-memory layout of one k_eval CTA (dynamic: > 48 KB)
-template <class T, int VW, int BLOCK, bool ASYNC, bool XCH> struct EvalSmem {
+template <class T, int VW, int BLOCK, bool ASYNC, bool XCH, int STAGES> struct EvalSmem {
   static constexpr int WARPS = BLOCK / 32;
   static constexpr int QCAP = 32 + 32 * VW;
   STab<T> tb;
   uint32_t qs[WARPS][QCAP];
-  __align__(16) T stg[ASYNC ? 2 : 1][2][BLOCK][VW];
+  __align__(16) T stg[ASYNC ? STAGES : 1][2][BLOCK][VW];
   Xch<VW> xch[XCH ? WARPS : 1];
 };
 template <class T, int FN, int VW> struct EvalCfg {
   static constexpr int BLOCK = KCfg<T, VW>::BLOCK;
   static constexpr bool ASYNC = VW * sizeof(T) % 16 == 0;
   static constexpr bool XCH = log1p_fn(FN) && sizeof(T) == 4 && VW >= 2;
-  typedef EvalSmem<T, VW, BLOCK, ASYNC, XCH> Smem;
+  static constexpr bool LOGF = FN == FN_TLOG || FN == FN_TLOG1P || FN == FN_PLOG0 ||
+                               FN == FN_TLOG0 || FN == FN_TLOGP || FN == FN_PLOG ||
+                               FN == FN_PLOG1P0 || FN == FN_TLOG1P0 || FN == FN_TLOG1PP ||
+                               FN == FN_PLOG1P;
+  static constexpr int STAGES =
+      sizeof(T) == 8 ? TF_STAGES64 : (LOGF ? TF_STAGES32_LOG : TF_STAGES32);
+  typedef EvalSmem<T, VW, BLOCK, ASYNC, XCH, STAGES> Smem;
 };
 
 // ---- asynchronous global -> shared staging (LDGSTS), one 16 B vector per
@@ -178,7 +195,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   constexpr int QCAP = 32 + 32 * VW;
   static_assert(QCAP <= 160, "queue compaction below moves at most 4 x 32 entries");
   static_assert(VW == 1 || VW * sizeof(T) % 16 == 0, "vector lanes must fill 16-byte chunks");
-  constexpr int STAGES = 2;
+  constexpr int STAGES = EvalCfg<T, FN, VW>::STAGES;
   constexpr bool ASYNC = VW * sizeof(T) % 16 == 0;
   constexpr int NC = VW * (int)sizeof(T) / 16;        // 16-byte chunks per thread
   constexpr int EC = 16 / (int)sizeof(T);             // elements per chunk
@@ -191,16 +208,12 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   auto& xch = S.xch;
   constexpr bool XCH = EvalCfg<T, FN, VW>::XCH;
   constexpr bool DOT = dotted_fn(FN);  // plain argument: x1 is never read
-  static_assert(STAGES == 2 || !ASYNC, "two-stage staging");
+  static_assert(STAGES >= 2, "at least double buffering");
 #if TF_TIMELINE
   unsigned long long tl0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl0));
 #endif
-  constexpr bool LOGF = FN == FN_TLOG || FN == FN_TLOG1P || FN == FN_PLOG0 ||
-                        FN == FN_TLOG0 || FN == FN_TLOGP || FN == FN_PLOG ||
-                        FN == FN_PLOG1P0 || FN == FN_TLOG1P0 || FN == FN_TLOG1PP ||
-                        FN == FN_PLOG1P;
-  load_tables(tb, LOGF);
+  load_tables(tb, EvalCfg<T, FN, VW>::LOGF);
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -223,15 +236,26 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   // partitions -- evened out the finish times but cost more than it saved:
   // 93.7 vs 95.7 G elem/s on the headline step.)
   uint32_t base = first, nbase = first + stride;
-  if constexpr (ASYNC) {
-    uint32_t vi = base + lane;
-    bool v = vi < nvec;
+  // staging: iteration i reads stage i % STAGES; the loads of iterations up to
+  // i + STAGES - 1 are in flight (one commit group each)
+  uint32_t pbase = first;                 // next base to prefetch
+  auto stage_in = [&](int st, uint32_t pb) {
+    uint32_t pv = pb + lane;
+    bool pvalid = pv < nvec;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      cp_async16(&stg[0][0][threadIdx.x][c * EC], x0 + (v ? vi * VW + c * EC : 0u), v);
-      if (!DOT) cp_async16(&stg[0][1][threadIdx.x][c * EC], x1 + (v ? vi * VW + c * EC : 0u), v);
+      cp_async16(&stg[st][0][threadIdx.x][c * EC], x0 + (pvalid ? pv * VW + c * EC : 0u), pvalid);
+      if (!DOT)
+        cp_async16(&stg[st][1][threadIdx.x][c * EC], x1 + (pvalid ? pv * VW + c * EC : 0u), pvalid);
     }
     cp_async_commit();
+  };
+  if constexpr (ASYNC) {
+#pragma unroll
+    for (int st = 0; st < STAGES - 1; ++st) {
+      stage_in(st, pbase);
+      pbase += stride;
+    }
   }
   int cs = 0;
   while (base < nvec) {
@@ -240,22 +264,17 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
     T a[VW], b[VW], r0[VW], r1[VW];
     bool rare[VW];
     if constexpr (ASYNC) {
-      uint32_t pv = nbase + lane;
-      bool pvalid = pv < nvec;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        cp_async16(&stg[cs ^ 1][0][threadIdx.x][c * EC], x0 + (pvalid ? pv * VW + c * EC : 0u), pvalid);
-        if (!DOT)
-          cp_async16(&stg[cs ^ 1][1][threadIdx.x][c * EC], x1 + (pvalid ? pv * VW + c * EC : 0u), pvalid);
-      }
-      cp_async_commit();
-      cp_async_wait<1>();
+      int ps = cs + STAGES - 1;
+      if (ps >= STAGES) ps -= STAGES;
+      stage_in(ps, pbase);
+      pbase += stride;
+      cp_async_wait<STAGES - 1>();
 #pragma unroll
       for (int e = 0; e < VW; ++e) {
         a[e] = stg[cs][0][threadIdx.x][e];
         b[e] = DOT ? T(0) : stg[cs][1][threadIdx.x][e];
       }
-      cs ^= 1;
+      if (++cs == STAGES) cs = 0;
     } else {
       if (valid) {
         ld<T, VW>(x0, vi, a);
