@@ -186,6 +186,23 @@ TF_DEV void drain(const STab<T>& tb, const uint32_t* q, int cnt, const T* __rest
   }
 }
 
+// Drop the first 32 entries of a warp's rare queue (entries [32, qn) move
+// down by 32): every lane reads its entries of all chunks, then writes.
+template <int QCAP>
+TF_DEV void queue_shift(uint32_t* q, int qn, int lane) {
+  constexpr int NCH = (QCAP + 31) / 32 - 1;
+  uint32_t mv[NCH > 0 ? NCH : 1];
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    const int src = lane + 32 * (k + 1);
+    mv[k] = src < qn ? q[src] : 0u;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < NCH; ++k)
+    if (lane + 32 * (k + 1) < qn) q[lane + 32 * k] = mv[k];
+}
+
 template <class T, int FN, int VW>
 __global__ void __launch_bounds__((KCfg<T, VW>::BLOCK), (KCfg<T, VW>::MINB))
 k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
@@ -193,7 +210,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   constexpr int BLOCK = KCfg<T, VW>::BLOCK;
   constexpr int WARPS = BLOCK / 32;
   constexpr int QCAP = 32 + 32 * VW;
-  static_assert(QCAP <= 160, "queue compaction below moves at most 4 x 32 entries");
+
   static_assert(VW == 1 || VW * sizeof(T) % 16 == 0, "vector lanes must fill 16-byte chunks");
   constexpr int STAGES = EvalCfg<T, FN, VW>::STAGES;
   constexpr bool ASYNC = VW * sizeof(T) % 16 == 0;
@@ -315,15 +332,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
 #endif
       drain<T, FN>(tb, q, 32, x0, x1, z0, z1, lane, count, mark, force);
       __syncwarp();
-      uint32_t mv = (lane + 32 < qn) ? q[lane + 32] : 0u;
-      uint32_t mv2 = (lane + 64 < qn) ? q[lane + 64] : 0u;
-      uint32_t mv3 = (lane + 96 < qn) ? q[lane + 96] : 0u;
-      uint32_t mv4 = (lane + 128 < qn) ? q[lane + 128] : 0u;
-      __syncwarp();
-      if (lane + 32 < qn) q[lane] = mv;
-      if (lane + 64 < qn) q[lane + 32] = mv2;
-      if (lane + 96 < qn) q[lane + 64] = mv3;
-      if (lane + 128 < qn) q[lane + 96] = mv4;
+      queue_shift<QCAP>(q, qn, lane);
       qn -= 32;
       __syncwarp();
     }
@@ -346,15 +355,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
     int c = qn < 32 ? qn : 32;
     drain<T, FN>(tb, q, c, x0, x1, z0, z1, lane, count, mark, force);
     __syncwarp();
-    uint32_t mv = (lane + 32 < qn) ? q[lane + 32] : 0u;
-    uint32_t mv2 = (lane + 64 < qn) ? q[lane + 64] : 0u;
-    uint32_t mv3 = (lane + 96 < qn) ? q[lane + 96] : 0u;
-    uint32_t mv4 = (lane + 128 < qn) ? q[lane + 128] : 0u;
-    __syncwarp();
-    if (lane + 32 < qn) q[lane] = mv;
-    if (lane + 64 < qn) q[lane + 32] = mv2;
-    if (lane + 96 < qn) q[lane + 64] = mv3;
-    if (lane + 128 < qn) q[lane + 96] = mv4;
+    queue_shift<QCAP>(q, qn, lane);
     qn -= c;
   }
 #if TF_TIMELINE
