@@ -720,6 +720,179 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
   }
 }
 
+// ------------------------------------------- binary32 tlog, lane pairs
+// The binary32 kernels are issue-bound: every scalar FP32 op costs an issue
+// slot.  This variant of fast_tlog<float> (RENORM / tlogp flavours of the main
+// kernels) runs the whole twofold pipeline -- renorm, seed polynomial, the
+// expm1 core, the Newton step, n ln2, the value part -- on f32x2 pairs
+// (FADD2 / FFMA2: one issue slot for two lanes).  The operation sequence per
+// lane is exactly fast_tlog<float>'s; classification and table indexing stay
+// per lane on the integer pipe.
+TF_DEV TF<f2> pk2(TF<float> a, TF<float> b) { return mk(pk(a.v, b.v), pk(a.e, b.e)); }
+
+// expm1 Taylor core on a lane pair (taylor_expm1_v's packed body)
+TF_DEV TF<f2> taylor_expm1_p(f2 yp) {
+  const f2 nyp = -yp;
+  f2 s = add(yp, splat(5.0f));
+  s = add(mul(s, yp), splat(20.0f));
+  TF<f2> tp = mk(s, splat(0.0f));
+#pragma unroll
+  for (int k = 0; k < 2; ++k) tp = t_add_d_u(t_mul_d_p(tp, yp, nyp), splat(c_texpm1_32[k]));
+  return t_mul_u(t_mul_d_p(tp, yp, nyp), mk(splat(P<float>::INVF_V), splat(P<float>::INVF_E)));
+}
+
+// table-driven seed log1p (seed_log1p_t<float>) on a lane pair
+TF_DEV f2 seed_log1p_p(const STab<float>& tb, f2 a) {
+  constexpr int B = TF32_SEED_BITS, NB = 1 << B;
+  f2 f = add(splat(1.0f), a);
+  f2 clo = sub(a, sub(f, splat(1.0f)));
+  int idx[2];
+  bool small[2];
+  float ax[2] = {lo(a), hi(a)}, fx[2] = {lo(f), hi(f)};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t fb = ubits(fx[h]);
+    int i = (((int)(fb >> 23) - 126) << B) | (int)((fb >> (23 - B)) & (NB - 1u));
+    small[h] = ahi(ax[h]) < 0x3b800000u;                 // |a| < 2^-8
+    idx[h] = small[h] ? NB : min(max(i, 0), 2 * NB);
+  }
+  const float2 t0 = tb.SEED[idx[0]], t1 = tb.SEED[idx[1]];
+  const f2 ic = pk(t0.x, t1.x);
+  f2 r = fmaop(f, ic, splat(-1.0f));
+  r = pk(small[0] ? ax[0] : lo(r), small[1] ? ax[1] : hi(r));
+  f2 q = mul(r, r);                                       // seed_poly<float>
+  f2 pp = fmaop(r, splat(-0.25f), splat(0x1.555556p-2f));
+  pp = fmaop(r, pp, splat(-0.5f));
+  pp = fmaop(q, pp, r);
+  const f2 lc = pk(small[0] ? 0.0f : t0.y, small[1] ? 0.0f : t1.y);
+  const f2 cl = pk(small[0] ? 0.0f : lo(clo), small[1] ? 0.0f : hi(clo));
+  return add(lc, fmaop(cl, ic, pp));
+}
+
+template <int VW, bool RENORM>
+TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const float (&y1i)[VW],
+                        float (&z0)[VW], float (&z1)[VW], bool (&ok)[VW]) {
+  static_assert(VW % 2 == 0, "lane pairs");
+  constexpr int NP = VW / 2;
+  using C = LogC<float>;
+  float y0[VW], y1[VW], r0[VW], dl[VW];
+  int n[VW];
+  unsigned near = 0;
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    ok[e] = C::eb(y0i[e]) - 1u < C::NORM_SPAN && is_finite(y1i[e]);
+    y0[e] = ok[e] ? y0i[e] : 1.0f;
+    y1[e] = ok[e] ? y1i[e] : 0.0f;
+  }
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const int a = 2 * p, b = 2 * p + 1;
+    TF<f2> v = mk(pk(y0[a], y0[b]), pk(y1[a], y1[b]));
+    if (RENORM) v = renorm_u(v);
+    // per-lane classification and frexp on the integer pipe
+    float vv[2] = {lo(v.v), hi(v.v)}, ve[2] = {lo(v.e), hi(v.e)};
+    float c0[2], p2[2];
+    bool zero1[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = 2 * p + h;
+      ok[e] = ok[e] && C::eb(vv[h]) - 1u < C::NORM_SPAN;
+      if (!ok[e]) { vv[h] = 1.0f; ve[h] = 0.0f; }
+      uint32_t vb = ubits(vv[h]);
+      bool band = vb >= C::HALF && vb <= C::TWO;
+      n[e] = band ? 0 : C::n_of(vv[h]);
+      c0[h] = band ? vv[h] : C::mant(vv[h]);
+      p2[h] = band ? 1.0f : C::p2n(-n[e]);            // band: v.e * 1 == v.e exactly
+      zero1[h] = !band && zbits(ve[h]);
+    }
+    const f2 zc0 = pk(c0[0], c0[1]);
+    f2 zc1 = mul(pk(ve[0], ve[1]), pk(p2[0], p2[1]));     // v.e * 2^-n
+    zc1 = pk(zero1[0] ? 0.0f : lo(zc1), zero1[1] ? 0.0f : hi(zc1));
+    const f2 rs = seed_log1p_p(tb, add(sub(zc0, splat(1.0f)), zc1));   // explog.py:196-199
+    float rr[2] = {lo(rs), hi(rs)};
+    float mr[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = 2 * p + h;
+      r0[e] = rr[h];
+      ok[e] = ok[e] && C::in_ln2(rr[h]);
+      mr[h] = ok[e] ? -rr[h] : 0.0f;                     // keeps the CM1 index in range
+    }
+    // s = pexpm10_raw(-r0), in-band branch (expcore.py:142-146)
+    const f2 mx = pk(mr[0], mr[1]);
+    const f2 tq = fmaop(mx, splat(128.0f), splat(12582912.0f));
+    const int n0 = (int)ubits(lo(tq)) - 0x4b400000, n1 = (int)ubits(hi(tq)) - 0x4b400000;
+    const f2 ym = fmaop(sub(tq, splat(12582912.0f)), splat(-0.0078125f), mx);
+    const TF<f2> tt = taylor_expm1_p(ym);
+    const TF<f2> cm = pk2(tv<float>(tb.CM1[n0 - P<float>::CM1_LO]),
+                          tv<float>(tb.CM1[n1 - P<float>::CM1_LO]));
+    const TF<f2> s = t_add_u(t_mul_u(cm, tt), t_add_u(cm, tt));
+    // Newton step (_newton_log_z, explog.py:170-186)
+    const TF<f2> w = fast_two_sum_u(sub(zc0, splat(1.0f)), zc1);
+    const TF<f2> u = t_add_u(t_mul_u(mk(zc0, zc1), s), w);
+    const f2 r1 = add(u.v, u.e);
+    const f2 r0p = pk(r0[2 * p], r0[2 * p + 1]);
+    // newton_quiet on the FP pipe: |r1| < 2^-21 max(|r0|, 1) (exact scaling)
+    const f2 lim = mul(pk(fmaxf(fabsf(r0[2 * p]), 1.0f), fmaxf(fabsf(r0[2 * p + 1]), 1.0f)),
+                       splat(0x1p-21f));
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      ok[2 * p + h] = ok[2 * p + h] && fabsf(h ? hi(r1) : lo(r1)) < (h ? hi(lim) : lo(lim));
+    const TF<f2> nl = t_mul_d_u(mk(splat(P<float>::LN2_V), splat(P<float>::LN2_E)),
+                                pk((float)n[2 * p], (float)n[2 * p + 1]));
+    const TF<f2> core = t_add_u(mk(r0p, r1), nl);
+    // value part: log(y0) = core - d, d = y1 2^-n / zc0
+    const f2 rc = pk(C::rcp(c0[0]), C::rcp(c0[1]));
+    const f2 d0 = mul(mul(pk(y1[2 * p], y1[2 * p + 1]), pk(p2[0], p2[1])), rc);
+    const f2 lz = sub(core.e, d0);
+    const f2 zs = add(core.v, lz);                          // rn_guard, packed sums
+    const f2 rho = add(sub(core.v, zs), lz);
+    float zx[2] = {lo(zs), hi(zs)}, rx[2] = {lo(rho), hi(rho)}, dx[2] = {lo(d0), hi(d0)};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = 2 * p + h;
+      ok[e] = ok[e] && ahi(dx[h]) < C::DMAX;
+      // rn_guard<-32> for a normal z >= 2^-102 (the log values here): half an
+      // ulp is 2^(e(z) - 24), one integer op on the exponent field
+      const float z = zx[h];
+      const float half = __int_as_float((ubits(z) & 0x7f800000u) - (24u << 23));
+      const float tol = 0x1p-32f * fabsf(z);
+      const bool pow2 = (ubits(z) & 0x7fffffu) == 0u;
+      const bool hard = fabsf(fabsf(rx[h]) - half) <= tol ||
+                        (pow2 && fabsf(fabsf(rx[h]) - 0.5f * half) <= tol);
+      z0[e] = z;
+      dl[e] = sub(y0[e], 1.0f);
+      if (ahi(dl[e]) < C::NEAR1H) near |= 1u << e;
+      else ok[e] = ok[e] && !hard;
+    }
+    // z1 = core.e + (core.v - z0) (_correct, explog.py:222-223), after near-1 fix-ups
+    z1[2 * p] = lo(core.v);
+    z1[2 * p + 1] = hi(core.v);
+    y1[2 * p] = lo(core.e);
+    y1[2 * p + 1] = hi(core.e);
+  }
+  while (near) {
+    float d = dl[0];
+#pragma unroll
+    for (int e = VW - 1; e > 0; --e)
+      if (near >> e & 1u) d = dl[e];
+    if (near & 1u) d = dl[0];
+    const unsigned low = near & (0u - near);
+    const float r = log_near1(d);
+#pragma unroll
+    for (int e = 0; e < VW; ++e)
+      if (low == 1u << e) z0[e] = r;
+    near &= near - 1u;
+  }
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const f2 cv = pk(z1[2 * p], z1[2 * p + 1]), ce = pk(y1[2 * p], y1[2 * p + 1]);
+    const f2 r = add(ce, sub(cv, pk(z0[2 * p], z0[2 * p + 1])));
+    z1[2 * p] = lo(r);
+    z1[2 * p + 1] = hi(r);
+  }
+}
+
 // =============================================================== tlog1p
 // _plog1p_raw (explog.py:290-294) with both branches sharing ONE in-band
 // pexpm10 evaluation (the Taylor core is ~3/4 of the work):
@@ -1103,9 +1276,11 @@ TF_DEV void fast_eval(const STab<T>& tb, void* xch, const T (&x0)[VW], const T (
   } else if constexpr (FN == FN_PEXPM10) {
     fast_texpm1<VW, true>(tb, x0, x1, z0, z1, ok);
   } else if constexpr (FN == FN_TLOG || FN == FN_TLOG0) {
-    fast_tlog<T, VW>(tb, x0, x1, z0, z1, ok);
+    if constexpr (sizeof(T) == 4 && VW % 2 == 0) fast_tlog_p<VW, true>(tb, x0, x1, z0, z1, ok);
+    else fast_tlog<T, VW>(tb, x0, x1, z0, z1, ok);
   } else if constexpr (FN == FN_TLOGP) {
-    fast_tlog<T, VW, false>(tb, x0, x1, z0, z1, ok);
+    if constexpr (sizeof(T) == 4 && VW % 2 == 0) fast_tlog_p<VW, false>(tb, x0, x1, z0, z1, ok);
+    else fast_tlog<T, VW, false>(tb, x0, x1, z0, z1, ok);
   } else if constexpr (FN == FN_PLOG0 || FN == FN_PLOG) {
     fast_tlog<T, VW, false, true>(tb, x0, x1, z0, z1, ok);
   } else {
