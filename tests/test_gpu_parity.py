@@ -338,3 +338,33 @@ def test_unaligned_arrays_use_scalar_kernel_same_bits(fn, width, cuda):
                        zb.value.view(torch.int64 if width == 64 else torch.int32))
     assert torch.equal(za.error.view(torch.int64 if width == 64 else torch.int32),
                        zb.error.view(torch.int64 if width == 64 else torch.int32))
+
+
+def test_beyond_2e31_elements_chunked(cuda):
+    """A launch beyond 2^31 elements is split by the host at 2^31 (the kernels
+    use 32-bit indices): binary32 texp over 2^31 + 37 elements (34 GB of
+    arrays), compared with an independent evaluation of the tail and of a
+    window across the chunk boundary."""
+    import torch
+
+    from paper_1502_05216_b200 import _lib, api
+
+    free, _ = torch.cuda.mem_get_info(cuda)
+    n = (1 << 31) + 37
+    if free < 4 * 4 * n + (1 << 30):
+        pytest.skip("not enough device memory")
+    L = _lib.ensure_device(cuda.index)
+    x0 = torch.empty(n, dtype=torch.float32, device=cuda)
+    x1 = torch.empty_like(x0)
+    _lib.check(L.tf_generate(_lib.DIST_CODES["exp32"], 3, 0, n, x0.data_ptr(), x1.data_ptr(),
+                             None), "gen")
+    f = api(32)
+    z = f.texp((x0, x1))
+    torch.cuda.synchronize()
+    for lo_, hi_ in (((1 << 31) - 1000, (1 << 31) + 37), (0, 4096)):
+        w = f.texp((x0[lo_:hi_].clone(), x1[lo_:hi_].clone()))
+        torch.cuda.synchronize()
+        assert torch.equal(z.value[lo_:hi_].view(torch.int32), w.value.view(torch.int32))
+        assert torch.equal(z.error[lo_:hi_].view(torch.int32), w.error.view(torch.int32))
+    del x0, x1, z
+    torch.cuda.empty_cache()
