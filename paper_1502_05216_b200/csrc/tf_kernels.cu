@@ -125,8 +125,13 @@ template <class T, int VW, int BLOCK, bool ASYNC, bool XCH, int STAGES> struct E
   __align__(16) T stg[ASYNC ? STAGES : 1][2][BLOCK][VW];
   Xch<VW> xch[XCH ? WARPS : 1];
 };
+#ifndef TF_BLOCK32_LOG1P
+#define TF_BLOCK32_LOG1P TF_BLOCK
+#endif
 template <class T, int FN, int VW> struct EvalCfg {
-  static constexpr int BLOCK = KCfg<T, VW>::BLOCK;
+  static constexpr int BLOCK =
+      (sizeof(T) == 4 && log1p_fn(FN)) ? TF_BLOCK32_LOG1P : KCfg<T, VW>::BLOCK;
+  static constexpr int MINB = BLOCK == KCfg<T, VW>::BLOCK ? KCfg<T, VW>::MINB : 1;
   static constexpr bool ASYNC = VW * sizeof(T) % 16 == 0;
   static constexpr bool XCH = log1p_fn(FN) && sizeof(T) == 4 && VW >= 2;
   static constexpr bool LOGF = FN == FN_TLOG || FN == FN_TLOG1P || FN == FN_PLOG0 ||
@@ -204,10 +209,10 @@ TF_DEV void queue_shift(uint32_t* q, int qn, int lane) {
 }
 
 template <class T, int FN, int VW>
-__global__ void __launch_bounds__((KCfg<T, VW>::BLOCK), (KCfg<T, VW>::MINB))
+__global__ void __launch_bounds__((EvalCfg<T, FN, VW>::BLOCK), (EvalCfg<T, FN, VW>::MINB))
 k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
        T* __restrict__ z1, uint32_t n, int flags) {
-  constexpr int BLOCK = KCfg<T, VW>::BLOCK;
+  constexpr int BLOCK = EvalCfg<T, FN, VW>::BLOCK;
   constexpr int WARPS = BLOCK / 32;
   constexpr int QCAP = 32 + 32 * VW;
 
@@ -570,16 +575,17 @@ int launch_one(const T* x0, const T* x1, T* z0, T* z1, int64_t n, cudaStream_t s
                          (int)SMEM);
     int v = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, tf::k_eval<T, FN, VW>,
-                                                  tf::KCfg<T, VW>::BLOCK, SMEM);
+                                                  tf::EvalCfg<T, FN, VW>::BLOCK, SMEM);
     occ = v > 0 ? v : 1;
   }
   const int64_t CHUNK = (int64_t)1 << 31;  // queue indices are 32-bit
   for (int64_t off = 0; off < n; off += CHUNK) {
     int64_t m = n - off < CHUNK ? n - off : CHUNK;
-    int64_t vecs = (m / VW + tf::KCfg<T, VW>::BLOCK - 1) / tf::KCfg<T, VW>::BLOCK;
+    constexpr int BLK = tf::EvalCfg<T, FN, VW>::BLOCK;
+    int64_t vecs = (m / VW + BLK - 1) / BLK;
     int64_t grid = (int64_t)device_sms() * occ;
     if (vecs < grid) grid = vecs > 0 ? vecs : 1;
-    tf::k_eval<T, FN, VW><<<(unsigned)grid, tf::KCfg<T, VW>::BLOCK, SMEM, s>>>(
+    tf::k_eval<T, FN, VW><<<(unsigned)grid, BLK, SMEM, s>>>(
         x0 + off, x1 + off, z0 + off, z1 + off, (uint32_t)m, flags);
   }
   return cuda_check("k_eval launch");
