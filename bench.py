@@ -13,8 +13,9 @@ of inputs per step exceed the 126 MB L2, so no flush is needed.
            events on the launching stream, max over ranks;
   e2e    = the same metric through the public API with pinned HOST buffers
            (H2D + kernels + D2H inside the timed region, wall clock);
-  per_function = every (function, width) kernel at its own config (2^24
-           binary64 / 2^26 binary32 elements), same timing rules;
+  per_function = every (function, width) kernel at its own config and size
+           (2^24 / 2^26 binary64, 2^28 binary32; config 1 at 2^26, its 2^20
+           launch-overhead regime separately as cfg1_small), same timing rules;
   roofline = the dominant kernel's algorithmic FP64 op rate vs the measured
            FP64 FMA-pipe peak of this GPU (tf_fma_peak), plus its HBM rate;
   cpu_baseline = the CPU oracle (C port of the reference algorithm, all host
@@ -56,7 +57,9 @@ EFT_ARRAYS_IN = {"fast_two_sum": 2, "two_sum": 2, "two_diff": 2, "two_prod": 2, 
                  "t_mul_d": 3, "t_div": 4, "t_sqrt": 2}
 EFT_BACKEND_OPS = ("two_prod", "t_mul", "t_mul_d", "t_div", "t_sqrt")
 N_HEAD = 1 << 24
-N_FN = {64: 1 << 24, 32: 1 << 26}
+# per-function sizes: each config's own N (BASELINE.json), except config 1's
+# 2^20 (the launch-overhead regime, measured separately as cfg1_small)
+N_CFG = {"cfg1_texp_f64": 1 << 26}
 SEED = 2024
 
 
@@ -280,7 +283,7 @@ def run_ours(args):
     if not args.headline_only:
         for (fn, width), cfg in PER_FN.items():
             _, _, dname, _ = workloads.CONFIGS[cfg]
-            m = N_FN[width]
+            m = N_CFG.get(cfg, workloads.CONFIGS[cfg][3])
             dt = torch.float64 if width == 64 else torch.float32
             a0, a1 = gen(dname, m, dt, rank * m)
             z0, z1 = torch.empty_like(a0), torch.empty_like(a1)

@@ -345,11 +345,13 @@ TF_DEV bool newton_quiet(float r1, float r0) {
 // (probability ~2^-9 ulp-relative, i.e. ~1e-5 of elements) so the exact path,
 // which rounds a binary64 core, decides it.  Exact powers of two are flagged
 // by the quarter-ulp boundary below them as well.
+// Every caller's z is a normal binary32 above 2^-102 (exp in band, expm1
+// beyond ln 2, logarithms away from their tiny-argument shortcuts), so half an
+// ulp is 2^(e(z) - 24): one integer op on the exponent field.
 template <int TOL = -32> TF_DEV float rn_guard(float h, float l, bool& hard) {
   float z = add(h, l);
   float rho = add(sub(h, z), l);                    // (h + l) - z
-  int ez = bexp(z);
-  float half = __int_as_float(max(ez - 24, 1) << 23);   // ulp(z) / 2
+  float half = __int_as_float((ubits(z) & 0x7f800000u) - (24u << 23));   // ulp(z) / 2
   float tol = __int_as_float((127 + TOL) << 23) * fabsf(z);
   bool pow2 = (ubits(z) & 0x7fffffu) == 0u;
   hard = fabsf(fabsf(rho) - half) <= tol || (pow2 && fabsf(fabsf(rho) - 0.5f * half) <= tol);
