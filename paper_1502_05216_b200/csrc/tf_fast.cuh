@@ -688,6 +688,10 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     // y1 * 2^-n over zc0 (= v0 * 2^-n, within an ulp of y0 * 2^-n).
     T d0 = mul(mul(y1[e], p2s(-n[e])), C::rcp(zc0[e]));
     ok[e] = ok[e] && ahi(d0) < C::DMAX;
+    // binary64: d carries the reciprocal's 2^-40 relative error, which must
+    // stay ~2^-30 below an ulp of log(y0): |d| <= 2^-42 |core| away from the
+    // near-1 series (only |log y0| < ~2^-11 is sent away)
+    const bool dsmall = sizeof(T) == 4 || ahi(d0) + (42u << 20) <= ahi(core.v);
     bool hard;
     dl[e] = sub(y0[e], T(1));                         // exact near 1
     if constexpr (DBLV && sizeof(T) == 4) {
@@ -696,7 +700,7 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     } else {
       z0[e] = rn_guard(core.v, sub(core.e, d0), hard);
       if (ahi(dl[e]) < C::NEAR1H) near |= 1u << e;
-      else ok[e] = ok[e] && !hard;
+      else ok[e] = ok[e] && !hard && dsmall;
     }
     cv[e] = core.v;
     ce[e] = core.e;

@@ -368,3 +368,31 @@ def test_beyond_2e31_elements_chunked(cuda):
         assert torch.equal(z.error[lo_:hi_].view(torch.int32), w.error.view(torch.int32))
     del x0, x1, z
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("fn", ("tlog", "tlogp", "tlog1p"))
+def test_near_one_shell_fast_equals_exact(fn, cuda):
+    """binary64 arguments just outside the near-1 series (|y - 1| in
+    [2^-20, 2^-8]; for tlog1p |y| in that range), where log(y) is small and
+    the value-part correction d = y1/y0 must be accurate to far below an ulp:
+    fast kernel == exact path bitwise on 2^22 elements."""
+    import torch
+
+    from paper_1502_05216_b200 import _lib, api
+
+    g = torch.Generator(device=cuda).manual_seed(5)
+    n = 1 << 22
+    k = torch.randint(8, 21, (n,), device=cuda, generator=g).to(torch.float64)
+    s = (torch.rand(n, dtype=torch.float64, device=cuda, generator=g) + 1.0) * \
+        torch.where(torch.rand(n, device=cuda, generator=g) < 0.5, -1.0, 1.0).to(torch.float64)
+    d = s * torch.exp2(-k)
+    x0 = d if fn == "tlog1p" else 1.0 + d
+    x1 = x0 * (torch.rand(n, dtype=torch.float64, device=cuda, generator=g) * 2 - 1) * 2.0 ** -53
+    lib = api(64)
+    a = lib._device(fn, x0, x1)
+    b = lib._device(fn, x0, x1, flags=_lib.FLAG_FORCE_EXACT)
+    torch.cuda.synchronize()
+    bad = (a.value.view(torch.int64) != b.value.view(torch.int64)) | \
+          (a.error.view(torch.int64) != b.error.view(torch.int64))
+    idx = torch.nonzero(bad).flatten()[:5].tolist()
+    assert not bad.any(), [(float(x0[i]).hex(), float(x1[i]).hex()) for i in idx]
