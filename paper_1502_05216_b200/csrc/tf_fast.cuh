@@ -923,8 +923,10 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
   constexpr bool D = sizeof(T) == 8;
   constexpr bool UNIFIED = UNI < 0 ? !D : UNI > 0;
   // out-of-band value part: log1p(d) = d - d^2/2 to the lane's precision needs
-  // |d| = |y1 / (1 + y0)| <= 2^-13 (binary32) / 2^-36 (binary64)
-  constexpr int DSEP = D ? 37 : 14;
+  // |d| = |y1 / (1 + y0)| <= 2^-13 (binary32); binary64 also needs the
+  // reciprocal's 2^-40 error in d far below an ulp: |d| <= 2^-51 (coupled
+  // arguments have |d| <= 2^-53)
+  constexpr int DSEP = D ? 52 : 14;
   using C = LogC<T>;
   T y0[VW], y1[VW], sd[VW], ms[VW], zc0[VW], zc1[VW];
   T wv[DBLV ? VW : 1];
