@@ -28,6 +28,7 @@ from paper_1502_05216_b200.explog import COUPLED_ARG
 pytestmark = pytest.mark.gpu
 
 WIDTHS = (64, 32)
+FNS_INDEX = {name: i for i, name in enumerate(ALL_FNS)}
 
 
 def _run(fn, width, x0, x1, dev, flags=0):
@@ -396,3 +397,50 @@ def test_near_one_shell_fast_equals_exact(fn, cuda):
           (a.error.view(torch.int64) != b.error.view(torch.int64))
     idx = torch.nonzero(bad).flatten()[:5].tolist()
     assert not bad.any(), [(float(x0[i]).hex(), float(x1[i]).hex()) for i in idx]
+
+
+@pytest.mark.parametrize("width", WIDTHS)
+@pytest.mark.parametrize("fn", ALL_FNS)
+def test_random_bit_patterns(fn, width, cuda):
+    """Fuzz: x0 and x1 drawn as raw bit patterns (every class: NaN payloads,
+    infinities, zeros, subnormals, huge and tiny normals), mixed with
+    exponent-local patterns near the functions' band edges.  The fast kernel
+    must equal the exact path bitwise and agree with the CR-sim oracle's
+    classes and tolerance."""
+    import torch
+
+    from paper_1502_05216_b200 import _lib, api
+
+    rng = np.random.default_rng(1000 + width + FNS_INDEX.get(fn, 0))
+    n = 1 << 14
+    u = np.uint64 if width == 64 else np.uint32
+    raw0 = rng.integers(0, np.iinfo(u).max, n, dtype=u, endpoint=True)
+    raw1 = rng.integers(0, np.iinfo(u).max, n, dtype=u, endpoint=True)
+    dt = np.float64 if width == 64 else np.float32
+    x0 = raw0.view(dt).copy()
+    x1 = raw1.view(dt).copy()
+    # half the elements: moderate x0 with a coupled or zero tail
+    m = n // 2
+    mant = rng.uniform(1.0, 2.0, m) * np.where(rng.random(m) < 0.5, -1.0, 1.0)
+    ex = rng.integers(-30, 11, m)
+    x0[:m] = (mant * np.exp2(ex)).astype(dt)
+    x1[:m] = np.where(rng.random(m) < 0.3, 0.0,
+                      x0[:m].astype(np.float64) * rng.uniform(-1, 1, m) *
+                      2.0 ** -(53 if width == 64 else 24)).astype(dt)
+    if fn.endswith("0"):
+        x1[:] = 0
+    lib = api(width)
+    t0 = torch.from_numpy(x0).to(cuda)
+    t1 = torch.from_numpy(x1).to(cuda)
+    a = lib._device(fn, t0, t0 if fn.endswith("0") else t1)
+    b = lib._device(fn, t0, t0 if fn.endswith("0") else t1, flags=_lib.FLAG_FORCE_EXACT)
+    torch.cuda.synchronize()
+    a0, a1, b0, b1 = (v.cpu().numpy() for v in (a.value, a.error, b.value, b.error))
+    same = lambda p, q: (p.view(u) == q.view(u)) | (np.isnan(p) & np.isnan(q))  # noqa: E731
+    bad = ~(same(a0, b0) & same(a1, b1))
+    assert not bad.any(), [(float(x0[i]), float(x1[i])) for i in np.nonzero(bad)[0][:5]]
+    r = compare(a0, a1, *_crsim(fn, width, x0, x1, "fma"), width)
+    keep = coupled_mask(x0, x1) if fn in COUPLED_ARG else np.ones(n, bool)
+    rk = compare(a0[keep], a1[keep], *[v[keep] for v in _crsim(fn, width, x0, x1, "fma")], width)
+    assert r["class_mismatch"] == 0, r
+    assert rk["tol_violations"] == 0, rk
