@@ -10,7 +10,9 @@ the shard-invariant generator (rank r of G owns global elements
 of inputs per step exceed the 126 MB L2, so no flush is needed.
 
   value  = elements evaluated per second, whole job (sum over ranks), CUDA
-           events on the launching stream, max over ranks;
+           events on the launching stream, max over ranks; the step's two
+           independent functions run on two streams (--streams 2), so one
+           launch's tail overlaps the next one's ramp;
   e2e    = the same metric through the public API with pinned HOST buffers
            (H2D + kernels + D2H inside the timed region, wall clock);
   per_function = every (function, width) kernel at its own config and size
@@ -226,15 +228,30 @@ def run_ours(args):
                     torch.empty(n, dtype=torch.float64, device=dev))
     torch.cuda.synchronize()
 
+    # The step's two functions are independent: with --streams 2 the second
+    # runs on its own stream, so its CTAs take each SM as soon as the first
+    # kernel's CTA there retires (the two launches' ramp and tail overlap).
+    streams = [stream] + [torch.cuda.Stream(dev) for _ in range(args.streams - 1)]
+
     def step(evs=None):
+        if len(streams) > 1:
+            go = torch.cuda.Event()
+            go.record(stream)
+            for s in streams[1:]:
+                s.wait_event(go)
         for k, (fn, _) in enumerate(HEADLINE):
+            st = streams[k % len(streams)]
             if evs is not None:
-                evs[k][0].record(stream)
+                evs[k][0].record(st)
             a0, a1 = ins[fn]
             z0, z1 = outs[fn]
-            f64._launch(fn, a0, a1, z0, z1, n, sp)
+            f64._launch(fn, a0, a1, z0, z1, n, st.cuda_stream)
             if evs is not None:
-                evs[k][1].record(stream)
+                evs[k][1].record(st)
+        for s in streams[1:]:
+            done = torch.cuda.Event()
+            done.record(s)
+            stream.wait_event(done)
 
     for _ in range(args.warmup):
         step()
@@ -255,8 +272,16 @@ def run_ours(args):
     ms_total = max_over_ranks(t0.elapsed_time(t1))
     ms_step = ms_total / args.steps
     value = 2 * n * world / (ms_step * 1e-3)
-    kern_ms = {fn: statistics.mean(launch_ev[s][k][0].elapsed_time(launch_ev[s][k][1])
-                                   for s in range(args.steps))
+    if len(streams) > 1:
+        # overlapped launches stretch each other's events: the per-kernel
+        # durations (roofline) come from the same steps run serialised
+        streams[1:] = []
+        torch.cuda.synchronize()
+        for s in range(args.steps):
+            step(launch_ev[s])
+        torch.cuda.synchronize()
+    kern_ms = {fn: max_over_ranks(statistics.mean(
+                   launch_ev[s][k][0].elapsed_time(launch_ev[s][k][1]) for s in range(args.steps)))
                for k, (fn, _) in enumerate(HEADLINE)}
 
     # ---- FP64 / FP32 FMA-pipe peak of this GPU (roofline denominator)
@@ -453,7 +478,9 @@ def run_ours(args):
             "config": {"workload": "cfg2: texpm1 + tlog1p over float64 twofolds",
                        "elements_per_function_per_gpu": n, "global_elements_per_step": 2 * n * world,
                        "parallelism": f"contiguous shards x{world}, no collective on the hot path",
-                       "l2": "inputs 512 MiB/step > 126 MB L2 (no flush needed)"},
+                       "l2": "inputs 512 MiB/step > 126 MB L2 (no flush needed)",
+                       "streams": args.streams,
+                       "kernel_ms": "per-kernel launch durations from the same steps run on one stream"},
             "gpu_launches": len(HEADLINE) * args.steps,
             "kernel_ms": kern_ms,
             "clocks": clk.summary(),
@@ -536,6 +563,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-siblings", action="store_true")
     ap.add_argument("--no-eft", action="store_true")
+    ap.add_argument("--streams", type=int, default=2, choices=(1, 2),
+                    help="run the step's two functions on 1 or 2 streams")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
