@@ -335,8 +335,9 @@ TF_DEV bool newton_quiet(double r1, double r0) {
   return e1 + 22 <= max(e0, 1023);
 }
 TF_DEV bool newton_quiet(float r1, float r0) {
-  int e1 = bexp(r1), e0 = bexp(r0);
-  return e1 + 22 <= max(e0, 127);
+  // on the FP pipe (the binary32 kernels are ALU-bound): |r1| < 2^-21 max(|r0|, 1),
+  // which implies the reference's |r1| <= 2^-20 (|r0| + 1) with a factor 2 to spare
+  return fabsf(r1) < 0x1p-21f * fmaxf(fabsf(r0), 1.0f);
 }
 
 // binary32 value part RN(h + l) from a twofold core that is only accurate to
@@ -759,7 +760,7 @@ TF_DEV f2 seed_log1p_p(const STab<float>& tb, f2 a) {
   for (int h = 0; h < 2; ++h) {
     uint32_t fb = ubits(fx[h]);
     int i = (((int)(fb >> 23) - 126) << B) | (int)((fb >> (23 - B)) & (NB - 1u));
-    small[h] = ahi(ax[h]) < 0x3b800000u;                 // |a| < 2^-8
+    small[h] = fabsf(ax[h]) < 0x1p-8f;                    // |a| < 2^-8 (FP pipe)
     idx[h] = small[h] ? NB : min(max(i, 0), 2 * NB);
   }
   const float2 t0 = tb.SEED[idx[0]], t1 = tb.SEED[idx[1]];
@@ -786,7 +787,9 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
   unsigned near = 0;
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    ok[e] = C::eb(y0i[e]) - 1u < C::NORM_SPAN && is_finite(y1i[e]);
+    // classification on the FP pipe (FSETP) where an integer test would load
+    // the ALU pipe, the binding one in this kernel: positive normal y0, finite y1
+    ok[e] = y0i[e] >= 0x1p-126f && y0i[e] <= 0x1.fffffep127f && fabsf(y1i[e]) <= 0x1.fffffep127f;
     y0[e] = ok[e] ? y0i[e] : 1.0f;
     y1[e] = ok[e] ? y1i[e] : 0.0f;
   }
@@ -802,14 +805,13 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = 2 * p + h;
-      ok[e] = ok[e] && C::eb(vv[h]) - 1u < C::NORM_SPAN;
+      ok[e] = ok[e] && vv[h] >= 0x1p-126f && vv[h] <= 0x1.fffffep127f;
       if (!ok[e]) { vv[h] = 1.0f; ve[h] = 0.0f; }
-      uint32_t vb = ubits(vv[h]);
-      bool band = vb >= C::HALF && vb <= C::TWO;
+      bool band = vv[h] >= 0.5f && vv[h] <= 2.0f;
       n[e] = band ? 0 : C::n_of(vv[h]);
       c0[h] = band ? vv[h] : C::mant(vv[h]);
       p2[h] = band ? 1.0f : C::p2n(-n[e]);            // band: v.e * 1 == v.e exactly
-      zero1[h] = !band && zbits(ve[h]);
+      zero1[h] = !band && ve[h] == 0.0f;
     }
     const f2 zc0 = pk(c0[0], c0[1]);
     f2 zc1 = mul(pk(ve[0], ve[1]), pk(p2[0], p2[1]));     // v.e * 2^-n
@@ -821,7 +823,7 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
     for (int h = 0; h < 2; ++h) {
       const int e = 2 * p + h;
       r0[e] = rr[h];
-      ok[e] = ok[e] && C::in_ln2(rr[h]);
+      ok[e] = ok[e] && fabsf(rr[h]) <= P<float>::LN2_V;
       mr[h] = ok[e] ? -rr[h] : 0.0f;                     // keeps the CM1 index in range
     }
     // s = pexpm10_raw(-r0), in-band branch (expcore.py:142-146)
@@ -857,7 +859,7 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = 2 * p + h;
-      ok[e] = ok[e] && ahi(dx[h]) < C::DMAX;
+      ok[e] = ok[e] && fabsf(dx[h]) < 0x1p-21f;             // C::DMAX
       // rn_guard<-32> for a normal z >= 2^-102 (the log values here): half an
       // ulp is 2^(e(z) - 24), one integer op on the exponent field
       const float z = zx[h];
@@ -868,7 +870,7 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
                         (pow2 && fabsf(fabsf(rx[h]) - 0.5f * half) <= tol);
       z0[e] = z;
       dl[e] = sub(y0[e], 1.0f);
-      if (ahi(dl[e]) < C::NEAR1H) near |= 1u << e;
+      if (fabsf(dl[e]) <= 0x1p-7f) near |= 1u << e;          // C::NEAR1H
       else ok[e] = ok[e] && !hard;
     }
     // z1 = core.e + (core.v - z0) (_correct, explog.py:222-223), after near-1 fix-ups
