@@ -938,7 +938,8 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
     // finite inputs; the size of y1 is checked where it matters, on d below
-    ok[e] = is_finite(y0i[e]) && is_finite(y1i[e]);
+    if constexpr (D) ok[e] = is_finite(y0i[e]) && is_finite(y1i[e]);
+    else ok[e] = fabsf(y0i[e]) <= 0x1.fffffep127f && fabsf(y1i[e]) <= 0x1.fffffep127f;
     y0[e] = ok[e] ? y0i[e] : T(0);
     y1[e] = ok[e] ? y1i[e] : T(0);
     v[e] = RENORM ? renorm_u(mk(y0[e], y1[e])) : mk(y0[e], y1[e]);
@@ -948,20 +949,23 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
     // stays below LN2 whatever the seed's last bit) and sends the rest away.
     if (D && !UNIFIED) inb[e] = ahi(v[e].v) < (sgn(v[e].v) ? H64_HALF : H64_ONE);
     else if (D) inb[e] = abits(v[e].v) <= (sgn(v[e].v) ? B64_HALF : B64_ONE);
-    else inb[e] = ahi(v[e].v) <= (sgn(v[e].v) ? B32_HALF : B32_ONE);
+    else inb[e] = v[e].v >= -0.5f && v[e].v <= 1.0f;     // FP pipe (binary32 is ALU-bound)
     T arg = v[e].v;
     n[e] = 0;
     zc0[e] = T(1);
     zc1[e] = T(0);
     if (UNIFIED && !inb[e]) {
       // out-of-band prologue; v0 > -1 keeps w0 = 1 + v0 positive and normal
-      ok[e] = ok[e] && (inb[e] || !sgn(v[e].v) || ahi(v[e].v) < (D ? H64_ONE : B32_ONE));
+      if constexpr (D) ok[e] = ok[e] && (inb[e] || !sgn(v[e].v) || ahi(v[e].v) < H64_ONE);
+      else ok[e] = ok[e] && (inb[e] || v[e].v > -1.0f);
       TF<T> w = renorm_u(t_add_d_u(v[e], T(1)));
       if constexpr (DBLV) wv[e] = w.v;
       // |d| = |y1 / (1 + y0)| <= ~2^-13 so log1p(d) = d - d^2/2 suffices below
-      ok[e] = ok[e] && (inb[e] || zbits(y1[e]) || bexp(y1[e]) + DSEP <= bexp(w.v));
-      auto wb = ubits(w.v);
-      bool band = wb >= C::HALF && wb <= C::TWO;
+      if constexpr (D) ok[e] = ok[e] && (inb[e] || zbits(y1[e]) || bexp(y1[e]) + DSEP <= bexp(w.v));
+      else ok[e] = ok[e] && (inb[e] || fabsf(y1[e]) * 0x1p14f <= fabsf(w.v));  // stricter
+      bool band;
+      if constexpr (D) band = ubits(w.v) >= C::HALF && ubits(w.v) <= C::TWO;
+      else band = w.v >= 0.5f && w.v <= 2.0f;
       int nn = band ? 0 : C::n_of(w.v);
       T c0 = band ? w.v : C::mant(w.v);
       T c1 = band ? w.e : (zbits(w.e) ? T(0) : mul(w.e, C::p2(-nn)));
@@ -979,7 +983,8 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
     // pexpm10_raw(-sd) must take its in-band branch (|sd| <= LN2); in band this
     // can fail only at v0 = -1/2 or 1 with a seed one ulp beyond ln 2
     if (D && !UNIFIED) ok[e] = ok[e] && (inb[e] || C::in_ln2(sd[e]));
-    else ok[e] = ok[e] && C::in_ln2(sd[e]);
+    else if (D) ok[e] = ok[e] && C::in_ln2(sd[e]);
+    else ok[e] = ok[e] && fabsf(sd[e]) <= T(P<T>::LN2_V);
     ms[e] = -sd[e];
   }
   TF<T> s[VW];
@@ -1003,13 +1008,16 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
         z1[e] = r.e;
         continue;
       }
-      bool tiny = ahi(y0[e]) < (D ? H64_TINY54 : B32_TINY25);
+      bool tiny;
+      if constexpr (D) tiny = ahi(y0[e]) < H64_TINY54;
+      else tiny = fabsf(y0[e]) < 0x1p-25f;
       // v - y0 == y1 exactly; with |d| <= 2^-48 |log1p(y0)| (2^-21 binary32)
       // ~2^-22 accuracy of d suffices; below 2^-54 the value part is y0 itself
       // binary64 needs the refined reciprocal: MUFU alone is 2^-19.9
       // (tools/micro/rcp_acc.cu), which would misround ~1e-6 of the z0
       T d = mul(y1[e], C::rcp(add(T(1), y0[e])));
-      ok[e] = ok[e] && (tiny || ahi(d) + ((uint32_t)(D ? 48 : 21) << (D ? 20 : 23)) <= ahi(sd[e]));
+      if constexpr (D) ok[e] = ok[e] && (tiny || ahi(d) + (48u << 20) <= ahi(sd[e]));
+      else ok[e] = ok[e] && (tiny || fabsf(d) * 0x1p21f <= fabsf(sd[e]));
       bool hard;
       T zz;
       if constexpr (DBLV && !D) zz = cr32_lib<DF_LOG1P>(y0[e], hard);
@@ -1086,10 +1094,10 @@ TF_DEV void tlog1p_sorted(const STab<float>& tb, Xch<VW>* xw, const float (&x0)[
   int pre[VW], nA = 0;
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    bool fin = is_finite(x0[e]) && is_finite(x1[e]);
+    bool fin = fabsf(x0[e]) <= 0x1.fffffep127f && fabsf(x1[e]) <= 0x1.fffffep127f;
     TF<float> v = mk(fin ? x0[e] : 0.0f, fin ? x1[e] : 0.0f);
     if (RENORM) v = renorm_u(v);
-    bool inb = ahi(v.v) <= (sgn(v.v) ? B32_HALF : B32_ONE);
+    bool inb = v.v >= -0.5f && v.v <= 1.0f;
     m[e] = __ballot_sync(0xffffffffu, inb);
     pre[e] = nA;
     nA += __popc(m[e]);
