@@ -428,8 +428,9 @@ TF_DEV void fast_texp(const STab<float>& tb, const float (&x0)[VW], const float 
   int m[VW], n[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    ok[e] = ahi(x0[e]) <= (sgn(x0[e]) ? B32_TEXP_NEG : B32_TEXP_POS) &&
-            ahi(x1[e]) < B32_X1_TINY;
+    // band tests on the FP pipe (the binary32 kernels are ALU-bound)
+    ok[e] = x0[e] >= -__uint_as_float(B32_TEXP_NEG) && x0[e] <= __uint_as_float(B32_TEXP_POS) &&
+            fabsf(x1[e]) < __uint_as_float(B32_X1_TINY);
     decomp_exp_u(ok[e] ? x0[e] : 0.0f, m[e], n[e], y[e]);
   }
   TF<float> t[VW];
@@ -529,9 +530,8 @@ TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const floa
   int m[VW], n[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    uint32_t ax = ahi(x0[e]);
-    ok[e] = ax > B32_LN2 && ax <= (sgn(x0[e]) ? B32_LO : B32_TEXP_POS) &&
-            ahi(x1[e]) < B32_X1_TINY;
+    ok[e] = fabsf(x0[e]) > __uint_as_float(B32_LN2) && x0[e] >= -__uint_as_float(B32_LO) &&
+            x0[e] <= __uint_as_float(B32_TEXP_POS) && fabsf(x1[e]) < __uint_as_float(B32_X1_TINY);
     decomp_exp_u(ok[e] ? x0[e] : 1.0f, m[e], n[e], y[e]);
   }
   TF<float> t[VW];
