@@ -238,7 +238,7 @@ TF_DEV double t1_tiny(double x) {
 TF_DEV float t1_tiny(float x) {
   double d = (double)x;
   double r = fmaop(mul(d, d), fmaop(d, 0x1.5555555555555p-3, 0.5), d);
-  return zbits(x) ? x : __double2float_rn(r);
+  return x == 0.0f ? x : __double2float_rn(r);
 }
 
 TF_DEV double expm1_cr(double x) {
