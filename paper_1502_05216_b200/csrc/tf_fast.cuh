@@ -790,8 +790,10 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
     // classification on the FP pipe (FSETP) where an integer test would load
     // the ALU pipe, the binding one in this kernel: positive normal y0, finite y1
     ok[e] = y0i[e] >= 0x1p-126f && y0i[e] <= 0x1.fffffep127f && fabsf(y1i[e]) <= 0x1.fffffep127f;
-    y0[e] = ok[e] ? y0i[e] : 1.0f;
-    y1[e] = ok[e] ? y1i[e] : 0.0f;
+    // rejected lanes compute on whatever they hold: every table index below is
+    // clamped or derived from a masked value, and their results are discarded
+    y0[e] = y0i[e];
+    y1[e] = y1i[e];
   }
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
@@ -806,7 +808,6 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
     for (int h = 0; h < 2; ++h) {
       const int e = 2 * p + h;
       ok[e] = ok[e] && vv[h] >= 0x1p-126f && vv[h] <= 0x1.fffffep127f;
-      if (!ok[e]) { vv[h] = 1.0f; ve[h] = 0.0f; }
       bool band = vv[h] >= 0.5f && vv[h] <= 2.0f;
       n[e] = band ? 0 : C::n_of(vv[h]);
       c0[h] = band ? vv[h] : C::mant(vv[h]);
