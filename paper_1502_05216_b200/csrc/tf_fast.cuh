@@ -941,8 +941,10 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
     // finite inputs; the size of y1 is checked where it matters, on d below
     if constexpr (D) ok[e] = is_finite(y0i[e]) && is_finite(y1i[e]);
     else ok[e] = fabsf(y0i[e]) <= 0x1.fffffep127f && fabsf(y1i[e]) <= 0x1.fffffep127f;
-    y0[e] = ok[e] ? y0i[e] : T(0);
-    y1[e] = ok[e] ? y1i[e] : T(0);
+    // binary32 (ALU-bound): rejected lanes keep their values; the prologue's
+    // `if (!ok) arg = 0` below keeps every table index in range
+    y0[e] = (D && !ok[e]) ? T(0) : y0i[e];
+    y1[e] = (D && !ok[e]) ? T(0) : y1i[e];
     v[e] = RENORM ? renorm_u(mk(y0[e], y1[e])) : mk(y0[e], y1[e]);
     // in band: -1/2 <= v0 <= 1 (explog.py:291).  The unified branch needs the
     // exact test (v0 = 1 or -1/2 must not go out of band); without it, the
