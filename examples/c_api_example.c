@@ -5,9 +5,9 @@
  *   LD_LIBRARY_PATH=paper_1502_05216_b200/lib /tmp/tf_example
  *
  * It exercises the error conventions of the ABI (status codes plus
- * tf_last_error(), never an abort) and initialises device 0 when one is
- * present.  Evaluating arrays needs device pointers from the caller's own CUDA
- * code: see INTEGRATION.md, "From C/C++". */
+ * tf_last_error(), never an abort) and, when a device is present, evaluates
+ * texp and tlog1p over plain host arrays through tf_eval_host -- the client
+ * needs no CUDA code at all.  Device-pointer use: examples/c_texp_device.c. */
 #include <stdio.h>
 #include <stdint.h>
 #include <string.h>
@@ -28,5 +28,20 @@ int main(void) {
     return 0;
   }
   printf("device 0 initialised\n");
+  /* host arrays (pageable here; pinned memory streams at full PCIe speed) */
+  double x0[4] = {1.0, -2.5, 0.0, 700.0}, x1[4] = {0.0, 1e-17, 0.0, 0.0}, z0[4], z1[4];
+  rc = tf_eval_host(TF_FN_TEXP, 64, x0, x1, z0, z1, 4, 0, NULL, 0);
+  if (rc != TF_OK) {
+    printf("tf_eval_host failed: %d (%s)\n", rc, tf_last_error());
+    return 1;
+  }
+  printf("host texp(1) = %a + %a\n", z0[0], z1[0]);
+  double y0[1] = {1.0}, y1[1] = {0.0};
+  rc = tf_eval_host(TF_FN_TLOG1P, 64, y0, y1, z0, z1, 1, 0, NULL, 0);
+  if (rc != TF_OK) {
+    printf("tf_eval_host failed: %d (%s)\n", rc, tf_last_error());
+    return 1;
+  }
+  printf("host tlog1p(1) = %a + %a\n", z0[0], z1[0]);
   return 0;
 }

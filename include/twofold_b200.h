@@ -110,6 +110,18 @@ TF_API int tf_tlog1p_f32(const float* x0, const float* x1, float* z0, float* z1,
 TF_API int tf_eval(int fn, int width, const void* x0, const void* x1, void* z0, void* z1,
                    int64_t n, void* stream, int flags);
 
+/* Host-buffer evaluation (the reference's own calling convention: api(width)
+ * methods on host numpy arrays, explog.py:333-349).  x0, x1, z0, z1 are HOST
+ * arrays -- pinned (cudaHostAlloc / torch pin_memory) for full PCIe speed,
+ * pageable memory works at the driver's staged rate.  The n elements stream
+ * through a three-stage chunk pipeline on the current device (H2D, kernel,
+ * D2H on three streams over a ring of device buffers) that starts after the
+ * work queued on `stream`; the call returns when z0, z1 hold the results.
+ * chunk = elements per pipeline chunk, 0 = default (2^18).  Dotted functions
+ * take x1 = NULL.  Thread-safe (calls on one device serialise). */
+TF_API int tf_eval_host(int fn, int width, const void* x0, const void* x1, void* z0, void* z1,
+                        int64_t n, int64_t chunk, void* stream, int flags);
+
 /* Shard-invariant synthetic inputs: elements [start, start+n) of distribution
  * `dist` for `seed` (bit-identical to workloads.generate). */
 TF_API int tf_generate(int dist, uint64_t seed, int64_t start, int64_t n, void* x0, void* x1,

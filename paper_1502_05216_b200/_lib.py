@@ -31,7 +31,8 @@ DIST_CODES = {"exp64": 0, "pow10_64": 1, "pow10c_64": 2, "log64": 3, "exp32": 4,
 EXPORTS = ("tf_version", "tf_last_error", "tf_init", "tf_texp_f64", "tf_texpm1_f64",
            "tf_tlog_f64", "tf_tlog1p_f64", "tf_texp_f32", "tf_texpm1_f32", "tf_tlog_f32",
            "tf_tlog1p_f32", "tf_eval", "tf_generate", "tf_compare", "tf_fma_peak",
-           "tf_exact_count", "tf_audit_errors", "tf_etalon", "tf_checksum", "tf_eft")
+           "tf_exact_count", "tf_audit_errors", "tf_etalon", "tf_checksum", "tf_eft",
+           "tf_eval_host")
 # tf_eft op codes (include/twofold_b200.h TF_OP_*)
 OP_CODES = {"fast_two_sum": 0, "two_sum": 1, "two_diff": 2, "two_prod": 3, "split": 4,
             "renorm_fast": 5, "renorm": 6, "t_add": 7, "t_add_d": 8, "t_mul": 9, "t_mul_d": 10,
@@ -95,6 +96,8 @@ def load() -> ctypes.CDLL:
         L.tf_checksum.restype = i32
         L.tf_eft.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, i64, vp]
         L.tf_eft.restype = i32
+        L.tf_eval_host.argtypes = [i32, i32, vp, vp, vp, vp, i64, i64, vp, i32]
+        L.tf_eval_host.restype = i32
         _lib = L
         return L
 

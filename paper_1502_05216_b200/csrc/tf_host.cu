@@ -1,0 +1,143 @@
+// tf_host.cu -- host-buffer entry point of libtwofold_b200.so (tf_eval_host).
+//
+// The reference evaluates host (numpy) arrays (explog.py:333-349 api(width)
+// methods); this entry point takes HOST arrays and streams them through a
+// three-stage chunk pipeline on the device:
+//
+//   copy-in stream   H2D of chunk k into ring slot k % RING
+//   compute stream   tf_eval of chunk k           (waits for its H2D)
+//   copy-out stream  D2H of chunk k's results     (waits for its kernel)
+//
+// A slot is refilled only after its previous copy-out completed.  The copy
+// engines therefore run both PCIe directions at once (measured 55 GB/s H2D,
+// 57 GB/s D2H, 99 GB/s together on the B200 box, tools/pcie_probe.py), while the
+// kernel time per chunk is ~2% of the copy time.
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "tf_abi.h"
+
+using tfabi::cuda_check;
+using tfabi::fail;
+
+namespace {
+
+constexpr int RING = 4;
+constexpr int MAX_DEV = 64;
+// elements per chunk: 8 MiB per binary64 array.  tools/pcie_pattern_probe.py
+// (one call = 2 x 2^24 binary64 in, 2 x 2^24 out, host-synchronised): 2^19
+// pays a per-copy overhead (6.7 ms for copies alone), 2^22 a longer pipeline fill and drain; 2^20 and
+// 2^21 both give 6.4 ms against 5.4 ms for the same bytes as two independent
+// bulk copies.  A geometric ramp of chunk sizes at both ends did not help: the
+// D2H stream trails by one chunk whatever the sizes (both directions run at
+// ~49.5 GB/s together), so the tail is set by the largest chunk.
+constexpr int64_t DEFAULT_CHUNK = 1 << 20;
+
+struct HostPipe {
+  bool ready = false;
+  int64_t cap_bytes = 0;  // bytes per ring buffer
+  cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
+  cudaEvent_t loaded[RING], done[RING], freed[RING], entry;
+  bool used[RING] = {};
+  void* buf[RING][4] = {};
+};
+
+HostPipe g_pipe[MAX_DEV];
+std::mutex g_pipe_mu[MAX_DEV];
+
+bool dotted_fn(int fn) {
+  return fn == TF_FN_PEXP0 || fn == TF_FN_TEXP0 || fn == TF_FN_PEXPM10 || fn == TF_FN_TEXPM10 ||
+         fn == TF_FN_PLOG0 || fn == TF_FN_TLOG0 || fn == TF_FN_PLOG1P0 || fn == TF_FN_TLOG1P0;
+}
+
+int setup(HostPipe& p, int64_t bytes) {
+  if (!p.ready) {
+    if (cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&p.comp, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&p.out, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p.entry, cudaEventDisableTiming) != cudaSuccess)
+      return cuda_check("tf_eval_host: stream/event creation");
+    for (int s = 0; s < RING; ++s)
+      if (cudaEventCreateWithFlags(&p.loaded[s], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&p.done[s], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&p.freed[s], cudaEventDisableTiming) != cudaSuccess)
+        return cuda_check("tf_eval_host: event creation");
+    p.ready = true;
+  }
+  if (bytes > p.cap_bytes) {
+    // the previous call returned only after its copy-out stream drained, so
+    // no ring buffer is in flight here
+    for (int s = 0; s < RING; ++s)
+      for (int a = 0; a < 4; ++a) {
+        if (p.buf[s][a]) cudaFree(p.buf[s][a]);
+        p.buf[s][a] = nullptr;
+      }
+    p.cap_bytes = 0;
+    for (int s = 0; s < RING; ++s)
+      for (int a = 0; a < 4; ++a)
+        if (cudaMalloc(&p.buf[s][a], (size_t)bytes) != cudaSuccess)
+          return cuda_check("tf_eval_host: ring buffer allocation");
+    p.cap_bytes = bytes;
+  }
+  return TF_OK;
+}
+
+}  // namespace
+
+extern "C" TF_API int tf_eval_host(int fn, int width, const void* x0, const void* x1, void* z0,
+                                   void* z1, int64_t n, int64_t chunk, void* stream, int flags) {
+  if (n < 0) return fail(TF_ERR_ARG, "negative element count%s");
+  if (width != 32 && width != 64) return fail(TF_ERR_ARG, "unsupported width (expected 32 or 64)%s");
+  if (fn < 0 || fn >= TF_FN_COUNT) return fail(TF_ERR_ARG, "unknown function code%s");
+  if (chunk < 0) return fail(TF_ERR_ARG, "negative chunk%s");
+  if (n == 0) return TF_OK;
+  const bool dotted = dotted_fn(fn);
+  if (!x0 || (!x1 && !dotted) || !z0 || !z1) return fail(TF_ERR_ARG, "null pointer%s");
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_check("tf_eval_host: cudaGetDevice");
+  if (dev < 0 || dev >= MAX_DEV) return fail(TF_ERR_ARG, "device index out of range%s");
+  const int64_t sz = width / 8;
+  const int64_t c = chunk > 0 ? (chunk < n ? chunk : n) : (DEFAULT_CHUNK < n ? DEFAULT_CHUNK : n);
+  const bool copy_x1 = !dotted || (x1 && x1 != x0);
+
+  std::lock_guard<std::mutex> lk(g_pipe_mu[dev]);
+  HostPipe& p = g_pipe[dev];
+  int rc = setup(p, c * sz);
+  if (rc) return rc;
+  // start after the work already queued on the caller's stream
+  if (cudaEventRecord(p.entry, static_cast<cudaStream_t>(stream)) != cudaSuccess ||
+      cudaStreamWaitEvent(p.in, p.entry, 0) != cudaSuccess)
+    return cuda_check("tf_eval_host: stream ordering");
+  const char* hx0 = static_cast<const char*>(x0);
+  const char* hx1 = static_cast<const char*>(x1);
+  char* hz0 = static_cast<char*>(z0);
+  char* hz1 = static_cast<char*>(z1);
+  int64_t k = 0;
+  for (int64_t off = 0; off < n; off += c, ++k) {
+    const int64_t m = c < n - off ? c : n - off;
+    const size_t bytes = (size_t)(m * sz), at = (size_t)(off * sz);
+    const int s = (int)(k % RING);
+    void *d0 = p.buf[s][0], *d1 = copy_x1 ? p.buf[s][1] : p.buf[s][0];
+    void *e0 = p.buf[s][2], *e1 = p.buf[s][3];
+    if (p.used[s] && cudaStreamWaitEvent(p.in, p.freed[s], 0) != cudaSuccess)
+      return cuda_check("tf_eval_host: ring wait");
+    if (cudaMemcpyAsync(d0, hx0 + at, bytes, cudaMemcpyHostToDevice, p.in) != cudaSuccess ||
+        (copy_x1 && cudaMemcpyAsync(d1, hx1 + at, bytes, cudaMemcpyHostToDevice, p.in) != cudaSuccess) ||
+        cudaEventRecord(p.loaded[s], p.in) != cudaSuccess ||
+        cudaStreamWaitEvent(p.comp, p.loaded[s], 0) != cudaSuccess)
+      return cuda_check("tf_eval_host: copy-in");
+    rc = tf_eval(fn, width, d0, d1, e0, e1, m, p.comp, flags);
+    if (rc) return rc;
+    if (cudaEventRecord(p.done[s], p.comp) != cudaSuccess ||
+        cudaStreamWaitEvent(p.out, p.done[s], 0) != cudaSuccess ||
+        cudaMemcpyAsync(hz0 + at, e0, bytes, cudaMemcpyDeviceToHost, p.out) != cudaSuccess ||
+        cudaMemcpyAsync(hz1 + at, e1, bytes, cudaMemcpyDeviceToHost, p.out) != cudaSuccess ||
+        cudaEventRecord(p.freed[s], p.out) != cudaSuccess)
+      return cuda_check("tf_eval_host: copy-out");
+    p.used[s] = true;
+  }
+  // the results are on the host when the call returns
+  if (cudaStreamSynchronize(p.out) != cudaSuccess) return cuda_check("tf_eval_host: drain");
+  return TF_OK;
+}

@@ -50,7 +50,7 @@ COUPLED_ARG = frozenset(("texpp", "pexp", "texpm1p", "pexpm1", "tlogp", "plog", 
                          "plog1p"))
 TWOFOLD_ARG = frozenset(("texp", "texpm1", "tlog", "tlog1p"))
 
-HOST_CHUNK = 1 << 22  # elements per pipelined host<->device chunk
+HOST_CHUNK = 1 << 20  # elements per pipelined host<->device chunk (tf_eval_host)
 
 
 def family_of(name: str) -> str:
@@ -266,9 +266,10 @@ class ExpLog:
 
 
 def _pipeline(lib: ExpLog, fn: str, h0, h1, device=None, chunk: int = HOST_CHUNK, out=None):
-    """Evaluate host tensors: chunked H2D -> kernel -> D2H on two streams so the
-    copy engines run both directions while the kernels execute.  `out` may
-    supply (pinned) host result tensors; otherwise pinned ones are allocated."""
+    """Evaluate host tensors through tf_eval_host (csrc/tf_host.cu): a three-stage
+    chunk pipeline -- H2D, kernel and D2H on three streams over a ring of device
+    buffers -- so both PCIe directions stay busy at once.  `out` may supply
+    (pinned) host result tensors; otherwise pinned ones are allocated."""
     import torch
 
     if not torch.cuda.is_available():
@@ -277,7 +278,6 @@ def _pipeline(lib: ExpLog, fn: str, h0, h1, device=None, chunk: int = HOST_CHUNK
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     n = h0.numel()
     dotted = fn in DOTTED_ARG
-    pinned = h0.is_pinned() and h1.is_pinned()
     if out is not None:
         z0, z1 = out
     else:
@@ -285,30 +285,19 @@ def _pipeline(lib: ExpLog, fn: str, h0, h1, device=None, chunk: int = HOST_CHUNK
         z1 = torch.empty(n, dtype=h0.dtype, pin_memory=True)
     if n == 0:
         return z0, z1
-    if not pinned:
+    if not h0.is_pinned():
         h0 = h0.pin_memory()
-        h1 = h0 if dotted else h1.pin_memory()
-    c = min(chunk, n)
-    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
-    bufs = [[torch.empty(c, dtype=h0.dtype, device=dev) for _ in range(4)] for _ in range(2)]
-    cur = torch.cuda.current_stream(dev)
-    for s in streams:
-        s.wait_stream(cur)
-    for k, off in enumerate(range(0, n, c)):
-        m = min(c, n - off)
-        s = streams[k & 1]
-        d0, d1, e0, e1 = (b[:m] for b in bufs[k & 1])
-        with torch.cuda.stream(s):
-            d0.copy_(h0[off:off + m], non_blocking=True)
-            if dotted:
-                d1 = d0
-            else:
-                d1.copy_(h1[off:off + m], non_blocking=True)
-            lib._launch(fn, d0, d1, e0, e1, m, s.cuda_stream)
-            z0[off:off + m].copy_(e0, non_blocking=True)
-            z1[off:off + m].copy_(e1, non_blocking=True)
-    for s in streams:
-        s.synchronize()
+    if dotted:
+        h1 = h0
+    elif not h1.is_pinned():
+        h1 = h1.pin_memory()
+    L = _lib.ensure_device(dev.index)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        rc = L.tf_eval_host(_lib.FN_CODES[fn], lib.width, h0.data_ptr(),
+                            None if dotted else h1.data_ptr(), z0.data_ptr(), z1.data_ptr(),
+                            n, chunk, stream, 0)
+    _lib.check(rc, f"tf_eval_host({fn}, width={lib.width})")
     return z0, z1
 
 

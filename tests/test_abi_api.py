@@ -54,6 +54,15 @@ def test_abi_argument_errors_without_gpu():
     assert L.tf_texp_f64(None, None, None, None, 0, None) == 0
     assert L.tf_generate(99, 0, 0, 10, 8, 8, None) == _lib.TF_ERR_ARG
     assert L.tf_exact_count(None, 0) == _lib.TF_ERR_ARG
+    # host-buffer entry point: argument checks precede any CUDA call
+    assert L.tf_eval_host(0, 64, None, None, None, None, 0, 0, None, 0) == 0   # n == 0: no-op
+    assert L.tf_eval_host(0, 64, 8, 8, 8, 8, -1, 0, None, 0) == _lib.TF_ERR_ARG
+    assert L.tf_eval_host(0, 16, 8, 8, 8, 8, 5, 0, None, 0) == _lib.TF_ERR_ARG
+    assert L.tf_eval_host(20, 64, 8, 8, 8, 8, 5, 0, None, 0) == _lib.TF_ERR_ARG
+    assert L.tf_eval_host(0, 64, 8, 8, 8, 8, 5, -4, None, 0) == _lib.TF_ERR_ARG
+    assert b"chunk" in L.tf_last_error()
+    assert L.tf_eval_host(_lib.FN_CODES["tlog"], 64, 8, None, 8, 8, 5, 0, None, 0) == _lib.TF_ERR_ARG
+    assert b"null" in L.tf_last_error()
     with pytest.raises(ValueError):
         _lib.check(-1, "x")
 

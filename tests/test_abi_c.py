@@ -32,6 +32,21 @@ def test_c_client_compiles_links_and_runs(tmp_path):
 
 
 @pytest.mark.gpu
+def test_c_client_host_arrays(tmp_path, cuda):
+    """The same C99 client on a GPU box: tf_eval_host on plain host arrays."""
+    lib = os.path.join(ROOT, "paper_1502_05216_b200", "lib")
+    exe = tmp_path / "tf_example"
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "c_api_example.c"), "-L", lib,
+                    "-ltwofold_b200", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True,
+                         env={**os.environ, "LD_LIBRARY_PATH": lib}, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "host texp(1) = 0x1.5bf0a8b145769p+1" in out.stdout          # RN(e)
+    assert "host tlog1p(1) = 0x1.62e42fefa39efp-1" in out.stdout        # RN(ln 2)
+
+
+@pytest.mark.gpu
 def test_c_client_on_device(tmp_path, cuda):
     lib = os.path.join(ROOT, "paper_1502_05216_b200", "lib")
     exe = tmp_path / "tf_texp"

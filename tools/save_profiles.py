@@ -15,11 +15,16 @@ def last_json(path):
     return json.loads(open(path).read().strip().splitlines()[-1])
 
 
-json.dump(last_json(f"{G}/bench_full.log"), open(f"{P}/{ROUND}_bench.json", "w"), indent=1)
-json.dump(last_json(f"{G}/bench_ref.log"), open(f"{P}/{ROUND}_bench_reference.json", "w"), indent=1)
-lines = [ln for ln in open(f"{G}/launches.csv") if not ln.startswith("==")]
-open(f"{P}/{ROUND}_launches.csv", "w").writelines(lines)
-traffic = {}
+# each part is optional: a capture-only call (tools/ncu_full.sh) has no bench logs
+if os.path.exists(f"{G}/bench_full.log"):
+    json.dump(last_json(f"{G}/bench_full.log"), open(f"{P}/{ROUND}_bench.json", "w"), indent=1)
+if os.path.exists(f"{G}/bench_ref.log"):
+    json.dump(last_json(f"{G}/bench_ref.log"), open(f"{P}/{ROUND}_bench_reference.json", "w"), indent=1)
+if os.path.exists(f"{G}/launches.csv"):
+    lines = [ln for ln in open(f"{G}/launches.csv") if not ln.startswith("==")]
+    open(f"{P}/{ROUND}_launches.csv", "w").writelines(lines)
+TPATH = f"{P}/ncu_traffic.json"
+traffic = json.load(open(TPATH)) if os.path.exists(TPATH) else {}   # merged per capture
 for name in sorted(os.listdir(G)):
     if not (name.startswith("full_") and name.endswith(".ncu-rep")):
         continue
@@ -47,5 +52,5 @@ for name in sorted(os.listdir(G)):
         "algorithmic_bytes": n * (32 if width == "64" else 16),
         "source": f"profiles/{ROUND}_ncu_full_{tag}.txt (ncu --set full)",
         "traffic_bytes": rd + wr}
-json.dump(traffic, open(f"{P}/ncu_traffic.json", "w"), indent=1)
+json.dump(traffic, open(TPATH, "w"), indent=1)
 print("saved", sorted(traffic))
