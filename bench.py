@@ -29,6 +29,7 @@ of inputs per step exceed the 126 MB L2, so no flush is needed.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -385,6 +386,40 @@ def run_ours(args):
                  "graph_launches": reps}
         del a0, a1, z0, z1, g
 
+    # ---- config 5: texp and tlog over 2^30 binary64 twofolds with 1% special
+    # values, sharded contiguously across the ranks (strong scaling: the total is
+    # fixed, each rank evaluates its 2^30 / N slice; no collective on the path)
+    cfg5 = {}
+    if not args.headline_only and not args.no_cfg5:
+        for cname in ("cfg5_texp_f64", "cfg5_tlog_f64"):
+            fn, _, dname, total = workloads.CONFIGS[cname]
+            per = total // world
+            a0, a1 = gen(dname, per, torch.float64, rank * per)
+            z0, z1 = torch.empty_like(a0), torch.empty_like(a0)
+            for _ in range(max(3, args.warmup)):
+                f64._launch(fn, a0, a1, z0, z1, per, sp)
+            reps = max(3, min(args.steps, 10))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            e0.record(stream)
+            for _ in range(reps):
+                f64._launch(fn, a0, a1, z0, z1, per, sp)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = max_over_ranks(e0.elapsed_time(e1) / reps)
+            # share of the slice the exact path evaluated (the specials and the
+            # rare fast-path rejects), counted in one extra launch
+            cnt = ctypes.c_ulonglong(0)
+            _lib.check(L.tf_exact_count(ctypes.byref(cnt), 1), "tf_exact_count")
+            f64._launch(fn, a0, a1, z0, z1, per, sp, flags=2)   # TF_FLAG_COUNT_EXACT
+            torch.cuda.synchronize()
+            _lib.check(L.tf_exact_count(ctypes.byref(cnt), 1), "tf_exact_count")
+            cfg5[cname] = {"elements_total": per * world, "elements_per_rank": per, "ms": ms,
+                           "elements_per_s": per * world / (ms * 1e-3), "scaling": "strong",
+                           "exact_path_fraction_rank0": cnt.value / per}
+            del a0, a1, z0, z1
+        torch.cuda.empty_cache()
+
     # ---- element-wise EFT / twofold arithmetic ops (HBM-bound streaming)
     eft_rates = {}
     if not args.headline_only and not args.no_eft:
@@ -490,7 +525,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "per_function": per_fn,
             "siblings": siblings,
-            "eft_ops": eft_rates,
+            "eft_ops": eft_rates, "cfg5": cfg5,
             "cfg1_small": small,
             "parity_sample": stats,
         }
@@ -560,6 +595,7 @@ def main():
                     help="ncu dram bytes per launch of the dominant kernel (profiles/)")
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the 2^30 config-5 section")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-siblings", action="store_true")
     ap.add_argument("--no-eft", action="store_true")
