@@ -21,9 +21,10 @@
 
 namespace tf {
 
-// binary64 lanes per thread: 4 for the exponential families (512-thread CTAs,
-// 112 registers: +6% texp, +3% texpm1), 2 for the logarithms (1024-thread CTAs;
-// 4 lanes cost them ~2%).  TF_VW64 forces one width for all.
+// binary64 lanes per thread: 4 (512-thread CTAs, up to 128 registers) for
+// every family: +6% texp, +3% texpm1 over 2 lanes in 1024-thread CTAs, and
+// +3% tlog / tlog1p since their near-1 and admission work moved onto the
+// integer pipe (tools/variant_rates.sh).  TF_VW64 forces one width for all.
 #ifndef TF_VW64
 #define TF_VW64 0
 #endif
@@ -31,7 +32,7 @@ namespace tf {
 #define TF_VW64_EXP 4
 #endif
 #ifndef TF_VW64_LOG
-#define TF_VW64_LOG 2
+#define TF_VW64_LOG 4
 #endif
 #ifndef TF_VW32
 #define TF_VW32 4
