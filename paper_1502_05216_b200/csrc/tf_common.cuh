@@ -55,7 +55,9 @@ TF_DEV f2 fmaop(f2 a, f2 b, f2 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.u) : "l"(a.u), "l"(b.u), "l"(c.u));
   return r;
 }
-TF_DEV f2 operator-(f2 a) { a.u ^= 0x8000000080000000ull; return a; }
+// sign flip per half as neg.f32: ptxas folds it into the consuming FFMA2 /
+// FADD2 as an operand modifier (a 64-bit XOR would cost two LOP3s)
+TF_DEV f2 operator-(f2 a) { return pk(-lo(a), -hi(a)); }
 TF_DEV f2 splat(float c) { return pk(c, c); }
 
 // ------------------------------------------------- integer-pipe classifiers

@@ -776,6 +776,45 @@ TF_DEV f2 seed_log1p_p(const STab<float>& tb, f2 a) {
   return add(lc, fmaop(cl, ic, pp));
 }
 
+// pexpm10_raw(mx), in-band branch (expcore.py:142-146), on a lane pair:
+// decompose_expm1 by the magic constant, the packed Taylor core, and the
+// coupled CM1 entry recombination
+TF_DEV TF<f2> pexpm10_inband_p(const STab<float>& tb, f2 mx) {
+  const f2 tq = fmaop(mx, splat(128.0f), splat(12582912.0f));
+  const int n0 = (int)ubits(lo(tq)) - 0x4b400000, n1 = (int)ubits(hi(tq)) - 0x4b400000;
+  const f2 ym = fmaop(sub(tq, splat(12582912.0f)), splat(-0.0078125f), mx);
+  const TF<f2> tt = taylor_expm1_p(ym);
+  const TF<f2> cm = pk2(tv<float>(tb.CM1[n0 - P<float>::CM1_LO]),
+                        tv<float>(tb.CM1[n1 - P<float>::CM1_LO]));
+  return t_add_u(t_mul_u(cm, tt), t_add_u(cm, tt));
+}
+
+// rn_guard<-32> (below) on a lane pair, for values |z| >= 2^-100 (the log
+// families away from their tiny-argument shortcuts): packed sums and one
+// threshold compare per lane.  rho = (h + l) - z is at most half an ulp, so
+// "within 2^-32 |z| of the midpoint" is implied by |rho| >= half (1 - 2^-7)
+// (2^-7 half >= 2^-32 |z|), a superset of rn_guard's test; below an exact
+// power of two the midpoint is half / 2.  The threshold is built on the
+// exponent field: 2^(e-25) * 0x1.fcp0 = half (1 - 2^-7).
+TF_DEV f2 rn_guard_p(f2 h, f2 l, bool (&hard)[2]) {
+  const f2 zs = add(h, l);
+  const f2 rho = add(sub(h, zs), l);
+  const float zx[2] = {lo(zs), hi(zs)}, rx[2] = {lo(rho), hi(rho)};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint32_t zb = ubits(zx[k]);
+    const uint32_t sh = (zb & 0x7fffffu) == 0u ? (26u << 23) : (25u << 23);
+    const float thr = __uint_as_float((zb & 0x7f800000u) - sh + 0x7e0000u);
+    hard[k] = fabsf(rx[k]) >= thr;
+  }
+  return zs;
+}
+
+// per-lane select of two lane pairs: (c0 ? a.lo : b.lo, c1 ? a.hi : b.hi)
+TF_DEV f2 sel2(bool c0, bool c1, f2 a, f2 b) {
+  return pk(c0 ? lo(a) : lo(b), c1 ? hi(a) : hi(b));
+}
+
 template <int VW, bool RENORM>
 TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const float (&y1i)[VW],
                         float (&z0)[VW], float (&z1)[VW], bool (&ok)[VW]) {
@@ -828,14 +867,7 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
       mr[h] = ok[e] ? -rr[h] : 0.0f;                     // keeps the CM1 index in range
     }
     // s = pexpm10_raw(-r0), in-band branch (expcore.py:142-146)
-    const f2 mx = pk(mr[0], mr[1]);
-    const f2 tq = fmaop(mx, splat(128.0f), splat(12582912.0f));
-    const int n0 = (int)ubits(lo(tq)) - 0x4b400000, n1 = (int)ubits(hi(tq)) - 0x4b400000;
-    const f2 ym = fmaop(sub(tq, splat(12582912.0f)), splat(-0.0078125f), mx);
-    const TF<f2> tt = taylor_expm1_p(ym);
-    const TF<f2> cm = pk2(tv<float>(tb.CM1[n0 - P<float>::CM1_LO]),
-                          tv<float>(tb.CM1[n1 - P<float>::CM1_LO]));
-    const TF<f2> s = t_add_u(t_mul_u(cm, tt), t_add_u(cm, tt));
+    const TF<f2> s = pexpm10_inband_p(tb, pk(mr[0], mr[1]));
     // Newton step (_newton_log_z, explog.py:170-186)
     const TF<f2> w = fast_two_sum_u(sub(zc0, splat(1.0f)), zc1);
     const TF<f2> u = t_add_u(t_mul_u(mk(zc0, zc1), s), w);
@@ -853,26 +885,17 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
     // value part: log(y0) = core - d, d = y1 2^-n / zc0
     const f2 rc = pk(C::rcp(c0[0]), C::rcp(c0[1]));
     const f2 d0 = mul(mul(pk(y1[2 * p], y1[2 * p + 1]), pk(p2[0], p2[1])), rc);
-    const f2 lz = sub(core.e, d0);
-    const f2 zs = add(core.v, lz);                          // rn_guard, packed sums
-    const f2 rho = add(sub(core.v, zs), lz);
-    float zx[2] = {lo(zs), hi(zs)}, rx[2] = {lo(rho), hi(rho)}, dx[2] = {lo(d0), hi(d0)};
+    bool hard[2];
+    const f2 zs = rn_guard_p(core.v, sub(core.e, d0), hard);   // |z| >= 2^-8 away from 1
+    float zx[2] = {lo(zs), hi(zs)}, dx[2] = {lo(d0), hi(d0)};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = 2 * p + h;
       ok[e] = ok[e] && fabsf(dx[h]) < 0x1p-21f;             // C::DMAX
-      // rn_guard<-32> for a normal z >= 2^-102 (the log values here): half an
-      // ulp is 2^(e(z) - 24), one integer op on the exponent field
-      const float z = zx[h];
-      const float half = __int_as_float((ubits(z) & 0x7f800000u) - (24u << 23));
-      const float tol = 0x1p-32f * fabsf(z);
-      const bool pow2 = (ubits(z) & 0x7fffffu) == 0u;
-      const bool hard = fabsf(fabsf(rx[h]) - half) <= tol ||
-                        (pow2 && fabsf(fabsf(rx[h]) - 0.5f * half) <= tol);
-      z0[e] = z;
+      z0[e] = zx[h];
       dl[e] = sub(y0[e], 1.0f);
       if (fabsf(dl[e]) <= 0x1p-7f) near |= 1u << e;          // C::NEAR1H
-      else ok[e] = ok[e] && !hard;
+      else ok[e] = ok[e] && !hard[h];
     }
     // z1 = core.e + (core.v - z0) (_correct, explog.py:222-223), after near-1 fix-ups
     z1[2 * p] = lo(core.v);
@@ -1076,6 +1099,132 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
   }
 }
 
+// ------------------------------------------ binary32 tlog1p, lane pairs
+// fast_tlog1p<float> (UNIFIED, PM = false, INNER = true) with the twofold
+// pipeline on f32x2 pairs.  The two branches of _plog1p_raw (explog.py:290-294)
+// share one seed, one pexpm10 and one twofold product of the Newton step, with
+// per-lane operand selects where they differ:
+//   in band:     u = ((v s) + v) + s                (explog.py:271-273)
+//   out of band: u = (zc s) + ((zc0 - 1) + zc1)     (explog.py:182-184)
+// so both lanes of a pair run one instruction stream whatever their branch.
+// The per-lane operation sequence is exactly fast_tlog1p<float>'s; in-band
+// lanes with v1 == 0 (explog.py:268-270) take a warp-uniform extra step.
+template <int VW, bool RENORM>
+TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const float (&y1i)[VW],
+                          float (&z0)[VW], float (&z1)[VW], bool (&ok)[VW]) {
+  static_assert(VW % 2 == 0, "lane pairs");
+  constexpr int NP = VW / 2;
+  using C = LogC<float>;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const int a = 2 * p, b = 2 * p + 1;
+    const float yy0[2] = {y0i[a], y0i[b]}, yy1[2] = {y1i[a], y1i[b]};
+    const f2 y0 = pk(yy0[0], yy0[1]), y1 = pk(yy1[0], yy1[1]);
+    TF<f2> v = mk(y0, y1);
+    if (RENORM) v = renorm_u(v);
+    // out-of-band prologue for both lanes: w = renorm(v + 1), then frexp
+    const TF<f2> w = renorm_u(t_add_d_u(v, splat(1.0f)));
+    const float vv[2] = {lo(v.v), hi(v.v)}, ve[2] = {lo(v.e), hi(v.e)};
+    const float wv[2] = {lo(w.v), hi(w.v)}, we[2] = {lo(w.e), hi(w.e)};
+    bool k[2], inb[2], zero1[2];
+    int n[2];
+    float xv[2], xe[2], p2[2], one[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      k[h] = (fabsf(yy0[h]) <= 0x1.fffffep127f) & (fabsf(yy1[h]) <= 0x1.fffffep127f);
+      inb[h] = (vv[h] >= -0.5f) & (vv[h] <= 1.0f);         // explog.py:291
+      // out of band: v0 > -1 and |y1 / (1 + y0)| <= 2^-14 (log1p(d) = d - d^2/2)
+      k[h] &= inb[h] | ((vv[h] > -1.0f) & (fabsf(yy1[h]) * 0x1p14f <= fabsf(wv[h])));
+      const bool band = (wv[h] >= 0.5f) & (wv[h] <= 2.0f);
+      const int nn = band ? 0 : C::n_of(wv[h]);
+      n[h] = inb[h] ? 0 : nn;
+      // the Newton product's left operand x: v in band, zc = (zc0, w1 2^-n) out
+      xv[h] = inb[h] ? vv[h] : band ? wv[h] : C::mant(wv[h]);
+      xe[h] = inb[h] ? ve[h] : we[h];
+      p2[h] = (inb[h] | band) ? 1.0f : C::p2(-nn);         // x1 * 1 == x1 exactly
+      zero1[h] = !(inb[h] | band) & (we[h] == 0.0f);
+      one[h] = inb[h] ? 0.0f : 1.0f;
+    }
+    const f2 xm_v = pk(xv[0], xv[1]);
+    f2 xm_e = mul(pk(xe[0], xe[1]), pk(p2[0], p2[1]));
+    xm_e = pk(zero1[0] ? 0.0f : lo(xm_e), zero1[1] ? 0.0f : hi(xm_e));
+    const f2 pa = sub(xm_v, pk(one[0], one[1]));           // v0 in band, zc0 - 1 out (exact)
+    f2 arg;
+    TF<f2> yw;
+    if constexpr (RENORM) {
+      // renormalised v: RN(v0 + v1) == v0 and fast_two_sum(v0, v1) == (v0, v1)
+      // bitwise, so one expression serves both branches
+      arg = add(pa, xm_e);
+      yw = fast_two_sum_u(pa, xm_e);
+    } else {
+      arg = sel2(inb[0], inb[1], v.v, add(pa, xm_e));
+      const TF<f2> wz = fast_two_sum_u(pa, xm_e);
+      yw = mk(sel2(inb[0], inb[1], v.v, wz.v), sel2(inb[0], inb[1], v.e, wz.e));
+    }
+    const f2 sd = seed_log1p_p(tb, arg);                   // explog.py:197-199, 277
+    const float sx[2] = {lo(sd), hi(sd)};
+    float ms[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      k[h] &= fabsf(sx[h]) <= P<float>::LN2_V;
+      ms[h] = k[h] ? -sx[h] : 0.0f;                         // keeps the CM1 index in range
+    }
+    const TF<f2> s = pexpm10_inband_p(tb, pk(ms[0], ms[1]));
+    // Newton step: one product x s, then + v + s in band, + wz out of band
+    const TF<f2> u1 = t_add_u(t_mul_u(mk(xm_v, xm_e), s), yw);
+    const TF<f2> u2 = t_add_u(u1, s);
+    TF<f2> u = mk(sel2(inb[0], inb[1], u2.v, u1.v), sel2(inb[0], inb[1], u2.e, u1.e));
+    const bool dot[2] = {inb[0] & (ve[0] == 0.0f), inb[1] & (ve[1] == 0.0f)};
+    if (__any_sync(0xffffffffu, dot[0] | dot[1])) {       // explog.py:268-270
+      const TF<f2> w1 = fast_two_sum_u(splat(1.0f), v.v);
+      const TF<f2> u0 = t_add_d_u(t_mul_u(w1, s), v.v);
+      u = mk(sel2(dot[0], dot[1], u0.v, u.v), sel2(dot[0], dot[1], u0.e, u.e));
+    }
+    const f2 x1 = add(u.v, u.e);
+    // newton_quiet: |x1| < 2^-21 max(|sd|, 1)
+    const f2 lim = mul(pk(fmaxf(fabsf(sx[0]), 1.0f), fmaxf(fabsf(sx[1]), 1.0f)), splat(0x1p-21f));
+    const float xx[2] = {lo(x1), hi(x1)}, lm[2] = {lo(lim), hi(lim)};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) k[h] &= fabsf(xx[h]) < lm[h];
+    // + n ln2 (explog.py:355-358).  In band n = 0 and core == (sd, x1) (up to
+    // the sign of a zero x1, which no result below can see)
+    const TF<f2> nl = t_mul_d_u(mk(splat(P<float>::LN2_V), splat(P<float>::LN2_E)),
+                                pk((float)n[0], (float)n[1]));
+    const TF<f2> core = t_add_u(mk(sd, x1), nl);
+    // one reciprocal per lane: 1 / (1 + y0) in band, 1 / zc0 out of band
+    const f2 q = sel2(inb[0], inb[1], add(splat(1.0f), y0), xm_v);
+    const f2 r = pk(rcp_approx(lo(q)), rcp_approx(hi(q)));
+    const f2 rc = fmaop(r, fmaop(-q, r, splat(1.0f)), r);   // rcp_nr
+    // tlogp's value part t0 = log(w0) (_correct, explog.py:366-373); in band
+    // t0 = RN(sd - 0) = sd, so that the final _correct below is x1 + (sd - z0)
+    bool hard0[2], hard[2];
+    const f2 t0 = rn_guard_p(core.v, sel2(inb[0], inb[1], splat(-0.0f), sub(core.e, mul(xm_e, rc))),
+                             hard0);
+    const f2 t1 = add(core.e, sub(core.v, t0));
+    // d = y1 / (1 + y0): in band y1 r, out of band (y1 2^-n) / zc0, which enters
+    // as log1p(d) = d - d^2/2 (fast_tlog1p<float>)
+    const f2 dd = mul(mul(y1, pk(p2[0], p2[1])), rc);
+    const f2 g = fmaop(mul(splat(-0.5f), dd), dd, dd);
+    const f2 zz = rn_guard_p(core.v, sub(core.e, sel2(inb[0], inb[1], dd, g)), hard);
+    const float dx[2] = {lo(dd), hi(dd)};
+    float zx[2] = {lo(zz), hi(zz)};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const bool tiny = inb[h] & (fabsf(yy0[h]) < 0x1p-25f);
+      const bool okin = tiny | ((fabsf(dx[h]) * 0x1p21f <= fabsf(sx[h])) & !hard[h]);
+      k[h] &= inb[h] ? okin : !(hard0[h] | hard[h]);
+      zx[h] = tiny ? yy0[h] : zx[h];
+    }
+    const f2 zr = add(t1, sub(t0, pk(zx[0], zx[1])));      // _correct (222-223, 372-373)
+    z0[a] = zx[0];
+    z0[b] = zx[1];
+    z1[a] = lo(zr);
+    z1[b] = hi(zr);
+    ok[a] = k[0];
+    ok[b] = k[1];
+  }
+}
+
 // Per-warp exchange buffer for class-sorting the 32 x VW elements of a warp
 // iteration (binary32 tlog1p, whose in-band / out-of-band split is ~50/50).
 template <int VW> struct Xch {
@@ -1275,10 +1424,17 @@ TF_DEV bool fast_alt(const STab<T>& tb, T x0, T x1, T& z0, T& z1) {
   }
 }
 
-// log1p-family functions (class-sorted in binary32)
+// binary32 tlog1p / tlog1pp run on lane pairs (fast_tlog1p_p); the other
+// log1p-family functions are class-sorted (tlog1p_sorted)
+#ifndef TF_TLOG1P32_PACKED
+#define TF_TLOG1P32_PACKED 1
+#endif
+__host__ __device__ constexpr bool log1p_packed32(int fn) {
+  return TF_TLOG1P32_PACKED && (fn == FN_TLOG1P || fn == FN_TLOG1PP);
+}
 __host__ __device__ constexpr bool log1p_fn(int fn) {
-  return fn == FN_TLOG1P || fn == FN_TLOG1P0 || fn == FN_TLOG1PP || fn == FN_PLOG1P ||
-         fn == FN_PLOG1P0;
+  return !log1p_packed32(fn) && (fn == FN_TLOG1P || fn == FN_TLOG1P0 || fn == FN_TLOG1PP ||
+                                 fn == FN_PLOG1P || fn == FN_PLOG1P0);
 }
 
 // All twenty functions (explog.py:101-325) on the admission-band cores.  The
@@ -1310,7 +1466,9 @@ TF_DEV void fast_eval(const STab<T>& tb, void* xch, const T (&x0)[VW], const T (
     constexpr bool RENORM = FN == FN_TLOG1P;
     constexpr bool PM = FN == FN_PLOG1P0 || FN == FN_PLOG1P;
     constexpr bool INNER = !(FN == FN_TLOG1P0 || FN == FN_PLOG1P0);
-    if constexpr (sizeof(T) == 4 && VW >= 2)
+    if constexpr (sizeof(T) == 4 && VW % 2 == 0 && log1p_packed32(FN))
+      fast_tlog1p_p<VW, RENORM>(tb, x0, x1, z0, z1, ok);
+    else if constexpr (sizeof(T) == 4 && VW >= 2)
       tlog1p_sorted<VW, RENORM, PM, INNER>(tb, static_cast<Xch<VW>*>(xch), x0, x1, z0, z1, ok);
     else
       fast_tlog1p<T, VW, RENORM, PM, INNER>(tb, x0, x1, z0, z1, ok);
