@@ -340,23 +340,63 @@ TF_DEV bool newton_quiet(float r1, float r0) {
   return fabsf(r1) < 0x1p-21f * fmaxf(fabsf(r0), 1.0f);
 }
 
-// binary32 value part RN(h + l) from a twofold core that is only accurate to
-// ~2^-36 relative (the reference's own binary32 L0 bound):
-// flag the element when h + l lies within 2^-32 |z| of a rounding boundary
-// (probability ~2^-9 ulp-relative, i.e. ~1e-5 of elements) so the exact path,
-// which rounds a binary64 core, decides it.  Exact powers of two are flagged
-// by the quarter-ulp boundary below them as well.
-// Every caller's z is a normal binary32 above 2^-102 (exp in band, expm1
-// beyond ln 2, logarithms away from their tiny-argument shortcuts), so half an
-// ulp is 2^(e(z) - 24): one integer op on the exponent field.
+// binary32 value part RN(h + l) from a twofold core: flag the element when
+// h + l lies within 2^TOL |z| of a rounding boundary, so the rare-element
+// drain decides it with the binary64 library (or the exact path).  The
+// reference's twofold results are accurate to ~2^-37 at worst (PAPER.md:745-755,
+// the near-1 log lanes), but the value-part sums of the fast kernels are far
+// better: built with TOL = -40, 2^30 config-4 samples per function show no
+// fast/exact difference (tools/guard_probe.py), so TOL = -36 keeps a 16x
+// margin while flagging only ~2^-11 of the elements.
+// rho = (h + l) - z is at most half an ulp (|z| < 2^(e+1): half = 2^(e-24),
+// 2^TOL |z| <= 2^(TOL+25) half), so "within 2^TOL |z| of the boundary" implies
+// |rho| k > half for k = 1 + eps + 2 eps^2, eps = 2^(TOL+25) ((1 - eps) k > 1),
+// where z + rho k crosses the midpoint and rounds away from z: one FFMA and
+// one compare, flagging |rho| >~ (1 - eps) half (~2^(TOL+25) of the
+// elements).  Below an exact power of two the midpoint is half / 2, which the
+// same rounding detects.
+// rounding-guard tolerances (2^TOL |z|) of the binary32 logarithms and
+// exponentials
+#ifndef TF_TOL32_LOG
+#define TF_TOL32_LOG -36
+#endif
+#ifndef TF_TOL32_EXP
+#define TF_TOL32_EXP -36
+#endif
+#ifndef TF_GUARD_TIGHT
+#define TF_GUARD_TIGHT 1
+#endif
+template <int TOL = -32> TF_DEV float kguard() {
+  // 2 eps^2 below 2^-23: one ulp of k still satisfies (1 - eps) k > 1
+  constexpr int SQ = 23 + 2 * (TOL + 25) + 1;
+  if (TF_GUARD_TIGHT)
+    return __int_as_float(0x3f800000 + (1 << (23 + TOL + 25)) + (SQ > 0 ? 1 << SQ : 1));
+  return __int_as_float(0x3f800000 + (1 << (23 + TOL + 26)));   // 1 + 2 eps
+}
 template <int TOL = -32> TF_DEV float rn_guard(float h, float l, bool& hard) {
   float z = add(h, l);
   float rho = add(sub(h, z), l);                    // (h + l) - z
-  float half = __int_as_float((ubits(z) & 0x7f800000u) - (24u << 23));   // ulp(z) / 2
-  float tol = __int_as_float((127 + TOL) << 23) * fabsf(z);
-  bool pow2 = (ubits(z) & 0x7fffffu) == 0u;
-  hard = fabsf(fabsf(rho) - half) <= tol || (pow2 && fabsf(fabsf(rho) - 0.5f * half) <= tol);
+  hard = fmaop(rho, kguard<TOL>(), z) != z;
   return z;
+}
+// binary32 log(1 + d) for an exact |d| <= 2^-7 (the logarithms' near-1
+// lanes): d - d^2/2 with d^2 split exactly by an FMA, then the d^3 .. d^7
+// terms (truncation d^8/8 <= 2^-59), rounded under the guard: the series'
+// own rounding error is ~2^-41 |z| at |d| = 2^-7, and a correctly rounded
+// value needs the midpoint test like every other binary32 value part
+// (tools/guard_probe.py found y = 0x1.01ed9ap+0 misrounded by the earlier
+// unguarded degree-5 series).
+TF_DEV float log_near1_g(float d, bool& hard) {
+  const float q = mul(d, d);
+  const float qe = fmaop(d, d, -q);
+  float p = fmaop(d, 0x1.24924ap-3f, -0x1.555556p-3f);      // 1/7, -1/6
+  p = fmaop(d, p, 0x1.99999ap-3f);                          // 1/5
+  p = fmaop(d, p, -0.25f);
+  p = fmaop(d, p, 0x1.555556p-2f);                          // 1/3
+  const float c = mul(mul(q, d), p);
+  const float lo = fmaop(-0.5f, qe, c);
+  const TF<float> s = fast_two_sum_u(d, mul(-0.5f, q));
+  return rn_guard<TF_TOL32_LOG>(s.v, add(s.e, lo), hard);
 }
 template <int TOL = -32>
 TF_DEV double rn_guard(double h, double l, bool& hard) {  // binary64 cores: ~2^-100, no guard
@@ -453,7 +493,7 @@ TF_DEV void fast_texp(const STab<float>& tb, const float (&x0)[VW], const float 
     TF<float> vs = t_mul_u(scaled ? es : ev, ct);
     bool hard;
     if constexpr (DBLV) z0[e] = cr32_lib<DF_EXP>(x0[e], hard);
-    else z0[e] = mul(rn_guard<-35>(vs.v, vs.e, hard), scaled ? 0x1p-64f : 1.0f);
+    else z0[e] = mul(rn_guard<TF_TOL32_EXP>(vs.v, vs.e, hard), scaled ? 0x1p-64f : 1.0f);
     ok[e] = ok[e] && !hard;
     z1[e] = add(mul(z0[e], t1_tiny(x1[e])), add(v.e, sub(v.v, z0[e])));
   }
@@ -549,7 +589,7 @@ TF_DEV void fast_texpm1(const STab<float>& tb, const float (&x0)[VW], const floa
     }
     bool hard;
     if constexpr (DBLV) z0[e] = cr32_lib<DF_EXPM1>(x0[e], hard);
-    else z0[e] = rn_guard<-35>(w.v, w.e, hard);
+    else z0[e] = rn_guard<TF_TOL32_EXP>(w.v, w.e, hard);
     ok[e] = ok[e] && !hard;
     float tail = add(w.e, sub(w.v, z0[e]));
     z1[e] = add(mul(add(z0[e], 1.0f), t1_tiny(x1[e])), tail);
@@ -572,7 +612,7 @@ TF_DEV void fast_texpm1_inb32(const STab<float>& tb, float x0, float x1, float& 
     return;
   }
   bool hard;
-  z0 = rn_guard<-35>(w[0].v, w[0].e, hard);        // binary64 library only when
+  z0 = rn_guard<TF_TOL32_EXP>(w[0].v, w[0].e, hard);        // binary64 library only when
   if (hard) z0 = cr32_lib<DF_EXPM1>(xs[0], hard);  // the core cannot decide
   if (ahi(xs[0]) < B32_TINY25) {                    // expm1(x) rounds to x (keeps -0)
     z0 = xs[0];
@@ -699,7 +739,7 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
       z0[e] = cr32_lib<DF_LOG>(y0[e], hard);
       ok[e] = ok[e] && !hard;
     } else {
-      z0[e] = rn_guard(core.v, sub(core.e, d0), hard);
+      z0[e] = rn_guard<TF_TOL32_LOG>(core.v, sub(core.e, d0), hard);
       if (ahi(dl[e]) < C::NEAR1H) near |= 1u << e;
       else ok[e] = ok[e] && !hard && dsmall;
     }
@@ -715,10 +755,13 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
       if (near >> e & 1u) d = dl[e];
     if (near & 1u) d = dl[0];
     const unsigned low = near & (0u - near);
-    T r = log_near1(d);
+    bool hn = false;
+    T r;
+    if constexpr (sizeof(T) == 4) r = log_near1_g(d, hn);
+    else r = log_near1(d);
 #pragma unroll
     for (int e = 0; e < VW; ++e)
-      if (low == 1u << e) z0[e] = r;
+      if (low == 1u << e) { z0[e] = r; ok[e] = ok[e] && !hn; }
     near &= near - 1u;
   }
   if constexpr (!PM) {
@@ -789,24 +832,13 @@ TF_DEV TF<f2> pexpm10_inband_p(const STab<float>& tb, f2 mx) {
   return t_add_u(t_mul_u(cm, tt), t_add_u(cm, tt));
 }
 
-// rn_guard<-32> (below) on a lane pair, for values |z| >= 2^-100 (the log
-// families away from their tiny-argument shortcuts): packed sums and one
-// threshold compare per lane.  rho = (h + l) - z is at most half an ulp, so
-// "within 2^-32 |z| of the midpoint" is implied by |rho| >= half (1 - 2^-7)
-// (2^-7 half >= 2^-32 |z|), a superset of rn_guard's test; below an exact
-// power of two the midpoint is half / 2.  The threshold is built on the
-// exponent field: 2^(e-25) * 0x1.fcp0 = half (1 - 2^-7).
+// rn_guard<TF_TOL32_LOG> on a lane pair: packed sums and crossing test
 TF_DEV f2 rn_guard_p(f2 h, f2 l, bool (&hard)[2]) {
   const f2 zs = add(h, l);
   const f2 rho = add(sub(h, zs), l);
-  const float zx[2] = {lo(zs), hi(zs)}, rx[2] = {lo(rho), hi(rho)};
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const uint32_t zb = ubits(zx[k]);
-    const uint32_t sh = (zb & 0x7fffffu) == 0u ? (26u << 23) : (25u << 23);
-    const float thr = __uint_as_float((zb & 0x7f800000u) - sh + 0x7e0000u);
-    hard[k] = fabsf(rx[k]) >= thr;
-  }
+  const f2 cr = fmaop(rho, splat(kguard<TF_TOL32_LOG>()), zs);
+  hard[0] = lo(cr) != lo(zs);
+  hard[1] = hi(cr) != hi(zs);
   return zs;
 }
 
@@ -910,10 +942,11 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
       if (near >> e & 1u) d = dl[e];
     if (near & 1u) d = dl[0];
     const unsigned low = near & (0u - near);
-    const float r = log_near1(d);
+    bool hn;
+    const float r = log_near1_g(d, hn);
 #pragma unroll
     for (int e = 0; e < VW; ++e)
-      if (low == 1u << e) z0[e] = r;
+      if (low == 1u << e) { z0[e] = r; ok[e] = ok[e] && !hn; }
     near &= near - 1u;
   }
 #pragma unroll
@@ -1047,7 +1080,7 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       bool hard;
       T zz;
       if constexpr (DBLV && !D) zz = cr32_lib<DF_LOG1P>(y0[e], hard);
-      else zz = rn_guard(sd[e], sub(x1, d), hard);
+      else zz = rn_guard<TF_TOL32_LOG>(sd[e], sub(x1, d), hard);
       z0[e] = tiny ? y0[e] : zz;
       ok[e] = ok[e] && (tiny || !hard);
       z1[e] = add(x1, sub(sd[e], z0[e]));               // _correct (372-373)
@@ -1073,7 +1106,7 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       if constexpr (DBLV && !D) {
         t0 = cr32_lib<DF_LOG>(wv[e], hard0);                 // log(w0)
       } else {
-        t0 = rn_guard(core.v, sub(core.e, mul(zc1[e], rc)), hard0);
+        t0 = rn_guard<TF_TOL32_LOG>(core.v, sub(core.e, mul(zc1[e], rc)), hard0);
       }
       ok[e] = ok[e] && !hard0;
       T t1 = add(core.e, sub(core.v, t0));
@@ -1090,7 +1123,7 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       bool hard;
       T zz;
       if constexpr (DBLV && !D) zz = cr32_lib<DF_LOG1P>(y0[e], hard);
-      else zz = rn_guard(core.v, sub(core.e, fmaop(mul(T(-0.5), dd), dd, dd)), hard);
+      else zz = rn_guard<TF_TOL32_LOG>(core.v, sub(core.e, fmaop(mul(T(-0.5), dd), dd, dd)), hard);
       ok[e] = ok[e] && !hard;
       z0[e] = zz;
       if constexpr (INNER) z1[e] = add(t1, sub(t0, zz));  // _correct (222-223)
@@ -1309,7 +1342,7 @@ template <class T, int FN> struct HasAlt {
 };
 
 // binary32 second chance: the same fast cores with the value part from the
-// binary64 library instead of the 2^-32 rounding guard (which sends ~0.5% of
+// binary64 library instead of the 2^-36 rounding guard (which sends ~0.05% of
 // elements away), and texpm1's in-band branch
 template <int FN>
 TF_DEV bool fast_alt32(const STab<float>& tb, float x0, float x1, float& z0, float& z1) {

@@ -423,7 +423,7 @@ template <class T> TF_DEV TF<T> log1p_core_c(T y0, T y1) {
   return mk(x0, x1);
 }
 
-// log(1 + d) for an exact |d| <= 2^-20 (resp. 2^-7 in binary32), correctly
+// log(1 + d) for an exact |d| <= 2^-20 (binary32: log_near1_g, tf_fast.cuh), correctly
 // rounded up to ~2^-40 ulp: d - d^2/2 with d^2 split exactly by an FMA, then
 // d^3/3 - d^4/4 + d^5/5.  Near y = 1 the log core's absolute accuracy is not
 // enough to round log(y) when d has few significant bits (y = 1 + k*2^-52),
@@ -434,14 +434,6 @@ TF_DEV double log_near1(double d) {
   double c = mul(mul(q, d), fmaop(d, fmaop(d, 0.2, -0.25), 0x1.5555555555555p-2));
   double lo = fmaop(-0.5, qe, c);
   TF<double> s = fast_two_sum_u(d, mul(-0.5, q));
-  return add(s.v, add(s.e, lo));
-}
-TF_DEV float log_near1(float d) {
-  float q = mul(d, d);
-  float qe = fmaop(d, d, -q);
-  float c = mul(mul(q, d), fmaop(d, fmaop(d, 0.2f, -0.25f), 0x1.555556p-2f));
-  float lo = fmaop(-0.5f, qe, c);
-  TF<float> s = fast_two_sum_u(d, mul(-0.5f, q));
   return add(s.v, add(s.e, lo));
 }
 constexpr uint64_t NEAR1_64 = 0x3eb0000000000000ull;  // 2^-20

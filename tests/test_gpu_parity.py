@@ -399,6 +399,35 @@ def test_near_one_shell_fast_equals_exact(fn, cuda):
     assert not bad.any(), [(float(x0[i]).hex(), float(x1[i]).hex()) for i in idx]
 
 
+@pytest.mark.parametrize("fn", ("tlog", "tlogp", "tlog0"))
+def test_near_one_binary32_exhaustive(fn, cuda):
+    """Every binary32 y0 in [1 - 2^-7, 1 + 2^-7] (the near-1 series lanes of
+    the binary32 logarithms), each with three tails: fast kernel == exact path
+    bitwise.  y0 = 0x1.01ed9ap+0 was misrounded by the unguarded degree-5
+    series (tools/guard_probe.py, 5 of 2^32 config-4 samples)."""
+    import torch
+
+    from paper_1502_05216_b200 import _lib, api
+
+    lo_b = int(np.float32(1 - 2.0 ** -7).view(np.int32))
+    hi_b = int(np.float32(1 + 2.0 ** -7).view(np.int32))
+    y0 = torch.arange(lo_b, hi_b + 1, dtype=torch.int32, device=cuda).view(torch.float32)
+    y0 = y0.repeat(3)
+    g = torch.Generator(device=cuda).manual_seed(3)
+    u = torch.rand(y0.numel(), dtype=torch.float32, device=cuda, generator=g) * 2 - 1
+    x1 = torch.zeros_like(y0) if fn == "tlog0" else y0 * u * 2.0 ** -24
+    x1[: y0.numel() // 3] = 0.0
+    y0[0] = float.fromhex("0x1.01ed9ap+0")
+    lib = api(32)
+    a = lib._device(fn, y0, x1)
+    b = lib._device(fn, y0, x1, flags=_lib.FLAG_FORCE_EXACT)
+    torch.cuda.synchronize()
+    bad = (a.value.view(torch.int32) != b.value.view(torch.int32)) | \
+          (a.error.view(torch.int32) != b.error.view(torch.int32))
+    idx = torch.nonzero(bad).flatten()[:5].tolist()
+    assert not bad.any(), [(float(y0[i]).hex(), float(x1[i]).hex()) for i in idx]
+
+
 @pytest.mark.parametrize("width", WIDTHS)
 @pytest.mark.parametrize("fn", ALL_FNS)
 def test_random_bit_patterns(fn, width, cuda):
