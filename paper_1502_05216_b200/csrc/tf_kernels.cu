@@ -110,10 +110,14 @@ TF_DEV void st(T* p, uint64_t vi, const T (&a)[VW]) {
 #ifndef TF_STAGES64
 #define TF_STAGES64 2
 #endif
+// CTA size of the 4-lane binary64 kernels (112 registers: 512 threads)
+#ifndef TF_BLOCK_WIDE
+#define TF_BLOCK_WIDE (TF_BLOCK / 2)
+#endif
 template <class T, int VW> struct KCfg {
   static constexpr bool WIDE = sizeof(T) == 8 && VW == 4;   // 4 binary64 lanes per thread
   static constexpr bool WIDE32 = sizeof(T) == 4 && VW == 8;  // 8 binary32 lanes per thread
-  static constexpr int BLOCK = (WIDE || WIDE32) ? TF_BLOCK / 2 : TF_BLOCK;
+  static constexpr int BLOCK = (WIDE || WIDE32) ? TF_BLOCK_WIDE : TF_BLOCK;
   static constexpr int MINB = (WIDE || WIDE32) ? 1 : 1024 / TF_BLOCK;
 };
 
