@@ -792,6 +792,27 @@ TF_DEV TF<f2> taylor_expm1_p(f2 yp) {
 }
 
 // table-driven seed log1p (seed_log1p_t<float>) on a lane pair
+// One 32-bit shared-memory load per half of a lane pair (TF_SPLIT_LDS): the two
+// lanes read different table entries, and loading each entry's (v, e) as one
+// 64-bit word leaves v0, v1 in two different register pairs, which ptxas then
+// copies into place (IMAD.MOV, on the busy fmaheavy pipe) for the packed
+// consumers.  The loads are volatile because ptxas merges adjacent plain
+// ld.shared.f32 back into LDS.64.  +6% tlog f32, +4% tlog1p f32.
+#ifndef TF_SPLIT_LDS
+#define TF_SPLIT_LDS 1
+#endif
+TF_DEV float lds32(const float* p) {
+  float r;
+  asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(r) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return r;
+}
+TF_DEV TF<f2> ldpair(const float2* t, int i0, int i1) {
+  if (TF_SPLIT_LDS)
+    return mk(pk(lds32(&t[i0].x), lds32(&t[i1].x)), pk(lds32(&t[i0].y), lds32(&t[i1].y)));
+  const float2 a = t[i0], b = t[i1];
+  return mk(pk(a.x, b.x), pk(a.y, b.y));
+}
+
 TF_DEV f2 seed_log1p_p(const STab<float>& tb, f2 a) {
   constexpr int B = TF32_SEED_BITS, NB = 1 << B;
   f2 f = add(splat(1.0f), a);
@@ -806,15 +827,15 @@ TF_DEV f2 seed_log1p_p(const STab<float>& tb, f2 a) {
     small[h] = fabsf(ax[h]) < 0x1p-8f;                    // |a| < 2^-8 (FP pipe)
     idx[h] = small[h] ? NB : min(max(i, 0), 2 * NB);
   }
-  const float2 t0 = tb.SEED[idx[0]], t1 = tb.SEED[idx[1]];
-  const f2 ic = pk(t0.x, t1.x);
+  const TF<f2> t = ldpair(tb.SEED, idx[0], idx[1]);
+  const f2 ic = t.v;
   f2 r = fmaop(f, ic, splat(-1.0f));
   r = pk(small[0] ? ax[0] : lo(r), small[1] ? ax[1] : hi(r));
   f2 q = mul(r, r);                                       // seed_poly<float>
   f2 pp = fmaop(r, splat(-0.25f), splat(0x1.555556p-2f));
   pp = fmaop(r, pp, splat(-0.5f));
   pp = fmaop(q, pp, r);
-  const f2 lc = pk(small[0] ? 0.0f : t0.y, small[1] ? 0.0f : t1.y);
+  const f2 lc = pk(small[0] ? 0.0f : lo(t.e), small[1] ? 0.0f : hi(t.e));
   const f2 cl = pk(small[0] ? 0.0f : lo(clo), small[1] ? 0.0f : hi(clo));
   return add(lc, fmaop(cl, ic, pp));
 }
@@ -827,8 +848,7 @@ TF_DEV TF<f2> pexpm10_inband_p(const STab<float>& tb, f2 mx) {
   const int n0 = (int)ubits(lo(tq)) - 0x4b400000, n1 = (int)ubits(hi(tq)) - 0x4b400000;
   const f2 ym = fmaop(sub(tq, splat(12582912.0f)), splat(-0.0078125f), mx);
   const TF<f2> tt = taylor_expm1_p(ym);
-  const TF<f2> cm = pk2(tv<float>(tb.CM1[n0 - P<float>::CM1_LO]),
-                        tv<float>(tb.CM1[n1 - P<float>::CM1_LO]));
+  const TF<f2> cm = ldpair(tb.CM1, n0 - P<float>::CM1_LO, n1 - P<float>::CM1_LO);
   return t_add_u(t_mul_u(cm, tt), t_add_u(cm, tt));
 }
 
