@@ -1227,7 +1227,7 @@ TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const f
     const TF<f2> u1 = t_add_u(t_mul_u(mk(xm_v, xm_e), s), yw);
     const TF<f2> u2 = t_add_u(u1, s);
     TF<f2> u = mk(sel2(inb[0], inb[1], u2.v, u1.v), sel2(inb[0], inb[1], u2.e, u1.e));
-    const bool dot[2] = {inb[0] & (ve[0] == 0.0f), inb[1] & (ve[1] == 0.0f)};
+    const bool dot[2] = {bool(inb[0] & (ve[0] == 0.0f)), bool(inb[1] & (ve[1] == 0.0f))};
     if (__any_sync(0xffffffffu, dot[0] | dot[1])) {       // explog.py:268-270
       const TF<f2> w1 = fast_two_sum_u(splat(1.0f), v.v);
       const TF<f2> u0 = t_add_d_u(t_mul_u(w1, s), v.v);

@@ -34,6 +34,9 @@ namespace tf {
 #ifndef TF_VW64_LOG
 #define TF_VW64_LOG 4
 #endif
+#ifndef TF_VW32_LOG
+#define TF_VW32_LOG TF_VW32
+#endif
 #ifndef TF_VW32
 #define TF_VW32 4
 #endif
@@ -612,7 +615,10 @@ int launch(const T* x0, const T* x1, T* z0, T* z1, int64_t n, void* stream, int 
       constexpr int VW = TF_VW64 ? TF_VW64 : (EXPF ? TF_VW64_EXP : TF_VW64_LOG);
       return launch_one<T, FN, VW>(x0, x1, z0, z1, n, s, flags);
     }
-    else return launch_one<T, FN, TF_VW32>(x0, x1, z0, z1, n, s, flags);
+    else {
+      constexpr bool LOGF = tf::EvalCfg<T, FN, 4>::LOGF;
+      return launch_one<T, FN, LOGF ? TF_VW32_LOG : TF_VW32>(x0, x1, z0, z1, n, s, flags);
+    }
   }
   if ((al & (sizeof(T) - 1)) != 0) return fail(TF_ERR_ARG, "misaligned pointer%s");
   return launch_one<T, FN, 1>(x0, x1, z0, z1, n, s, flags);
