@@ -879,8 +879,12 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
     // classification on the FP pipe (FSETP) where an integer test would load
-    // the ALU pipe, the binding one in this kernel: positive normal y0, finite y1
-    ok[e] = y0i[e] >= 0x1p-126f && y0i[e] <= 0x1.fffffep127f && fabsf(y1i[e]) <= 0x1.fffffep127f;
+    // the ALU pipe: positive normal y0, finite y1.  With RENORM the finiteness
+    // tests are implied by the positive-normal test of v = renorm(y) below (an
+    // infinite or NaN operand, or an overflowing sum, makes v0 NaN)
+    ok[e] = RENORM ? y0i[e] >= 0x1p-126f
+                   : y0i[e] >= 0x1p-126f && y0i[e] <= 0x1.fffffep127f &&
+                         fabsf(y1i[e]) <= 0x1.fffffep127f;
     // rejected lanes compute on whatever they hold: every table index below is
     // clamped or derived from a masked value, and their results are discarded
     y0[e] = y0i[e];
@@ -1184,7 +1188,10 @@ TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const f
     float xv[2], xe[2], p2[2], one[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      k[h] = (fabsf(yy0[h]) <= 0x1.fffffep127f) & (fabsf(yy1[h]) <= 0x1.fffffep127f);
+      // finite operands; with RENORM implied by the tests on v below (an
+      // infinite or NaN operand or an overflowing sum makes v0 NaN, which is
+      // neither in band nor > -1)
+      k[h] = RENORM || ((fabsf(yy0[h]) <= 0x1.fffffep127f) & (fabsf(yy1[h]) <= 0x1.fffffep127f));
       inb[h] = (vv[h] >= -0.5f) & (vv[h] <= 1.0f);         // explog.py:291
       // out of band: v0 > -1 and |y1 / (1 + y0)| <= 2^-14 (log1p(d) = d - d^2/2)
       k[h] &= inb[h] | ((vv[h] > -1.0f) & (fabsf(yy1[h]) * 0x1p14f <= fabsf(wv[h])));
