@@ -399,6 +399,37 @@ def test_near_one_shell_fast_equals_exact(fn, cuda):
     assert not bad.any(), [(float(x0[i]).hex(), float(x1[i]).hex()) for i in idx]
 
 
+@pytest.mark.parametrize("fn", ("tlog1p", "tlog1pp"))
+def test_binary32_log1p_lane_pairs_zero_tails(fn, cuda):
+    """The lane-pair tlog1p kernel's warp-uniform extra step for in-band
+    arguments with v1 == 0 (explog.py:268-270): every tail zero, every other
+    tail zero, and random tails, on config-4 arguments and on [-1/2, 1]:
+    fast kernel == exact path bitwise."""
+    import torch
+
+    from paper_1502_05216_b200 import _lib, api
+
+    L = _lib.ensure_device(cuda.index)
+    n = 1 << 20
+    x0 = torch.empty(n, dtype=torch.float32, device=cuda)
+    x1 = torch.empty_like(x0)
+    _lib.check(L.tf_generate(_lib.DIST_CODES["log32"], 21, 0, n, x0.data_ptr(), x1.data_ptr(),
+                             None), "gen")
+    g = torch.Generator(device=cuda).manual_seed(4)
+    x0[n // 2:] = torch.rand(n - n // 2, device=cuda, generator=g) * 1.5 - 0.5
+    x1[n // 2:] = x0[n // 2:] * (torch.rand(n - n // 2, device=cuda, generator=g) * 2 - 1) * 2.0 ** -24
+    lib = api(32)
+    for tails in (torch.zeros_like(x1), torch.where(torch.arange(n, device=cuda) % 2 == 0, 0.0, x1),
+                  x1):
+        a = lib._device(fn, x0, tails)
+        b = lib._device(fn, x0, tails, flags=_lib.FLAG_FORCE_EXACT)
+        torch.cuda.synchronize()
+        bad = (a.value.view(torch.int32) != b.value.view(torch.int32)) | \
+              (a.error.view(torch.int32) != b.error.view(torch.int32))
+        idx = torch.nonzero(bad).flatten()[:5].tolist()
+        assert not bad.any(), [(float(x0[i]).hex(), float(tails[i]).hex()) for i in idx]
+
+
 @pytest.mark.parametrize("fn", ("tlog", "tlogp", "tlog0"))
 def test_near_one_binary32_exhaustive(fn, cuda):
     """Every binary32 y0 in [1 - 2^-7, 1 + 2^-7] (the near-1 series lanes of
