@@ -27,7 +27,8 @@ template <class T> struct STab {
   typename V2<T>::t C[P<T>::C_N];
   typename V2<T>::t CM1[P<T>::CM1_N];
   typename V2<T>::t ESC[sizeof(T) == 8 ? TF64_ESC_COUNT : TF32_ESC_COUNT];
-  typename V2<T>::t SEED[sizeof(T) == 8 ? TF64_SEED_COUNT : TF32_SEED_COUNT];
+  typename V2<T>::t SEED[sizeof(T) == 8 ? TF64_SEED_COUNT + 1 : TF32_SEED_COUNT];
+  T SEEDM1[sizeof(T) == 8 ? TF64_SEED_COUNT + 1 : 1];   // binary64: invc - 1 (seed_log1p_t)
 };
 
 // SEED (the log seed table, 32 KB in binary64) is staged only by the
@@ -45,9 +46,24 @@ template <class T> __device__ void load_tables(STab<T>& s, bool seed) {
   const typename V2<T>::t* srcD =
       sizeof(T) == 8 ? (const typename V2<T>::t*)g_SEED64 : (const typename V2<T>::t*)g_SEED32;
   constexpr int ND = sizeof(T) == 8 ? TF64_SEED_COUNT : TF32_SEED_COUNT;
-  if (seed)
-    for (int i = threadIdx.x; i < ND; i += blockDim.x) s.SEED[i] = srcD[i];
+  if (seed) {
+    for (int i = threadIdx.x; i < ND; i += blockDim.x) {
+      s.SEED[i] = srcD[i];
+      if constexpr (sizeof(T) == 8) s.SEEDM1[i] = sub(srcD[i].x, 1.0);
+    }
+    if constexpr (sizeof(T) == 8)
+      if (threadIdx.x == 0) {                     // identity entry for |a| < 2^-11
+        s.SEED[ND].x = 1.0;
+        s.SEED[ND].y = 0.0;
+        s.SEEDM1[ND] = 0.0;
+      }
+  }
 }
+// binary64 seed entry from the staged tables
+TF_DEV SeedE64 seed_entry(const STab<double>& tb, int i) {
+  return SeedE64{tb.SEED[i].x, tb.SEEDM1[i], tb.SEED[i].y};
+}
+TF_DEV float2 seed_entry(const STab<float>& tb, int i) { return tb.SEED[i]; }
 
 template <class T, class V> TF_DEV TF<T> tv(V a) { return mk(a.x, a.y); }
 
@@ -699,7 +715,7 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     zc0[e] = band ? v[e].v : C::mant(v[e].v);
     zc1[e] = band ? v[e].e : (zbits(v[e].e) ? T(0) : mul(v[e].e, p2s(-n[e])));
     r0[e] = seed_log1p_t(add(sub(zc0[e], T(1)), zc1[e]),      // explog.py:196-199
-                         [&](int i) { return tb.SEED[i]; });
+                         [&](int i) { return seed_entry(tb, i); });
     ok[e] = ok[e] && C::in_ln2(r0[e]);
     // keeps the CM1 index in range for rejected lanes (tlogp / plog take y1
     // unrenormalised, so the seed of a non-coupled input can be anything)
@@ -1062,7 +1078,7 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       ok[e] = ok[e] && inb[e];
     }
     if (!ok[e]) { arg = T(0); inb[e] = true; }
-    sd[e] = seed_log1p_t(arg, [&](int i) { return tb.SEED[i]; });  // explog.py:197-199, 277
+    sd[e] = seed_log1p_t(arg, [&](int i) { return seed_entry(tb, i); });  // explog.py:197-199, 277
     // pexpm10_raw(-sd) must take its in-band branch (|sd| <= LN2); in band this
     // can fail only at v0 = -1/2 or 1 with a seed one ulp beyond ln 2
     if (D && !UNIFIED) ok[e] = ok[e] && (inb[e] || C::in_ln2(sd[e]));

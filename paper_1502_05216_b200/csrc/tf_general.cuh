@@ -315,18 +315,23 @@ TF_DEV float seed_poly(float r) {   // degree 4
   p = fmaop(r, p, -0.5f);
   return fmaop(q, p, r);
 }
+// binary64: the table entry also carries invc - 1 (exact: invc is in [1/2, 2]),
+// so the reduced argument r = (1 + a) invc - 1 is one FMA on a itself,
+// fma(a, invc, invc - 1), rounded once -- no split of 1 + a into f + clo and
+// no clo / f correction term (8 FP64 ops instead of 11).  Entry 2 NB + 1 is the
+// identity (invc 1, log 0) used for |a| < 2^-11, where r = a exactly.
+struct SeedE64 { double invc, invcm1, logc; };
 template <class Get> TF_DEV double seed_log1p_t(double a, Get get) {
   constexpr int B = TF64_SEED_BITS, NB = 1 << B;
   double f = add(1.0, a);
-  double clo = sub(a, sub(f, 1.0));                    // 1 + a == f + clo exactly
   uint32_t h = (uint32_t)hi32(f);
   int idx = (((int)(h >> 20) - 1022) << B) | (int)((h >> (20 - B)) & (NB - 1u));
   bool small = ahi(a) < 0x3f400000u;                  // |a| < 2^-11
-  idx = small ? NB : min(max(idx, 0), 2 * NB);
-  double2 t = get(idx);
-  double r = small ? a : fmaop(f, t.x, -1.0);
+  idx = small ? 2 * NB + 1 : min(max(idx, 0), 2 * NB);
+  const SeedE64 t = get(idx);
+  double r = fmaop(a, t.invc, t.invcm1);
   double p = seed_poly(r);
-  return add(small ? 0.0 : t.y, fmaop(small ? 0.0 : clo, t.x, p));
+  return add(t.logc, p);
 }
 template <class Get> TF_DEV float seed_log1p_t(float a, Get get) {
   float f = add(1.0f, a);
@@ -344,7 +349,12 @@ template <class Get> TF_DEV float seed_log1p_t(float a, Get get) {
 // exact path: table seed on [-1/2, 1] (bit-identical to the fast kernels),
 // CUDA log1p elsewhere (non-finite / out-of-domain arguments only)
 TF_DEV double seed_log1p(double x) {
-  if (x >= -0.5 && x <= 1.0) return seed_log1p_t(x, [](int i) { return __ldg(&g_SEED64[i]); });
+  if (x >= -0.5 && x <= 1.0)
+    return seed_log1p_t(x, [](int i) {
+      if (i == TF64_SEED_COUNT) return SeedE64{1.0, 0.0, 0.0};
+      const double2 t = __ldg(&g_SEED64[i]);
+      return SeedE64{t.x, sub(t.x, 1.0), t.y};
+    });
   return log1p(x);
 }
 TF_DEV float seed_log1p(float x) {
