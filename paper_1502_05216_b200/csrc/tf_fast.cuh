@@ -27,8 +27,8 @@ template <class T> struct STab {
   typename V2<T>::t C[P<T>::C_N];
   typename V2<T>::t CM1[P<T>::CM1_N];
   typename V2<T>::t ESC[sizeof(T) == 8 ? TF64_ESC_COUNT : TF32_ESC_COUNT];
-  typename V2<T>::t SEED[sizeof(T) == 8 ? TF64_SEED_COUNT + 1 : TF32_SEED_COUNT];
-  T SEEDM1[sizeof(T) == 8 ? TF64_SEED_COUNT + 1 : 1];   // binary64: invc - 1 (seed_log1p_t)
+  typename V2<T>::t SEED[(sizeof(T) == 8 ? TF64_SEED_COUNT : TF32_SEED_COUNT) + 1];
+  T SEEDM1[(sizeof(T) == 8 ? TF64_SEED_COUNT : TF32_SEED_COUNT) + 1];   // invc - 1
 };
 
 // SEED (the log seed table, 32 KB in binary64) is staged only by the
@@ -49,21 +49,22 @@ template <class T> __device__ void load_tables(STab<T>& s, bool seed) {
   if (seed) {
     for (int i = threadIdx.x; i < ND; i += blockDim.x) {
       s.SEED[i] = srcD[i];
-      if constexpr (sizeof(T) == 8) s.SEEDM1[i] = sub(srcD[i].x, 1.0);
+      s.SEEDM1[i] = sub(srcD[i].x, T(1));
     }
-    if constexpr (sizeof(T) == 8)
-      if (threadIdx.x == 0) {                     // identity entry for |a| < 2^-11
-        s.SEED[ND].x = 1.0;
-        s.SEED[ND].y = 0.0;
-        s.SEEDM1[ND] = 0.0;
-      }
+    if (threadIdx.x == 0) {                       // identity entry for tiny arguments
+      s.SEED[ND].x = T(1);
+      s.SEED[ND].y = T(0);
+      s.SEEDM1[ND] = T(0);
+    }
   }
 }
-// binary64 seed entry from the staged tables
+// seed entries from the staged tables
 TF_DEV SeedE64 seed_entry(const STab<double>& tb, int i) {
   return SeedE64{tb.SEED[i].x, tb.SEEDM1[i], tb.SEED[i].y};
 }
-TF_DEV float2 seed_entry(const STab<float>& tb, int i) { return tb.SEED[i]; }
+TF_DEV SeedE32 seed_entry(const STab<float>& tb, int i) {
+  return SeedE32{tb.SEED[i].x, tb.SEEDM1[i], tb.SEED[i].y};
+}
 
 template <class T, class V> TF_DEV TF<T> tv(V a) { return mk(a.x, a.y); }
 
@@ -831,29 +832,24 @@ TF_DEV TF<f2> ldpair(const float2* t, int i0, int i1) {
 
 TF_DEV f2 seed_log1p_p(const STab<float>& tb, f2 a) {
   constexpr int B = TF32_SEED_BITS, NB = 1 << B;
-  f2 f = add(splat(1.0f), a);
-  f2 clo = sub(a, sub(f, splat(1.0f)));
+  const f2 f = add(splat(1.0f), a);
   int idx[2];
-  bool small[2];
-  float ax[2] = {lo(a), hi(a)}, fx[2] = {lo(f), hi(f)};
+  const float ax[2] = {lo(a), hi(a)}, fx[2] = {lo(f), hi(f)};
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    uint32_t fb = ubits(fx[h]);
-    int i = (((int)(fb >> 23) - 126) << B) | (int)((fb >> (23 - B)) & (NB - 1u));
-    small[h] = fabsf(ax[h]) < 0x1p-8f;                    // |a| < 2^-8 (FP pipe)
-    idx[h] = small[h] ? NB : min(max(i, 0), 2 * NB);
+    const uint32_t fb = ubits(fx[h]);
+    const int i = (((int)(fb >> 23) - 126) << B) | (int)((fb >> (23 - B)) & (NB - 1u));
+    idx[h] = fabsf(ax[h]) < 0x1p-8f ? 2 * NB + 1 : min(max(i, 0), 2 * NB);   // FP pipe test
   }
-  const TF<f2> t = ldpair(tb.SEED, idx[0], idx[1]);
-  const f2 ic = t.v;
-  f2 r = fmaop(f, ic, splat(-1.0f));
-  r = pk(small[0] ? ax[0] : lo(r), small[1] ? ax[1] : hi(r));
-  f2 q = mul(r, r);                                       // seed_poly<float>
+  const TF<f2> t = ldpair(tb.SEED, idx[0], idx[1]);       // (invc, logc)
+  const f2 m1 = TF_SPLIT_LDS ? pk(lds32(&tb.SEEDM1[idx[0]]), lds32(&tb.SEEDM1[idx[1]]))
+                             : pk(tb.SEEDM1[idx[0]], tb.SEEDM1[idx[1]]);
+  const f2 r = fmaop(a, t.v, m1);                          // (1 + a) invc - 1, one rounding
+  const f2 q = mul(r, r);                                  // seed_poly<float>
   f2 pp = fmaop(r, splat(-0.25f), splat(0x1.555556p-2f));
   pp = fmaop(r, pp, splat(-0.5f));
   pp = fmaop(q, pp, r);
-  const f2 lc = pk(small[0] ? 0.0f : lo(t.e), small[1] ? 0.0f : hi(t.e));
-  const f2 cl = pk(small[0] ? 0.0f : lo(clo), small[1] ? 0.0f : hi(clo));
-  return add(lc, fmaop(cl, ic, pp));
+  return add(t.e, pp);
 }
 
 // pexpm10_raw(mx), in-band branch (expcore.py:142-146), on a lane pair:

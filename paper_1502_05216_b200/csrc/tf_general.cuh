@@ -315,11 +315,11 @@ TF_DEV float seed_poly(float r) {   // degree 4
   p = fmaop(r, p, -0.5f);
   return fmaop(q, p, r);
 }
-// binary64: the table entry also carries invc - 1 (exact: invc is in [1/2, 2]),
+// The table entry also carries invc - 1 (exact: invc is in [1/2, 2]),
 // so the reduced argument r = (1 + a) invc - 1 is one FMA on a itself,
 // fma(a, invc, invc - 1), rounded once -- no split of 1 + a into f + clo and
-// no clo / f correction term (8 FP64 ops instead of 11).  Entry 2 NB + 1 is the
-// identity (invc 1, log 0) used for |a| < 2^-11, where r = a exactly.
+// no clo / f correction term (8 FP ops instead of 11).  Entry 2 NB + 1 is the
+// identity (invc 1, log 0) used for |a| < 2^-11 (binary32: 2^-8), where r = a.
 struct SeedE64 { double invc, invcm1, logc; };
 template <class Get> TF_DEV double seed_log1p_t(double a, Get get) {
   constexpr int B = TF64_SEED_BITS, NB = 1 << B;
@@ -333,18 +333,18 @@ template <class Get> TF_DEV double seed_log1p_t(double a, Get get) {
   double p = seed_poly(r);
   return add(t.logc, p);
 }
-template <class Get> TF_DEV float seed_log1p_t(float a, Get get) {
-  float f = add(1.0f, a);
-  float clo = sub(a, sub(f, 1.0f));
-  uint32_t h = ubits(f);
+struct SeedE32 { float invc, invcm1, logc; };
+template <class Get> TF_DEV float seed_log1p_t(float a, Get get) {   // as binary64
   constexpr int B = TF32_SEED_BITS, NB = 1 << B;
+  float f = add(1.0f, a);
+  uint32_t h = ubits(f);
   int idx = (((int)(h >> 23) - 126) << B) | (int)((h >> (23 - B)) & (NB - 1u));
-  bool small = ahi(a) < 0x3b800000u;                  // |a| < 2^-8
-  idx = small ? NB : min(max(idx, 0), 2 * NB);
-  float2 t = get(idx);
-  float r = small ? a : fmaop(f, t.x, -1.0f);
+  bool small = fabsf(a) < 0x1p-8f;                    // |a| < 2^-8
+  idx = small ? 2 * NB + 1 : min(max(idx, 0), 2 * NB);
+  const SeedE32 t = get(idx);
+  float r = fmaop(a, t.invc, t.invcm1);
   float p = seed_poly(r);
-  return add(small ? 0.0f : t.y, fmaop(small ? 0.0f : clo, t.x, p));
+  return add(t.logc, p);
 }
 // exact path: table seed on [-1/2, 1] (bit-identical to the fast kernels),
 // CUDA log1p elsewhere (non-finite / out-of-domain arguments only)
@@ -358,7 +358,12 @@ TF_DEV double seed_log1p(double x) {
   return log1p(x);
 }
 TF_DEV float seed_log1p(float x) {
-  if (x >= -0.5f && x <= 1.0f) return seed_log1p_t(x, [](int i) { return __ldg(&g_SEED32[i]); });
+  if (x >= -0.5f && x <= 1.0f)
+    return seed_log1p_t(x, [](int i) {
+      if (i == TF32_SEED_COUNT) return SeedE32{1.0f, 0.0f, 0.0f};
+      const float2 t = __ldg(&g_SEED32[i]);
+      return SeedE32{t.x, sub(t.x, 1.0f), t.y};
+    });
   return log1pf(x);
 }
 
