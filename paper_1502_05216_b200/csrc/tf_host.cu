@@ -43,8 +43,12 @@ struct HostPipe {
   void* buf[RING][4] = {};
 };
 
-HostPipe g_pipe[MAX_DEV];
-std::mutex g_pipe_mu[MAX_DEV];
+// A small pool of pipelines per device: concurrent calls from different host
+// threads (e.g. two independent functions of one step) each take a free
+// pipeline, so one call's fill and drain overlap the other's copies.
+constexpr int POOL = 2;
+HostPipe g_pipe[MAX_DEV][POOL];
+std::mutex g_pipe_mu[MAX_DEV][POOL];
 
 bool dotted_fn(int fn) {
   return fn == TF_FN_PEXP0 || fn == TF_FN_TEXP0 || fn == TF_FN_PEXPM10 || fn == TF_FN_TEXPM10 ||
@@ -101,8 +105,20 @@ extern "C" TF_API int tf_eval_host(int fn, int width, const void* x0, const void
   const int64_t c = chunk > 0 ? (chunk < n ? chunk : n) : (DEFAULT_CHUNK < n ? DEFAULT_CHUNK : n);
   const bool copy_x1 = !dotted || (x1 && x1 != x0);
 
-  std::lock_guard<std::mutex> lk(g_pipe_mu[dev]);
-  HostPipe& p = g_pipe[dev];
+  std::unique_lock<std::mutex> lk;
+  int slot = -1;
+  for (int i = 0; i < POOL && slot < 0; ++i) {
+    std::unique_lock<std::mutex> t(g_pipe_mu[dev][i], std::try_to_lock);
+    if (t.owns_lock()) {
+      lk = std::move(t);
+      slot = i;
+    }
+  }
+  if (slot < 0) {                                 // all busy: queue on the first
+    slot = 0;
+    lk = std::unique_lock<std::mutex>(g_pipe_mu[dev][0]);
+  }
+  HostPipe& p = g_pipe[dev][slot];
   int rc = setup(p, c * sz);
   if (rc) return rc;
   // start after the work already queued on the caller's stream

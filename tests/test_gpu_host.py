@@ -132,3 +132,26 @@ def test_host_pipeline_orders_after_caller_stream(cuda):
     _lib.check(rc, "tf_eval_host")
     np.testing.assert_array_equal(z0.numpy().view(np.uint8), r0.view(np.uint8))
     np.testing.assert_array_equal(z1.numpy().view(np.uint8), r1.view(np.uint8))
+
+
+def test_host_pipeline_concurrent_callers(cuda):
+    """Calls from several host threads at once take different pipelines of the
+    per-device pool (or queue on a busy one): every result equals the
+    device-pointer path bit for bit."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+
+    jobs = [(fn, 64 if k % 2 == 0 else 32, k) for k, fn in enumerate(FNS * 2)]
+    data = {j: _inputs(j[0], j[1], 300_001 + 17 * j[2], seed=j[2]) for j in jobs}
+
+    def run(j):
+        torch.cuda.set_device(cuda)
+        return _host(j[0], j[1], *data[j], chunk=1 << 16)
+
+    with ThreadPoolExecutor(4) as pool:
+        got = list(pool.map(run, jobs))
+    for j, (z0, z1) in zip(jobs, got):
+        r0, r1 = _device_ref(j[0], j[1], *data[j])
+        assert np.array_equal(z0.view(np.uint8), r0.view(np.uint8)), j
+        assert np.array_equal(z1.view(np.uint8), r1.view(np.uint8)), j
