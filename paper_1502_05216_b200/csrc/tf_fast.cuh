@@ -1453,35 +1453,73 @@ TF_DEV bool alt_log1p_exact1p(const STab<double>& tb, double y0, double y1, doub
   }
 }
 
-template <int FN>
-TF_DEV bool fast_alt64(const STab<double>& tb, double x0, double x1, double& z0, double& z1) {
+// DR queued elements per lane at once (independent chains: the drain's
+// evaluation is latency-bound with one)
+template <int FN, int DR>
+TF_DEV void fast_alt64_v(const STab<double>& tb, const double (&x0)[DR], const double (&x1)[DR],
+                         double (&z0)[DR], double (&z1)[DR], bool (&ok)[DR]) {
   using T = double;
-  if constexpr (sizeof(T) == 8 && (FN == FN_TLOG1P || FN == FN_TLOG1PP || FN == FN_PLOG1P)) {
-    if (alt_log1p_exact1p<FN>(tb, x0, x1, z0, z1)) return true;
+  constexpr bool L1P = FN == FN_TLOG1P || FN == FN_TLOG1PP || FN == FN_PLOG1P;
+  // log1p family: the unified branch below admits |y1| <= 2^-52 |1 + y0| (its
+  // d test) with one evaluation; alt_log1p_exact1p costs two and serves the
+  // arguments with a larger tail (cfg 2's clamp value y0 = -1 + 2^-52), so it
+  // goes first only for those
+  bool small_d[DR], pre[DR];
+#pragma unroll
+  for (int k = 0; k < DR; ++k) {
+    small_d[k] = true;
+    pre[k] = false;
+    if constexpr (L1P) {
+      small_d[k] = zbits(x1[k]) || bexp(x1[k]) + 52 <= bexp(add(1.0, x0[k]));
+      if (!small_d[k]) pre[k] = alt_log1p_exact1p<FN>(tb, x0[k], x1[k], z0[k], z1[k]);
+    }
   }
-  T a[1] = {x0}, b[1] = {x1}, r0[1], r1[1];
-  bool ok[1];
+  T r0[DR], r1[DR];
   if constexpr (FN == FN_TEXPM1 || FN == FN_TEXPM10 || FN == FN_PEXPM1) {
-    fast_texpm1_fb<1>(tb, a, b, r0, r1, ok);
+    fast_texpm1_fb<DR>(tb, x0, x1, r0, r1, ok);
     if constexpr (FN == FN_PEXPM1) {
-      TF<T> r = fast_two_sum_u(r0[0], r1[0]);
-      r0[0] = r.v;
-      r1[0] = r.e;
+#pragma unroll
+      for (int k = 0; k < DR; ++k) {
+        TF<T> r = fast_two_sum_u(r0[k], r1[k]);
+        r0[k] = r.v;
+        r1[k] = r.e;
+      }
     }
   } else if constexpr (FN == FN_PEXPM10) {
-    fast_texpm1_fb<1, true>(tb, a, b, r0, r1, ok);
+    fast_texpm1_fb<DR, true>(tb, x0, x1, r0, r1, ok);
   } else if constexpr (FN == FN_TLOG || FN == FN_TLOG0) {       // top binade
-    fast_tlog<T, 1, true, false, false, true>(tb, a, b, r0, r1, ok);
+    fast_tlog<T, DR, true, false, false, true>(tb, x0, x1, r0, r1, ok);
   } else if constexpr (FN == FN_TLOGP) {
-    fast_tlog<T, 1, false, false, false, true>(tb, a, b, r0, r1, ok);
+    fast_tlog<T, DR, false, false, false, true>(tb, x0, x1, r0, r1, ok);
   } else if constexpr (FN == FN_PLOG0 || FN == FN_PLOG) {
-    fast_tlog<T, 1, false, true, false, true>(tb, a, b, r0, r1, ok);
+    fast_tlog<T, DR, false, true, false, true>(tb, x0, x1, r0, r1, ok);
   } else {
     constexpr bool RENORM = FN == FN_TLOG1P;
     constexpr bool PM = FN == FN_PLOG1P0 || FN == FN_PLOG1P;
     constexpr bool INNER = !(FN == FN_TLOG1P0 || FN == FN_PLOG1P0);
-    fast_tlog1p<T, 1, RENORM, PM, INNER, 1>(tb, a, b, r0, r1, ok);
+    fast_tlog1p<T, DR, RENORM, PM, INNER, 1>(tb, x0, x1, r0, r1, ok);
   }
+#pragma unroll
+  for (int k = 0; k < DR; ++k) {
+    if (pre[k]) {
+      ok[k] = true;                                 // z0 / z1 set by alt_log1p_exact1p
+      continue;
+    }
+    if constexpr (L1P)
+      if (!ok[k] && small_d[k]) {
+        ok[k] = alt_log1p_exact1p<FN>(tb, x0[k], x1[k], z0[k], z1[k]);
+        continue;
+      }
+    z0[k] = r0[k];
+    z1[k] = r1[k];
+  }
+}
+
+template <int FN>
+TF_DEV bool fast_alt64(const STab<double>& tb, double x0, double x1, double& z0, double& z1) {
+  double a[1] = {x0}, b[1] = {x1}, r0[1], r1[1];
+  bool ok[1];
+  fast_alt64_v<FN, 1>(tb, a, b, r0, r1, ok);
   z0 = r0[0];
   z1 = r1[0];
   return ok[0];
