@@ -865,10 +865,11 @@ TF_DEV TF<f2> pexpm10_inband_p(const STab<float>& tb, f2 mx) {
 }
 
 // rn_guard<TF_TOL32_LOG> on a lane pair: packed sums and crossing test
+template <int TOL = TF_TOL32_LOG>
 TF_DEV f2 rn_guard_p(f2 h, f2 l, bool (&hard)[2]) {
   const f2 zs = add(h, l);
   const f2 rho = add(sub(h, zs), l);
-  const f2 cr = fmaop(rho, splat(kguard<TF_TOL32_LOG>()), zs);
+  const f2 cr = fmaop(rho, splat(kguard<TOL>()), zs);
   hard[0] = lo(cr) != lo(zs);
   hard[1] = hi(cr) != hi(zs);
   return zs;
@@ -1297,6 +1298,99 @@ TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const f
   }
 }
 
+// ------------------------------------- binary32 texp / texpm1, lane pairs
+// fast_texp<float> / fast_texpm1<float> with the recombination on f32x2
+// pairs too: C and E entries of the two lanes loaded straight into register
+// pairs (ldpair), the two twofold products, the value-part guard and z1 packed.
+// The per-lane operation sequence is exactly the scalar kernels'.
+TF_DEV TF<f2> taylor_exp_p(f2 yp) {                 // taylor_exp_v<float>'s packed body
+  const f2 nyp = -yp;
+  f2 s = add(yp, splat(6.0f));
+  s = add(mul(s, yp), splat(30.0f));
+  TF<f2> tp = mk(s, splat(0.0f));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) tp = t_add_d_u(t_mul_d_p(tp, yp, nyp), splat(c_texp32[k]));
+  return tp;
+}
+
+template <int VW, bool PM = false>
+TF_DEV void fast_texp_p(const STab<float>& tb, const float (&x0)[VW], const float (&x1)[VW],
+                        float (&z0)[VW], float (&z1)[VW], bool (&ok)[VW]) {
+  static_assert(VW % 2 == 0, "lane pairs");
+  float y[VW];
+  int m[VW], n[VW];
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    ok[e] = x0[e] >= -__uint_as_float(B32_TEXP_NEG) && x0[e] <= __uint_as_float(B32_TEXP_POS) &&
+            fabsf(x1[e]) < __uint_as_float(B32_X1_TINY);
+    decomp_exp_u(ok[e] ? x0[e] : 0.0f, m[e], n[e], y[e]);
+  }
+#pragma unroll
+  for (int p = 0; p < VW / 2; ++p) {
+    const int a = 2 * p, b = 2 * p + 1;
+    const TF<f2> t = taylor_exp_p(pk(y[a], y[b]));
+    const TF<f2> ct = t_mul_u(ldpair(tb.C, n[a] - P<float>::C_LO, n[b] - P<float>::C_LO), t);
+    const TF<f2> ev = ldpair(tb.E, m[a] - P<float>::E_LO, m[b] - P<float>::E_LO);
+    const TF<f2> v = t_mul_u(ev, ct);
+    if constexpr (PM) {
+      const TF<f2> r = fast_two_sum_u(v.v, v.e);
+      z0[a] = lo(r.v); z0[b] = hi(r.v);
+      z1[a] = lo(r.e); z1[b] = hi(r.e);
+      continue;
+    }
+    // value part near the subnormal range from the 2^64-scaled coarse table
+    const bool sc0 = m[a] <= -35, sc1 = m[b] <= -35;
+    const TF<f2> es = ldpair(tb.ESC, sc0 ? m[a] - TF32_ESC_LO : 0, sc1 ? m[b] - TF32_ESC_LO : 0);
+    const TF<f2> vs = t_mul_u(mk(sel2(sc0, sc1, es.v, ev.v), sel2(sc0, sc1, es.e, ev.e)), ct);
+    bool hard[2];
+    const f2 zz = mul(rn_guard_p<TF_TOL32_EXP>(vs.v, vs.e, hard),
+                      pk(sc0 ? 0x1p-64f : 1.0f, sc1 ? 0x1p-64f : 1.0f));
+    ok[a] = ok[a] && !hard[0];
+    ok[b] = ok[b] && !hard[1];
+    const f2 t1 = pk(t1_tiny(x1[a]), t1_tiny(x1[b]));
+    const f2 zr = add(mul(zz, t1), add(v.e, sub(v.v, zz)));   // explog.py:125
+    z0[a] = lo(zz); z0[b] = hi(zz);
+    z1[a] = lo(zr); z1[b] = hi(zr);
+  }
+}
+
+template <int VW, bool PM = false>
+TF_DEV void fast_texpm1_p(const STab<float>& tb, const float (&x0)[VW], const float (&x1)[VW],
+                          float (&z0)[VW], float (&z1)[VW], bool (&ok)[VW]) {
+  static_assert(VW % 2 == 0, "lane pairs");
+  float y[VW];
+  int m[VW], n[VW];
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    ok[e] = fabsf(x0[e]) > __uint_as_float(B32_LN2) && x0[e] >= -__uint_as_float(B32_LO) &&
+            x0[e] <= __uint_as_float(B32_TEXP_POS) && fabsf(x1[e]) < __uint_as_float(B32_X1_TINY);
+    decomp_exp_u(ok[e] ? x0[e] : 1.0f, m[e], n[e], y[e]);
+  }
+#pragma unroll
+  for (int p = 0; p < VW / 2; ++p) {
+    const int a = 2 * p, b = 2 * p + 1;
+    const TF<f2> t = taylor_exp_p(pk(y[a], y[b]));
+    const TF<f2> v = t_mul_u(ldpair(tb.E, m[a] - P<float>::E_LO, m[b] - P<float>::E_LO),
+                             t_mul_u(ldpair(tb.C, n[a] - P<float>::C_LO, n[b] - P<float>::C_LO), t));
+    const TF<f2> w = t_add_d_u(v, splat(-1.0f));             // expcore.py:147
+    if constexpr (PM) {
+      const TF<f2> r = fast_two_sum_u(w.v, w.e);
+      z0[a] = lo(r.v); z0[b] = hi(r.v);
+      z1[a] = lo(r.e); z1[b] = hi(r.e);
+      continue;
+    }
+    bool hard[2];
+    const f2 zz = rn_guard_p<TF_TOL32_EXP>(w.v, w.e, hard);
+    ok[a] = ok[a] && !hard[0];
+    ok[b] = ok[b] && !hard[1];
+    const f2 tail = add(w.e, sub(w.v, zz));
+    const f2 t1 = pk(t1_tiny(x1[a]), t1_tiny(x1[b]));
+    const f2 zr = add(mul(add(zz, splat(1.0f)), t1), tail);   // explog.py:159-160
+    z0[a] = lo(zz); z0[b] = hi(zz);
+    z1[a] = lo(zr); z1[b] = hi(zr);
+  }
+}
+
 // Per-warp exchange buffer for class-sorting the 32 x VW elements of a warp
 // iteration (binary32 tlog1p, whose in-band / out-of-band split is ~50/50).
 template <int VW> struct Xch {
@@ -1534,6 +1628,10 @@ TF_DEV bool fast_alt(const STab<T>& tb, T x0, T x1, T& z0, T& z1) {
   }
 }
 
+// binary32 exponential families with the recombination on lane pairs
+#ifndef TF_EXP32_PACKED
+#define TF_EXP32_PACKED 1
+#endif
 // binary32 tlog1p / tlog1pp run on lane pairs (fast_tlog1p_p); the other
 // log1p-family functions are class-sorted (tlog1p_sorted)
 #ifndef TF_TLOG1P32_PACKED
@@ -1555,15 +1653,20 @@ __host__ __device__ constexpr bool log1p_fn(int fn) {
 template <class T, int FN, int VW>
 TF_DEV void fast_eval(const STab<T>& tb, void* xch, const T (&x0)[VW], const T (&x1)[VW],
                       T (&z0)[VW], T (&z1)[VW], bool (&ok)[VW]) {
+  constexpr bool PK = sizeof(T) == 4 && VW % 2 == 0 && TF_EXP32_PACKED;
   if constexpr (FN == FN_TEXP || FN == FN_TEXPP || FN == FN_TEXP0 || FN == FN_PEXP) {
-    fast_texp<VW>(tb, x0, x1, z0, z1, ok);
+    if constexpr (PK) fast_texp_p<VW>(tb, x0, x1, z0, z1, ok);
+    else fast_texp<VW>(tb, x0, x1, z0, z1, ok);
   } else if constexpr (FN == FN_PEXP0) {
-    fast_texp<VW, true>(tb, x0, x1, z0, z1, ok);
+    if constexpr (PK) fast_texp_p<VW, true>(tb, x0, x1, z0, z1, ok);
+    else fast_texp<VW, true>(tb, x0, x1, z0, z1, ok);
   } else if constexpr (FN == FN_TEXPM1 || FN == FN_TEXPM1P || FN == FN_TEXPM10 ||
                        FN == FN_PEXPM1) {
-    fast_texpm1<VW>(tb, x0, x1, z0, z1, ok);
+    if constexpr (PK) fast_texpm1_p<VW>(tb, x0, x1, z0, z1, ok);
+    else fast_texpm1<VW>(tb, x0, x1, z0, z1, ok);
   } else if constexpr (FN == FN_PEXPM10) {
-    fast_texpm1<VW, true>(tb, x0, x1, z0, z1, ok);
+    if constexpr (PK) fast_texpm1_p<VW, true>(tb, x0, x1, z0, z1, ok);
+    else fast_texpm1<VW, true>(tb, x0, x1, z0, z1, ok);
   } else if constexpr (FN == FN_TLOG || FN == FN_TLOG0) {
     if constexpr (sizeof(T) == 4 && VW % 2 == 0) fast_tlog_p<VW, true>(tb, x0, x1, z0, z1, ok);
     else fast_tlog<T, VW>(tb, x0, x1, z0, z1, ok);
