@@ -34,6 +34,10 @@ namespace tf {
 #ifndef TF_VW64_LOG
 #define TF_VW64_LOG 4
 #endif
+// binary64 log1p family: drain through a called function (drain_call)
+#ifndef TF_DRAIN_CALL_LOG1P64
+#define TF_DRAIN_CALL_LOG1P64 1
+#endif
 #ifndef TF_VW32_LOG
 #define TF_VW32_LOG TF_VW32
 #endif
@@ -199,6 +203,29 @@ TF_DEV void drain(const STab<T>& tb, const uint32_t* q, int cnt, const T* __rest
   }
 }
 
+// The same drain as a called function: its register needs then do not shape
+// the main loop's allocation.  Measured per kernel (tools/variant_rates.sh):
+// +1.6% for binary64 tlog1p (the headline's dominant kernel), but -4% for
+// binary64 tlog and -1..2% for the binary32 exponentials, so only the binary64
+// log1p family calls it.
+template <class T, int FN>
+__device__ __noinline__ void drain_call(const STab<T>& tb, const uint32_t* q, int cnt,
+                                        const T* __restrict__ x0, const T* __restrict__ x1,
+                                        T* __restrict__ z0, T* __restrict__ z1, int lane,
+                                        bool count, bool mark, bool force) {
+  drain<T, FN>(tb, q, cnt, x0, x1, z0, z1, lane, count, mark, force);
+}
+template <class T, int FN>
+TF_DEV void drain_any(const STab<T>& tb, const uint32_t* q, int cnt, const T* __restrict__ x0,
+                      const T* __restrict__ x1, T* __restrict__ z0, T* __restrict__ z1,
+                      int lane, bool count, bool mark, bool force) {
+  constexpr bool CALL = TF_DRAIN_CALL_LOG1P64 && sizeof(T) == 8 &&
+                        (FN == FN_TLOG1P || FN == FN_TLOG1PP || FN == FN_PLOG1P ||
+                         FN == FN_TLOG1P0 || FN == FN_PLOG1P0);
+  if constexpr (CALL) drain_call<T, FN>(tb, q, cnt, x0, x1, z0, z1, lane, count, mark, force);
+  else drain<T, FN>(tb, q, cnt, x0, x1, z0, z1, lane, count, mark, force);
+}
+
 // Drop the first 32 entries of a warp's rare queue (entries [32, qn) move
 // down by 32): every lane reads its entries of all chunks, then writes.
 template <int QCAP>
@@ -343,7 +370,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
 #if TF_TIMELINE
       ++tl_drains;
 #endif
-      drain<T, FN>(tb, q, 32, x0, x1, z0, z1, lane, count, mark, force);
+      drain_any<T, FN>(tb, q, 32, x0, x1, z0, z1, lane, count, mark, force);
       __syncwarp();
       queue_shift<QCAP>(q, qn, lane);
       qn -= 32;
@@ -366,7 +393,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   while (qn > 0) {
     __syncwarp();
     int c = qn < 32 ? qn : 32;
-    drain<T, FN>(tb, q, c, x0, x1, z0, z1, lane, count, mark, force);
+    drain_any<T, FN>(tb, q, c, x0, x1, z0, z1, lane, count, mark, force);
     __syncwarp();
     queue_shift<QCAP>(q, qn, lane);
     qn -= c;
