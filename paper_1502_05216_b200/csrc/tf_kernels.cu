@@ -140,9 +140,16 @@ template <class T, int VW, int BLOCK, bool ASYNC, bool XCH, int STAGES> struct E
 #ifndef TF_BLOCK32_LOG1P
 #define TF_BLOCK32_LOG1P TF_BLOCK
 #endif
+// CTA size of the lane-pair binary32 tlog1p / tlog1pp kernels (768: +1%, within
+// box noise; 512: -2%)
+#ifndef TF_BLOCK32_LOG1P_PK
+#define TF_BLOCK32_LOG1P_PK TF_BLOCK
+#endif
 template <class T, int FN, int VW> struct EvalCfg {
   static constexpr int BLOCK =
-      (sizeof(T) == 4 && log1p_fn(FN)) ? TF_BLOCK32_LOG1P : KCfg<T, VW>::BLOCK;
+      (sizeof(T) == 4 && log1p_fn(FN))         ? TF_BLOCK32_LOG1P
+      : (sizeof(T) == 4 && log1p_packed32(FN)) ? TF_BLOCK32_LOG1P_PK
+                                               : KCfg<T, VW>::BLOCK;
   static constexpr int MINB = BLOCK == KCfg<T, VW>::BLOCK ? KCfg<T, VW>::MINB : 1;
   static constexpr bool ASYNC = VW * sizeof(T) % 16 == 0;
   static constexpr bool XCH = log1p_fn(FN) && sizeof(T) == 4 && VW >= 2;
