@@ -117,8 +117,9 @@ TF_API int tf_eval(int fn, int width, const void* x0, const void* x1, void* z0, 
  * through a three-stage chunk pipeline on the current device (H2D, kernel,
  * D2H on three streams over a ring of device buffers) that starts after the
  * work queued on `stream`; the call returns when z0, z1 hold the results.
- * chunk = elements per pipeline chunk, 0 = default (2^18).  Dotted functions
- * take x1 = NULL.  Thread-safe (calls on one device serialise). */
+ * chunk = elements per pipeline chunk, 0 = default (2^20).  Dotted functions
+ * take x1 = NULL.  Thread-safe: each device has two pipelines, so two calls
+ * from different host threads run concurrently; further calls queue. */
 TF_API int tf_eval_host(int fn, int width, const void* x0, const void* x1, void* z0, void* z1,
                         int64_t n, int64_t chunk, void* stream, int flags);
 
