@@ -823,7 +823,18 @@ TF_DEV float lds32(const float* p) {
   asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(r) : "r"((unsigned)__cvta_generic_to_shared(p)));
   return r;
 }
-TF_DEV TF<f2> ldpair(const float2* t, int i0, int i1) {
+// TF_BOUNDS_CHECK (diagnostic builds, tools/sanitize_target.py): trap on a table
+// index outside the staged table; the pool has no compute-sanitizer
+#ifndef TF_BOUNDS_CHECK
+#define TF_BOUNDS_CHECK 0
+#endif
+TF_DEV void bounds(int i, int n) {
+  if (TF_BOUNDS_CHECK && (unsigned)i >= (unsigned)n) __trap();
+}
+template <int N>
+TF_DEV TF<f2> ldpair(const float2 (&t)[N], int i0, int i1) {
+  bounds(i0, N);
+  bounds(i1, N);
   if (TF_SPLIT_LDS)
     return mk(pk(lds32(&t[i0].x), lds32(&t[i1].x)), pk(lds32(&t[i0].y), lds32(&t[i1].y)));
   const float2 a = t[i0], b = t[i1];
@@ -842,6 +853,8 @@ TF_DEV f2 seed_log1p_p(const STab<float>& tb, f2 a) {
     idx[h] = fabsf(ax[h]) < 0x1p-8f ? 2 * NB + 1 : min(max(i, 0), 2 * NB);   // FP pipe test
   }
   const TF<f2> t = ldpair(tb.SEED, idx[0], idx[1]);       // (invc, logc)
+  bounds(idx[0], TF32_SEED_COUNT + 1);
+  bounds(idx[1], TF32_SEED_COUNT + 1);
   const f2 m1 = TF_SPLIT_LDS ? pk(lds32(&tb.SEEDM1[idx[0]]), lds32(&tb.SEEDM1[idx[1]]))
                              : pk(tb.SEEDM1[idx[0]], tb.SEEDM1[idx[1]]);
   const f2 r = fmaop(a, t.v, m1);                          // (1 + a) invc - 1, one rounding

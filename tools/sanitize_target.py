@@ -22,3 +22,22 @@ for width in (64, 32):
                     lib._launch(fn, a0, a1, z0, z1, a0.numel(), torch.cuda.current_stream().cuda_stream, flags)
         torch.cuda.synchronize()
 print("sanitize target ok")
+
+# every function, both widths, on raw random bit patterns (NaN, inf, subnormal
+# and out-of-domain operands reach every rejected-lane path of the fast kernels)
+from paper_1502_05216_b200 import FUNCTION_NAMES
+rng = np.random.default_rng(5)
+for width in (64, 32):
+    it = np.uint64 if width == 64 else np.uint32
+    ft = np.float64 if width == 64 else np.float32
+    n = 4099
+    b0 = rng.integers(0, np.iinfo(it).max, n, dtype=it, endpoint=True).view(ft)
+    b1 = rng.integers(0, np.iinfo(it).max, n, dtype=it, endpoint=True).view(ft)
+    x0 = torch.from_numpy(b0.copy()).to(dev); x1 = torch.from_numpy(b1.copy()).to(dev)
+    lib = api(width)
+    for fn in FUNCTION_NAMES:
+        z0 = torch.empty_like(x0); z1 = torch.empty_like(x0)
+        for flags in (0, _lib.FLAG_FORCE_EXACT):
+            lib._launch(fn, x0, x1, z0, z1, n, torch.cuda.current_stream().cuda_stream, flags)
+    torch.cuda.synchronize()
+print("sanitize bit patterns ok")
