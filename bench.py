@@ -1,29 +1,40 @@
 #!/usr/bin/env python
 """Benchmark of the B200 twofold hot path (driver contract: one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1], the single-GPU config the metric is quoted
-on): one STEP = texpm1 and tlog1p over the cfg-2 float64 twofolds, N = 2^24
-each (x0 = +-s*10^-e, s~U[1,10), e~U{0..300}; tlog1p clamped to
-[-1+2^-52, 1e300]; x1 = x0*u*2^-53).  Inputs are generated on the device by
-the shard-invariant generator (rank r of G owns global elements
-[r*N, (r+1)*N) -- weak scaling, no collective on the hot path).  The 512 MiB
-of inputs per step exceed the 126 MB L2, so no flush is needed.
+Headline workload: BASELINE.json configs[4] ("cfg5"), the largest config and the
+one BASELINE.json shards over 1/2/4/8 GPUs.  One STEP = texp and tlog over 2^30
+binary64 twofolds each (x0 ~ U[-700, 700] for texp, 2^e*m log-uniform stand-in
+for tlog, x1 = x0*u*2^-53, plus 1% special values -- +-0, +-inf, NaN,
+subnormals, exp thresholds -- at seeded positions).  The 2^30 elements of each
+function are sharded contiguously over the ranks (rank r of G owns global
+elements [r*2^30/G, (r+1)*2^30/G): strong scaling, no collective on the hot
+path).  Inputs are generated on the device by the shard-invariant generator;
+16 GiB of inputs per function per step exceed the 126 MB L2 (no flush needed).
 
-  value  = elements evaluated per second, whole job (sum over ranks), CUDA
-           events on the launching stream, max over ranks; the step's two
-           independent functions run on two streams (--streams 2), so one
-           launch's tail overlaps the next one's ramp;
-  e2e    = the same metric through the public API with pinned HOST buffers
-           (H2D + kernels + D2H inside the timed region, wall clock);
-  per_function = every (function, width) kernel at its own config and size
-           (2^24 / 2^26 binary64, 2^28 binary32; config 1 at 2^26, its 2^20
-           launch-overhead regime separately as cfg1_small), same timing rules;
-  roofline = the dominant kernel's algorithmic FP64 op rate vs the measured
-           FP64 FMA-pipe peak of this GPU (tf_fma_peak), plus its HBM rate;
-  cpu_baseline = the CPU oracle (C port of the reference algorithm, all host
-           threads) on a bounded sample of the same workload.
+  value    = elements evaluated per second, whole job (2 * 2^30 / step time),
+             CUDA events on the launching stream, max over ranks; the step's two
+             independent launches run on two streams so one's tail overlaps the
+             other's ramp;
+  e2e      = the same metric through the public API, api(64).texp / .tlog on
+             pinned HOST tensors (out= pinned host tensors): H2D + kernel + D2H
+             inside the timed region (tf_eval_host pipeline), max over ranks;
+  roofline = the dominant kernel (tlog): algorithmic FP64 ops per launch over its
+             CUDA-event duration, against this GPU's FP64 pipe peak measured in
+             the same run (tf_fma_peak; MEASURED_PEAKS.json has no FP64 figure);
+             traffic = ncu dram bytes of the same kernel (profiles/);
+  cpu_baseline = the CPU port of the reference algorithm (oracle/, "dv" backend,
+             bit-exact to the reference package) on all host threads, timed on a
+             bounded prefix of rank 0's slice; its outputs are also the parity
+             reference for that prefix (parity_cfg5);
+  per_function = the eight (function, width) kernels at the north-star size
+             2^28 on their own configs' distributions;
+  parity_f32 = config 4 samples vs the reference-equivalent oracle (numpy libm)
+             and vs the CR-sim oracle (correctly rounded libm).
 
-`--impl reference` times that CPU port alone (rank 0) on the same workload.
+`--impl reference` times the CPU port alone (rank 0; the reference package is
+pure Python and ~2000x slower still -- it is timed too, on a small sample, when
+baseline/_ref holds it) on the same workload and config.
+`--gpus N` without torchrun relaunches itself under torch.distributed.run.
 """
 
 from __future__ import annotations
@@ -33,6 +44,7 @@ import ctypes
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -43,27 +55,27 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 # algorithmic FP ops per element (reference op sequence,
-# config branch mix), the roofline numerators.
+# config branch mix), the roofline numerators.  cfg5: the general-path count
+# over the 99% non-special elements, specials counted as 0 ops (conservative:
+# zeros, subnormals and the thresholds do run the full path in the reference).
 ALG_OPS = {("texp", 64): 123.0, ("texpm1", 64): 111.1, ("tlog", 64): 151.4,
            ("tlog1p", 64): 142.1, ("texp", 32): 66.0, ("texpm1", 32): 73.9,
            ("tlog", 32): 106.0, ("tlog1p", 32): 110.0}
-HEADLINE = (("texpm1", "cfg2_texpm1_f64"), ("tlog1p", "cfg2_tlog1p_f64"))
-PER_FN = {
-    ("texp", 64): "cfg1_texp_f64", ("texpm1", 64): "cfg2_texpm1_f64",
-    ("tlog", 64): "cfg3_tlog_f64", ("tlog1p", 64): "cfg2_tlog1p_f64",
-    ("texp", 32): "cfg4_texp_f32", ("texpm1", 32): "cfg4_texpm1_f32",
-    ("tlog", 32): "cfg4_tlog_f32", ("tlog1p", 32): "cfg4_tlog1p_f32",
-}
+ALG_OPS_CFG5 = {"texp": 0.99 * 123.0, "tlog": 0.99 * 152.0}
+HEADLINE = (("texp", "exp64s"), ("tlog", "logu64s"))
+N_TOTAL = 1 << 30          # elements per function (BASELINE.json configs[4])
+# per-function kernels at the north-star size 2^28 (BASELINE.json north_star)
+PER_FN = (("texp", 64, "exp64"), ("texpm1", 64, "pow10_64"), ("tlog", 64, "log64"),
+          ("tlog1p", 64, "pow10c_64"), ("texp", 32, "exp32"), ("texpm1", 32, "exp32"),
+          ("tlog", 32, "log32"), ("tlog1p", 32, "log32"))
+N_PER_FN = 1 << 28
+SEED = 2024
+METRIC = "twofold evals/sec (cfg5: texp+tlog float64, 2^30 each, 1% specials)"
 # input arrays each tf_eft op streams (a0 + a1/b0/b1 as the op needs them)
 EFT_ARRAYS_IN = {"fast_two_sum": 2, "two_sum": 2, "two_diff": 2, "two_prod": 2, "split": 1,
                  "renorm_fast": 2, "renorm": 2, "t_add": 4, "t_add_d": 3, "t_mul": 4,
                  "t_mul_d": 3, "t_div": 4, "t_sqrt": 2}
 EFT_BACKEND_OPS = ("two_prod", "t_mul", "t_mul_d", "t_div", "t_sqrt")
-N_HEAD = 1 << 24
-# per-function sizes: each config's own N (BASELINE.json), except config 1's
-# 2^20 (the launch-overhead regime, measured separately as cfg1_small)
-N_CFG = {"cfg1_texp_f64": 1 << 26}
-SEED = 2024
 
 
 def _peaks():
@@ -72,6 +84,15 @@ def _peaks():
             return json.load(f)
     except OSError:
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+def config_for(world: int) -> dict:
+    """The workload description both arms print (identical for the same N)."""
+    return {"workload": "cfg5: texp + tlog over 2^30 float64 twofolds each, 1% specials",
+            "elements_per_function": N_TOTAL, "elements_per_function_per_gpu": N_TOTAL // world,
+            "global_elements_per_step": 2 * N_TOTAL,
+            "parallelism": f"contiguous shards x{world}, no collective on the hot path",
+            "l2": "inputs 16 GiB per function per step > 126 MB L2 (no flush needed)"}
 
 
 class ClockSampler:
@@ -123,7 +144,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
         names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": names, "samples": len(self.samples)}
+                "sm_min_mhz": min(self.samples), "reasons": names, "samples": len(self.samples)}
 
 
 def dist_env():
@@ -133,9 +154,69 @@ def dist_env():
     return rank, world, local
 
 
+def _r(x, nd=4):
+    """Compact floats for the JSON line (the driver keeps its tail)."""
+    if x is None:
+        return None
+    return float(f"{x:.{nd}g}")
+
+
 # ---------------------------------------------------------------- reference arm
+def _py_ref_worker(args):
+    """Time the reference package itself (scalar calls, its own convention,
+    audit.py:343-349) on one chunk of the cfg5 stream."""
+    path, fn, dist, start, count = args
+    sys.path.insert(0, path)
+    from twofold import api
+
+    from paper_1502_05216_b200 import workloads
+
+    x0, x1 = workloads.generate(dist, start, count, seed=SEED)
+    f = getattr(api(64), fn)
+    pairs = list(zip(x0.tolist(), x1.tolist()))
+    t = time.perf_counter()
+    for p in pairs:
+        f(p)
+    return time.perf_counter() - t
+
+
+def python_reference(nt: int, per_proc: int) -> dict | None:
+    """The reference package (pkg/src/twofold, installed in baseline/_ref) on
+    a small sample: nt processes, each evaluating per_proc elements of each
+    function in a loop of scalar calls."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "twofold")):
+        return {"unavailable": "baseline/_ref not installed"}
+    import multiprocessing as mp
+
+    jobs = [(path, fn, dist, k * per_proc, per_proc) for fn, dist in HEADLINE for k in range(nt)]
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(nt) as pool:
+        pool.map(_py_ref_worker, [(path, fn, dist, 0, 64) for fn, dist in HEADLINE] * nt)
+        t = time.perf_counter()
+        busy = pool.map(_py_ref_worker, jobs)
+        wall = time.perf_counter() - t
+    n = len(jobs) * per_proc
+    return {"value": _r(n / wall), "unit": "elements/s", "processes": nt,
+            "us_per_call_1core": _r(sum(busy) / n * 1e6),
+            "sample": f"{per_proc} elements x {nt} processes per function, scalar calls",
+            "backend": "dv (no gmpy2 / math.fma on the box)"}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
-    """CPU port of the reference algorithm (oracle/, kind "port"), all host threads."""
+    """CPU port of the reference algorithm (oracle/, kind "port"), all host
+    threads, on rank 0; other ranks exit without work."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
@@ -144,11 +225,8 @@ def run_reference(args):
 
     O.build()
     nt = O.default_threads()
-    sample = args.ref_sample
-    data = {}
-    for fn, cfg in HEADLINE:
-        _, width, dist, _ = workloads.CONFIGS[cfg]
-        data[fn] = workloads.generate(dist, 0, sample, seed=SEED)
+    sample = min(args.ref_sample, N_TOTAL)
+    data = {fn: workloads.generate(dist, 0, sample, seed=SEED) for fn, dist in HEADLINE}
     times = []
     for it in range(args.warmup + args.steps):
         t = time.perf_counter()
@@ -158,31 +236,31 @@ def run_reference(args):
             times.append(time.perf_counter() - t)
     per_step = statistics.median(times)
     value = 2 * sample / per_step
+    pyref = python_reference(nt, args.py_ref_sample) if args.py_ref_sample > 0 else None
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg-2 generator)",
-        "config": {"workload": "cfg2: texpm1 + tlog1p over float64 twofolds",
-                   "elements_per_function": sample, "sample_of": N_HEAD},
+        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg-5 generator)",
+        "config": config_for(world),
         "cpu_baseline": {"value": value, "unit": "elements/s", "cores": nt, "kind": "port",
-                         "sample": f"{sample} elements per function per step "
-                                   f"(bounded sample of the 2^24-element cfg-2 step)"},
+                         "cpu": cpu_model(),
+                         "sample": f"{sample} elements per function per step (prefix of the "
+                                   f"2^30-element cfg-5 stream), C port of the reference "
+                                   f"algorithm, {nt} threads"},
         "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "reference_python": pyref,
     }
     print(json.dumps(line), flush=True)
     return 0
-
-
-METRIC = "twofold evals/sec (cfg2: texpm1+tlog1p float64, N=2^24 each)"
 
 
 # ---------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
 
-    from paper_1502_05216_b200 import DOTTED_ARG, FAMILIES, Twofold, _lib, api, family_of, workloads
+    from paper_1502_05216_b200 import Twofold, _lib, api, workloads
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -195,6 +273,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
     f64 = api(64)
+    peaks = _peaks()
 
     def gen(dist_name, n, dt, start):
         x0 = torch.empty(n, dtype=dt, device=dev)
@@ -218,20 +297,17 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- headline step: texpm1 + tlog1p over cfg-2, N per rank
-    n = args.n
-    start = rank * n
+    def events():
+        return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    # ---- headline step: texp + tlog over this rank's cfg-5 slice
+    start, n = shard(N_TOTAL, rank, world)
     ins, outs = {}, {}
-    for fn, cfg in HEADLINE:
-        _, width, dname, _ = workloads.CONFIGS[cfg]
+    for fn, dname in HEADLINE:
         ins[fn] = gen(dname, n, torch.float64, start)
         outs[fn] = (torch.empty(n, dtype=torch.float64, device=dev),
                     torch.empty(n, dtype=torch.float64, device=dev))
     torch.cuda.synchronize()
-
-    # The step's two functions are independent: with --streams 2 the second
-    # runs on its own stream, so its CTAs take each SM as soon as the first
-    # kernel's CTA there retires (the two launches' ramp and tail overlap).
     streams = [stream] + [torch.cuda.Stream(dev) for _ in range(args.streams - 1)]
 
     def step(evs=None):
@@ -259,10 +335,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    launch_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                  for _ in HEADLINE] for _ in range(args.steps)]
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
+    launch_ev = [[events() for _ in HEADLINE] for _ in range(args.steps)]
+    t0, t1 = events()
     with ClockSampler(local) as clk:
         t0.record(stream)
         for s in range(args.steps):
@@ -272,97 +346,98 @@ def run_ours(args):
     barrier()
     ms_total = max_over_ranks(t0.elapsed_time(t1))
     ms_step = ms_total / args.steps
-    value = 2 * n * world / (ms_step * 1e-3)
-    if len(streams) > 1:
-        # overlapped launches stretch each other's events: the per-kernel
-        # durations (roofline) come from the same steps run serialised
-        streams[1:] = []
-        torch.cuda.synchronize()
-        for s in range(args.steps):
-            step(launch_ev[s])
-        torch.cuda.synchronize()
+    value = 2 * N_TOTAL / (ms_step * 1e-3)
+    # per-kernel durations (roofline) from the same steps run serialised on one
+    # stream (overlapped launches stretch each other's events)
+    streams[1:] = []
+    torch.cuda.synchronize()
+    for s in range(args.steps):
+        step(launch_ev[s])
+    torch.cuda.synchronize()
     kern_ms = {fn: max_over_ranks(statistics.mean(
                    launch_ev[s][k][0].elapsed_time(launch_ev[s][k][1]) for s in range(args.steps)))
                for k, (fn, _) in enumerate(HEADLINE)}
+    # share of the slice the exact path evaluated, counted in one extra launch
+    exact_frac = {}
+    cnt = ctypes.c_ulonglong(0)
+    for fn, _ in HEADLINE:
+        _lib.check(L.tf_exact_count(ctypes.byref(cnt), 1), "tf_exact_count")
+        f64._launch(fn, *ins[fn], *outs[fn], n, sp, flags=_lib.FLAG_COUNT_EXACT)
+        torch.cuda.synchronize()
+        _lib.check(L.tf_exact_count(ctypes.byref(cnt), 1), "tf_exact_count")
+        exact_frac[fn] = _r(cnt.value / n, 3)
 
-    # ---- FP64 / FP32 FMA-pipe peak of this GPU (roofline denominator)
-    peak = {}
+    # ---- FP64 / FP32 pipe peak of this GPU (roofline denominator)
+    peak, peak_by_op = {}, {}
     buf = torch.zeros(4, dtype=torch.float64, device=dev)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak_by_op = {}
     for width in (64, 32):
         blocks, iters = sms * 8, 4096 if width == 64 else 8192
         for op, name in ((0, "fma"), (1, "add"), (2, "mul")):
             code = width + 100 * op
             _lib.check(L.tf_fma_peak(code, buf.data_ptr(), blocks, iters, sp), "peak")
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0, e1 = events()
             e0.record(stream)
             _lib.check(L.tf_fma_peak(code, buf.data_ptr(), blocks, iters, sp), "peak")
             e1.record(stream)
             torch.cuda.synchronize()
             peak_by_op[f"f{width}_{name}"] = blocks * 256 * iters * 8 / (e0.elapsed_time(e1) * 1e-3)
-        # the roofline denominator: the fastest of add / mul / fma (conservative)
-        peak[width] = max(peak_by_op[f"f{width}_{n}"] for n in ("fma", "add", "mul"))
+        peak[width] = max(peak_by_op[f"f{width}_{k}"] for k in ("fma", "add", "mul"))
 
-    # ---- per-function kernel rates at their configs
-    per_fn, siblings = {}, {}
-    if not args.headline_only:
-        for (fn, width), cfg in PER_FN.items():
-            _, _, dname, _ = workloads.CONFIGS[cfg]
-            m = N_CFG.get(cfg, workloads.CONFIGS[cfg][3])
-            dt = torch.float64 if width == 64 else torch.float32
-            a0, a1 = gen(dname, m, dt, rank * m)
-            z0, z1 = torch.empty_like(a0), torch.empty_like(a1)
-            lib = api(width)
+    # ---- roofline of the dominant kernel
+    dom = max(kern_ms, key=kern_ms.get)
+    dom_ms = kern_ms[dom]
+    ops = ALG_OPS_CFG5[dom] * n / (dom_ms * 1e-3)
+    gbs = 32 * n / (dom_ms * 1e-3) / 1e9
+    roof = {"bound": "fp64", "kernel": f"k_eval<double,{dom}>", "achieved": ops / 1e12,
+            "peak": peak[64] / 1e12, "unit": "TFLOP/s", "frac": ops / peak[64],
+            "traffic": _traffic(dom, n), "ops_per_element": ALG_OPS_CFG5[dom],
+            "elements_per_launch": n, "launch_ms": dom_ms,
+            "peak_source": "measured in this run: tf_fma_peak, best of DADD/DMUL/DFMA chains",
+            "hbm_gbs": gbs, "hbm_frac": gbs / peaks["hbm_gbs"]}
 
-            def time_fn(name, reps):
-                b1 = a0 if name in DOTTED_ARG else a1      # plain argument: x1 unused
-                for _ in range(max(3, args.warmup)):
-                    lib._launch(name, a0, b1, z0, z1, m, sp)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                for _ in range(reps):
-                    lib._launch(name, a0, b1, z0, z1, m, sp)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                return max_over_ranks(e0.elapsed_time(e1) / reps)
+    # ---- parity of this rank's slice prefix against the CPU port (which is
+    # also the timed cpu_baseline on rank 0); one small merge over the ranks
+    from oracle import oracle as O
 
-            ms = time_fn(fn, max(5, min(args.steps, 50)))
-            rate = m * world / (ms * 1e-3)
-            ops = ALG_OPS[(fn, width)] * m / (ms * 1e-3)
-            gbs = (32 if width == 64 else 16) * m / (ms * 1e-3) / 1e9
-            per_fn[f"{fn}_f{width}"] = {
-                "config": cfg, "elements": m, "ms": ms, "elements_per_s": rate,
-                "alg_gops": ops / 1e9, "fp_pipe_frac": ops / peak[width],
-                "hbm_gbs": gbs, "hbm_frac": gbs / _peaks()["hbm_gbs"]}
-            if not args.no_siblings:
-                # the other four functions of the family, same inputs (a dotted
-                # function reads x0 only)
-                for name in FAMILIES[family_of(fn)]:
-                    if name == fn:
-                        continue
-                    sms = time_fn(name, 5)
-                    siblings[f"{name}_f{width}"] = {
-                        "config": cfg, "elements": m, "ms": sms,
-                        "elements_per_s": m * world / (sms * 1e-3),
-                        "vs_" + fn: ms / sms}
-            del a0, a1, z0, z1
+    O.build()
+    nt = O.default_threads()
+    m = min(args.parity_sample, n)
+    cpu = None
+    parity5 = {}
+    for fn, _ in HEADLINE:
+        x0 = ins[fn][0][:m].cpu().numpy()
+        x1 = ins[fn][1][:m].cpu().numpy()
+        tc = time.perf_counter()
+        r0, r1 = O.evaluate(fn, 64, x0, x1, backend="dv", nthreads=nt)
+        cpu_s = time.perf_counter() - tc
+        parity5[fn] = _parity_device(L, dev, sp, outs[fn][0][:m], outs[fn][1][:m], r0, r1, 64,
+                                     args.parity_host)
+        parity5[fn]["cpu_s"] = cpu_s
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu_s = sum(parity5[fn].pop("cpu_s") for fn, _ in HEADLINE)
+        cpu = {"value": _r(2 * m / cpu_s), "unit": "elements/s", "cores": nt, "kind": "port",
+               "cpu": cpu_model(),
+               "sample": f"{m} elements of each function (prefix of the cfg-5 slice), C port "
+                         f"of the reference algorithm ('dv' backend), {nt} threads"}
+    for fn, _ in HEADLINE:
+        parity5[fn].pop("cpu_s", None)
+        parity5[fn] = _reduce(parity5[fn], dev)
 
-    # ---- config 1 at its own size (2^20 texp f64): the launch-overhead regime,
-    # eager launches vs one CUDA graph of 100 launches (SURVEY.md 8(d))
+    # ---- config 1 at its own size (2^20 texp f64): launch-overhead regime,
+    # eager launches vs one CUDA graph of 100 launches
     small = None
     if not args.headline_only:
-        m = 1 << 20
-        a0, a1 = gen("exp64", m, torch.float64, rank * m)
+        ms_ = 1 << 20
+        a0, a1 = gen("exp64", ms_, torch.float64, rank * ms_)
         z0, z1 = torch.empty_like(a0), torch.empty_like(a0)
-        f = api(64)
         for _ in range(5):
-            f._launch("texp", a0, a1, z0, z1, m, sp)
+            f64._launch("texp", a0, a1, z0, z1, ms_, sp)
         reps = 100
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1 = events()
         e0.record(stream)
         for _ in range(reps):
-            f._launch("texp", a0, a1, z0, z1, m, sp)
+            f64._launch("texp", a0, a1, z0, z1, ms_, sp)
         e1.record(stream)
         torch.cuda.synchronize()
         eager_ms = max_over_ranks(e0.elapsed_time(e1) / reps)
@@ -372,7 +447,7 @@ def run_ours(args):
         with torch.cuda.stream(gs):
             with torch.cuda.graph(g, stream=gs):
                 for _ in range(reps):
-                    f._launch("texp", a0, a1, z0, z1, m, gs.cuda_stream)
+                    f64._launch("texp", a0, a1, z0, z1, ms_, gs.cuda_stream)
         g.replay()
         torch.cuda.synchronize()
         e0.record(stream)
@@ -380,157 +455,117 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
         graph_ms = max_over_ranks(e0.elapsed_time(e1) / reps)
-        small = {"config": "cfg1_texp_f64", "elements": m,
-                 "eager_ms": eager_ms, "eager_elements_per_s": m * world / (eager_ms * 1e-3),
-                 "graph_ms": graph_ms, "graph_elements_per_s": m * world / (graph_ms * 1e-3),
-                 "graph_launches": reps}
+        small = {"n": ms_, "eager_gps": _r(ms_ * world / (eager_ms * 1e-3) / 1e9),
+                 "graph_gps": _r(ms_ * world / (graph_ms * 1e-3) / 1e9)}
         del a0, a1, z0, z1, g
 
-    # ---- config 5: texp and tlog over 2^30 binary64 twofolds with 1% special
-    # values, sharded contiguously across the ranks (strong scaling: the total is
-    # fixed, each rank evaluates its 2^30 / N slice; no collective on the path)
-    cfg5 = {}
-    if not args.headline_only and not args.no_cfg5:
-        for cname in ("cfg5_texp_f64", "cfg5_tlog_f64"):
-            fn, _, dname, total = workloads.CONFIGS[cname]
-            per = total // world
-            a0, a1 = gen(dname, per, torch.float64, rank * per)
-            z0, z1 = torch.empty_like(a0), torch.empty_like(a0)
-            for _ in range(max(3, args.warmup)):
-                f64._launch(fn, a0, a1, z0, z1, per, sp)
-            reps = max(3, min(args.steps, 10))
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            barrier()
-            e0.record(stream)
-            for _ in range(reps):
-                f64._launch(fn, a0, a1, z0, z1, per, sp)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ms = max_over_ranks(e0.elapsed_time(e1) / reps)
-            # share of the slice the exact path evaluated (the specials and the
-            # rare fast-path rejects), counted in one extra launch
-            cnt = ctypes.c_ulonglong(0)
-            _lib.check(L.tf_exact_count(ctypes.byref(cnt), 1), "tf_exact_count")
-            f64._launch(fn, a0, a1, z0, z1, per, sp, flags=2)   # TF_FLAG_COUNT_EXACT
-            torch.cuda.synchronize()
-            _lib.check(L.tf_exact_count(ctypes.byref(cnt), 1), "tf_exact_count")
-            cfg5[cname] = {"elements_total": per * world, "elements_per_rank": per, "ms": ms,
-                           "elements_per_s": per * world / (ms * 1e-3), "scaling": "strong",
-                           "exact_path_fraction_rank0": cnt.value / per}
-            del a0, a1, z0, z1
-        torch.cuda.empty_cache()
-
-    # ---- element-wise EFT / twofold arithmetic ops (HBM-bound streaming)
-    eft_rates = {}
-    if not args.headline_only and not args.no_eft:
-        m = 1 << 25
-        for width in (64, 32):
-            dt = torch.float64 if width == 64 else torch.float32
-            sz = 8 if width == 64 else 4
-            ops_in = [torch.empty(m, dtype=dt, device=dev).uniform_(1.0, 2.0) for _ in range(4)]
-            z0, z1 = torch.empty_like(ops_in[0]), torch.empty_like(ops_in[0])
-            ptrs = [a.data_ptr() for a in ops_in]
-            for op, code in _lib.OP_CODES.items():
-                for backend in ((0, 1) if op in EFT_BACKEND_OPS else (0,)):
-                    def go():
-                        _lib.check(L.tf_eft(code, width, backend, *ptrs, z0.data_ptr(),
-                                            z1.data_ptr(), m, sp), "tf_eft")
-                    for _ in range(3):
-                        go()
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record(stream)
-                    for _ in range(10):
-                        go()
-                    e1.record(stream)
-                    torch.cuda.synchronize()
-                    ms = max_over_ranks(e0.elapsed_time(e1) / 10)
-                    gbs = (EFT_ARRAYS_IN[op] + 2) * sz * m / (ms * 1e-3) / 1e9
-                    name = f"{op}{'_dv' if backend else ''}_f{width}"
-                    eft_rates[name] = {"elements_per_s": m * world / (ms * 1e-3), "ms": ms,
-                                       "hbm_gbs": gbs, "hbm_frac": gbs / _peaks()["hbm_gbs"]}
-            del ops_in, z0, z1
     # ---- end to end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        host, hout = {}, {}
+        del outs
+        torch.cuda.empty_cache()
+        host = {}
         for fn, _ in HEADLINE:
             a0, a1 = ins[fn]
-            host[fn] = (a0.cpu().pin_memory(), a1.cpu().pin_memory())
-            hout[fn] = (torch.empty(n, dtype=torch.float64).pin_memory(),
-                        torch.empty(n, dtype=torch.float64).pin_memory())
-        # warm the pipeline (ring buffers, pinned-page mappings)
-        for _ in range(2):
+            h0 = torch.empty(n, dtype=torch.float64, pin_memory=True)
+            h1 = torch.empty(n, dtype=torch.float64, pin_memory=True)
+            h0.copy_(a0)
+            h1.copy_(a1)
+            host[fn] = (h0, h1)
+        del ins
+        torch.cuda.empty_cache()
+        hout = (torch.empty(n, dtype=torch.float64, pin_memory=True),
+                torch.empty(n, dtype=torch.float64, pin_memory=True))
+        for _ in range(min(args.warmup, 2)):
             for fn, _ in HEADLINE:
-                getattr(f64, fn)(Twofold(*host[fn]), out=hout[fn])
-        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+                getattr(f64, fn)(Twofold(*host[fn]), out=hout)
         barrier()
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
         tw = time.perf_counter()
         for _ in range(e2e_steps):
             for fn, _ in HEADLINE:
-                z = getattr(f64, fn)(Twofold(*host[fn]), out=hout[fn])
-        torch.cuda.synchronize()
+                z = getattr(f64, fn)(Twofold(*host[fn]), out=hout)
+                _ = float(z.value[n - 1])          # the step's result is on the host
         t_e2e = max_over_ranks((time.perf_counter() - tw) / e2e_steps)
-        _ = float(z.value[0])  # the result is on the host
-        e2e = {"value": 2 * n * world / t_e2e, "unit": "elements/s",
+        e2e = {"value": 2 * N_TOTAL / t_e2e, "unit": "elements/s",
                "h2d_bytes_per_step": 2 * 2 * n * 8, "d2h_bytes_per_step": 2 * 2 * n * 8,
-               "ms_per_step": t_e2e * 1e3, "path": "api(64).texpm1/tlog1p(Twofold(pinned CPU tensors), out=pinned CPU tensors)"}
+               "ms_per_step": _r(t_e2e * 1e3), "steps": e2e_steps,
+               "path": "api(64).texp/tlog(Twofold(pinned host tensors), out=pinned host tensors)"}
+        del host, hout
+    else:
+        del ins, outs
+    torch.cuda.empty_cache()
 
-    # ---- parity sample + the one small NCCL reduce of error statistics
-    stats = parity_sample(args, ins, outs, n, rank, world, dev)
+    # ---- per-function kernel rates at 2^28 (north-star size)
+    per_fn = {}
+    if not args.headline_only:
+        for fn, width, dname in PER_FN:
+            mm = N_PER_FN
+            dt = torch.float64 if width == 64 else torch.float32
+            a0, a1 = gen(dname, mm, dt, rank * mm)
+            z0, z1 = torch.empty_like(a0), torch.empty_like(a1)
+            lib = api(width)
+            for _ in range(max(3, args.warmup)):
+                lib._launch(fn, a0, a1, z0, z1, mm, sp)
+            reps = max(5, min(args.steps, 20))
+            e0, e1 = events()
+            e0.record(stream)
+            for _ in range(reps):
+                lib._launch(fn, a0, a1, z0, z1, mm, sp)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = max_over_ranks(e0.elapsed_time(e1) / reps)
+            fp = ALG_OPS[(fn, width)] * mm / (ms * 1e-3) / peak[width]
+            hbm = (32 if width == 64 else 16) * mm / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"]
+            # bound = the slower of the two rooflines (north_star)
+            bound = "fp" if ALG_OPS[(fn, width)] / peak[width] > \
+                (32 if width == 64 else 16) / (peaks["hbm_gbs"] * 1e9) else "hbm"
+            per_fn[f"{fn}{width}"] = [_r(mm * world / (ms * 1e-3) / 1e9), bound,
+                                      _r(fp if bound == "fp" else hbm, 3), _r(fp, 3), _r(hbm, 3)]
+            del a0, a1, z0, z1
+        torch.cuda.empty_cache()
 
-    # ---- roofline of the dominant kernel
-    dom = max(kern_ms, key=kern_ms.get)
-    dom_ms = kern_ms[dom]
-    ops = ALG_OPS[(dom, 64)] * n / (dom_ms * 1e-3)
-    gbs = 32 * n / (dom_ms * 1e-3) / 1e9
-    traffic = args.traffic
-    if traffic is None:
-        try:
-            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                rec = json.load(f).get(f"k_eval<double,{dom}>")
-            if rec:  # per launch of the same size (ncu --set full capture)
-                traffic = rec["traffic_bytes"] * n / rec["elements"]
-        except (OSError, ValueError, KeyError):
-            traffic = None
-    roof = {"bound": "fp64", "kernel": f"k_eval<double,{dom}>",
-            "achieved": ops / 1e12, "peak": peak[64] / 1e12, "unit": "TFLOP/s",
-            "frac": ops / peak[64], "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
-            "algorithmic_bytes": 32 * n,
-            "ops_per_element": ALG_OPS[(dom, 64)], "elements_per_launch": n,
-            "launch_ms": dom_ms, "peak_source": "measured tf_fma_peak, best of DADD/DMUL/DFMA chains (this GPU, this run)",
-            "hbm_achieved_gbs": gbs, "hbm_peak_gbs": _peaks()["hbm_gbs"],
-            "hbm_frac": gbs / _peaks()["hbm_gbs"]}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args)
+    # ---- binary32 parity (config 4 samples) vs the reference and CR-sim oracles
+    par32 = {}
+    if not args.headline_only and args.parity32_sample > 0:
+        m32 = args.parity32_sample
+        for fn, width, dname in PER_FN:
+            if width != 32:
+                continue
+            a0, a1 = gen(dname, m32, torch.float32, rank * m32)
+            z = getattr(api(32), fn)((a0, a1))
+            torch.cuda.synchronize()
+            z0, z1 = z.value.cpu().numpy(), z.error.cpu().numpy()
+            x0, x1 = a0.cpu().numpy(), a1.cpu().numpy()
+            ref = O.evaluate(fn, 32, x0, x1, backend="dv", nthreads=nt)
+            crs = O.evaluate(fn, 32, x0, x1, backend="fma", libm32="cr", nthreads=nt)
+            par32[fn] = {"ref": _compact(_reduce(_host_compare(z0, z1, *ref, 32), dev)),
+                         "crsim": _compact(_reduce(_host_compare(z0, z1, *crs, 32), dev))}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded shard-invariant cfg-2 generator, on device)",
-            "config": {"workload": "cfg2: texpm1 + tlog1p over float64 twofolds",
-                       "elements_per_function_per_gpu": n, "global_elements_per_step": 2 * n * world,
-                       "parallelism": f"contiguous shards x{world}, no collective on the hot path",
-                       "l2": "inputs 512 MiB/step > 126 MB L2 (no flush needed)",
-                       "streams": args.streams,
-                       "kernel_ms": "per-kernel launch durations from the same steps run on one stream"},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded shard-invariant cfg-5 generator, on device)",
+            "config": config_for(world),
             "gpu_launches": len(HEADLINE) * args.steps,
-            "kernel_ms": kern_ms,
+            "kernel_ms": {k: _r(v) for k, v in kern_ms.items()},
+            "exact_path_frac": exact_frac,
             "clocks": clk.summary(),
-            "roofline": roof,
-            "fp_peak_tops": {k: v / 1e12 for k, v in peak_by_op.items()},
+            "roofline": {k: (_r(v) if isinstance(v, float) else v) for k, v in roof.items()},
+            "fp_peak_tops": {k: _r(v / 1e12) for k, v in peak_by_op.items()},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "per_function": per_fn,
-            "siblings": siblings,
-            "eft_ops": eft_rates, "cfg5": cfg5,
             "cfg1_small": small,
-            "parity_sample": stats,
+            "parity_legend": PARITY_LEGEND,
+            "parity_cfg5": {fn: _compact(v) for fn, v in parity5.items()},
+            "per_function_legend": "G elem/s, bound, frac of bound, fp frac, hbm frac (2^28)",
+            "parity_f32_legend": "vs the reference (numpy libm) / vs CR-sim, 2^22 of cfg 4",
+            "per_function": per_fn,
+            "parity_f32": par32,
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line, separators=(",", ":")), flush=True)
     if world > 1:
         import torch.distributed as dist
 
@@ -538,73 +573,131 @@ def run_ours(args):
     return 0
 
 
-def parity_sample(args, ins, outs, n, rank, world, dev):
-    """Check a seeded sample of each rank's outputs against the CPU oracle, then
-    combine the per-rank counters with the one small all-reduce of the run
-    (paper_1502_05216_b200.dist.reduce_stats; NCCL here, gloo in the tests)."""
-    from oracle import oracle as O
-    from oracle.compare import compare
-    from paper_1502_05216_b200.dist import reduce_stats
+def shard(total: int, rank: int, world: int) -> tuple[int, int]:
+    """This rank's contiguous slice [start, start + n) of the global index
+    range (paper_1502_05216_b200.dist.shard_range)."""
+    from paper_1502_05216_b200.dist import shard_range
 
-    m = min(args.parity_sample, n)
-    out = {}
-    for fn, _ in HEADLINE:
-        x0 = ins[fn][0][:m].cpu().numpy()
-        x1 = ins[fn][1][:m].cpu().numpy()
-        z0 = outs[fn][0][:m].cpu().numpy()
-        z1 = outs[fn][1][:m].cpu().numpy()
-        r0, r1 = O.evaluate(fn, 64, x0, x1, backend="dv")
-        r = compare(z0, z1, r0, r1, 64)
-        out[fn] = reduce_stats(r, device=dev)
-        out[fn].pop("bad_idx", None)
-        out[fn].pop("z0_ulp_hist", None)
-    out["oracle"] = "CPU port, dv backend (bit-exact vs reference goldens)"
+    return shard_range(total, rank, world)
+
+
+def _traffic(fn, n):
+    """ncu dram read+write bytes per launch of k_eval<double,fn> on the cfg-5
+    inputs, from the committed `ncu --set full` capture (profiles/), scaled
+    to this launch's element count (traffic per element is size-independent
+    for a streaming kernel); None without a capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            rec = json.load(f).get(f"cfg5_{fn}_f64")
+        if rec:
+            return rec["traffic_bytes"] * n / rec["elements"]
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
+
+
+def _parity_device(L, dev, sp, z0, z1, r0, r1, width, host_n):
+    """Parity counters of GPU (z0, z1) against reference (r0, r1): the whole
+    sample on the device (tf_compare), plus the host comparator's finer
+    statistics (ulp histogram, given-z0-match counts, worst error) on the
+    first host_n elements."""
+    import torch
+
+    from paper_1502_05216_b200 import _lib
+
+    rel, guard = (2.0 ** -95, 2 * 2.0 ** -1074) if width == 64 else (2.0 ** -42, 2 * 2.0 ** -149)
+    t0 = torch.from_numpy(r0).to(dev)
+    t1 = torch.from_numpy(r1).to(dev)
+    st = torch.zeros(6, dtype=torch.int64, device=dev)
+    _lib.check(L.tf_compare(width, z0.data_ptr(), z1.data_ptr(), t0.data_ptr(), t1.data_ptr(),
+                            z0.numel(), rel, guard, st.data_ptr(), sp), "tf_compare")
+    torch.cuda.synchronize()
+    c = st.tolist()
+    out = {"n": c[0], "z0_mismatch": c[1], "z0_gt1ulp": c[2], "tol_violations": c[3],
+           "class_mismatch": c[4], "z1_bit_mismatch": c[5]}
+    k = min(host_n, z0.numel())
+    if k:
+        h = _host_compare(z0[:k].cpu().numpy(), z1[:k].cpu().numpy(), r0[:k], r1[:k], width)
+        out["host_n"] = k
+        for key in ("tol_violations_given_z0_match", "z1_bit_mismatch_given_z0_match",
+                    "worst_rel_log2", "z0_ulp_hist"):
+            out[key] = h[key]
     return out
 
 
-def cpu_baseline(args):
-    from oracle import oracle as O
-    from paper_1502_05216_b200 import workloads
+def _host_compare(z0, z1, r0, r1, width):
+    from oracle.compare import compare
 
-    O.build()
-    nt = O.default_threads()
-    sample = args.ref_sample
-    data = {fn: workloads.generate(workloads.CONFIGS[cfg][2], 0, sample, seed=SEED)
-            for fn, cfg in HEADLINE}
-    for fn, _ in HEADLINE:
-        O.evaluate(fn, 64, *data[fn], backend="dv", nthreads=nt)
-    t = time.perf_counter()
-    for fn, _ in HEADLINE:
-        O.evaluate(fn, 64, *data[fn], backend="dv", nthreads=nt)
-    dt = time.perf_counter() - t
-    return {"value": 2 * sample / dt, "unit": "elements/s", "cores": nt, "kind": "port",
-            "sample": f"{sample} elements each of texpm1 and tlog1p (cfg-2 generator), "
-                      f"C port of the reference algorithm (oracle/), {nt} threads"}
+    return compare(z0, z1, r0, r1, width)
+
+
+def _reduce(stats, dev):
+    """Merge a rank's parity record over all ranks (the one small collective
+    of the run: an 80-byte all-gather merged by tf_reduce_stats)."""
+    from paper_1502_05216_b200.dist import reduce_stats
+
+    s = dict(stats)
+    s.pop("bad_idx", None)
+    return reduce_stats(s, device=dev)
+
+
+PARITY_LEGEND = ("n, z0 mismatches, z0 beyond 1 ulp, tol violations, tol violations given "
+                 "z0 match, class mismatches, worst log2 rel, z0 ulp histogram")
+
+
+def _compact(s):
+    """One parity record as a short list (PARITY_LEGEND order)."""
+    hist = s.get("z0_ulp_hist")
+    return [s.get("n"), s.get("z0_mismatch"), s.get("z0_gt1ulp"), s.get("tol_violations"),
+            s.get("tol_violations_given_z0_match"), s.get("class_mismatch"),
+            _r(s.get("worst_rel_log2")),
+            {str(a): b for a, b in hist.items()} if isinstance(hist, dict) else None]
+
+
+def relaunch(args) -> int:
+    """--gpus N outside torchrun: run this script under torch.distributed.run
+    with one rank per GPU (the driver's own launch for N > 1)."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--n", type=int, default=N_HEAD, help="elements per function per GPU")
-    ap.add_argument("--ref-sample", type=int, default=1 << 21)
-    ap.add_argument("--parity-sample", type=int, default=1 << 16)
-    ap.add_argument("--e2e-steps", type=int, default=6)
-    ap.add_argument("--traffic", type=float, default=None,
-                    help="ncu dram bytes per launch of the dominant kernel (profiles/)")
+    ap.add_argument("--ref-sample", type=int, default=1 << 25,
+                    help="reference arm: elements per function per step (prefix of the stream)")
+    ap.add_argument("--py-ref-sample", type=int, default=2048,
+                    help="reference arm: elements per process per function for the Python package")
+    ap.add_argument("--parity-sample", type=int, default=1 << 26,
+                    help="cfg-5 elements per function checked against the CPU port")
+    ap.add_argument("--parity-host", type=int, default=1 << 22,
+                    help="of those, elements also run through the host comparator")
+    ap.add_argument("--parity32-sample", type=int, default=1 << 22)
+    ap.add_argument("--e2e-steps", type=int, default=1 << 30)
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cfg5", action="store_true", help="skip the 2^30 config-5 section")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-siblings", action="store_true")
-    ap.add_argument("--no-eft", action="store_true")
     ap.add_argument("--streams", type=int, default=2, choices=(1, 2),
                     help="run the step's two functions on 1 or 2 streams")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        return relaunch(args)
+    if world is not None and int(world) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

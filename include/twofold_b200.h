@@ -136,6 +136,30 @@ TF_API int tf_compare(int width, const void* z0, const void* z1, const void* r0,
                       int64_t n, double rel, double abs_guard, unsigned long long* stats_dev,
                       void* stream);
 
+/* Parity / error statistics of one shard: the tf_compare counters plus the
+ * accuracy audit's (sum, max, count) of relative errors (reference
+ * audit.py:205-269 run_accuracy; SPEC.md "merge of (sum, max, count) is
+ * order-independent").  err_max is -inf when no error was recorded. */
+typedef struct tf_stats {
+  uint64_t n;              /* elements compared */
+  uint64_t z0_mismatch;    /* z0 bit mismatches */
+  uint64_t z0_gt1ulp;      /* z0 mismatches beyond 1 ulp */
+  uint64_t tol_violations; /* |(z0 + z1) - (r0 + r1)| beyond the tolerance */
+  uint64_t class_mismatch; /* non-finite class mismatches */
+  uint64_t z1_mismatch;    /* z1 bit mismatches */
+  uint64_t included;       /* samples in the error sum (audit) */
+  uint64_t warnings;       /* errors above the L0 threshold (audit) */
+  double err_sum;          /* sum of relative errors (audit L1 numerator) */
+  double err_max;          /* max relative error (audit L0, or log2 of it) */
+} tf_stats;
+
+/* Merge nparts shard statistics into *out: counts and sums add, maxima take
+ * the max (NaN entries ignored).  Host memory only, no device work; the
+ * contiguous shards of a multi-GPU run merge to the single-process result
+ * (the one small cross-rank reduction of SURVEY.md 8(e)).  nparts == 0 gives
+ * the empty record. */
+TF_API int tf_reduce_stats(const tf_stats* parts, int64_t nparts, tf_stats* out);
+
 /* FP-pipe calibration: `blocks` CTAs x 256 threads x `iters` x 8 independent
  * ops of the given width; width + 100 selects DADD/FADD chains, width + 200
  * DMUL/FMUL chains, plain width FMA chains. */

@@ -32,7 +32,7 @@ EXPORTS = ("tf_version", "tf_last_error", "tf_init", "tf_texp_f64", "tf_texpm1_f
            "tf_tlog_f64", "tf_tlog1p_f64", "tf_texp_f32", "tf_texpm1_f32", "tf_tlog_f32",
            "tf_tlog1p_f32", "tf_eval", "tf_generate", "tf_compare", "tf_fma_peak",
            "tf_exact_count", "tf_audit_errors", "tf_etalon", "tf_checksum", "tf_eft",
-           "tf_eval_host")
+           "tf_eval_host", "tf_reduce_stats")
 # tf_eft op codes (include/twofold_b200.h TF_OP_*)
 OP_CODES = {"fast_two_sum": 0, "two_sum": 1, "two_diff": 2, "two_prod": 3, "split": 4,
             "renorm_fast": 5, "renorm": 6, "t_add": 7, "t_add_d": 8, "t_mul": 9, "t_mul_d": 10,
@@ -40,6 +40,22 @@ OP_CODES = {"fast_two_sum": 0, "two_sum": 1, "two_diff": 2, "two_prod": 3, "spli
 FAMILY_CODES = {"exp": 0, "expm1": 1, "log": 2, "log1p": 3}
 ETALON_CODES = {"oracle": 0, "lib": 1}
 AUDIT_INCLUDED, AUDIT_FLOOR, AUDIT_DOMAIN, AUDIT_ABSOLUTE = 0, 1, 2, 3
+
+
+
+class TfStats(ctypes.Structure):
+    """struct tf_stats (include/twofold_b200.h): one shard's parity / error statistics."""
+
+    _fields_ = [("n", ctypes.c_uint64), ("z0_mismatch", ctypes.c_uint64),
+                ("z0_gt1ulp", ctypes.c_uint64), ("tol_violations", ctypes.c_uint64),
+                ("class_mismatch", ctypes.c_uint64), ("z1_mismatch", ctypes.c_uint64),
+                ("included", ctypes.c_uint64), ("warnings", ctypes.c_uint64),
+                ("err_sum", ctypes.c_double), ("err_max", ctypes.c_double)]
+
+
+STATS_COUNT_KEYS = ("n", "z0_mismatch", "z0_gt1ulp", "tol_violations", "class_mismatch",
+                    "z1_mismatch", "included", "warnings")
+
 
 _lib = None
 _lock = threading.Lock()
@@ -98,8 +114,20 @@ def load() -> ctypes.CDLL:
         L.tf_eft.restype = i32
         L.tf_eval_host.argtypes = [i32, i32, vp, vp, vp, vp, i64, i64, vp, i32]
         L.tf_eval_host.restype = i32
+        L.tf_reduce_stats.argtypes = [ctypes.POINTER(TfStats), i64, ctypes.POINTER(TfStats)]
+        L.tf_reduce_stats.restype = i32
         _lib = L
         return L
+
+
+def reduce_stats_c(parts: list[TfStats]) -> TfStats:
+    """Merge shard statistics with the C ABI's tf_reduce_stats (host code only:
+    works without a GPU)."""
+    L = load()
+    arr = (TfStats * max(1, len(parts)))(*parts)
+    out = TfStats()
+    check(L.tf_reduce_stats(arr, len(parts), ctypes.byref(out)), "tf_reduce_stats")
+    return out
 
 
 def check(rc: int, what: str) -> None:

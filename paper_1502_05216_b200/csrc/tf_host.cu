@@ -121,6 +121,21 @@ extern "C" TF_API int tf_eval_host(int fn, int width, const void* x0, const void
   HostPipe& p = g_pipe[dev][slot];
   int rc = setup(p, c * sz);
   if (rc) return rc;
+  // On an error after the first enqueue, copies that touch the caller's host
+  // buffers may still be in flight: drain all three streams before returning
+  // (their own status is ignored; the first error is what gets reported), and
+  // forget the ring state so the next call starts clean.
+  struct Drain {
+    HostPipe& p;
+    bool armed = true;
+    ~Drain() {
+      if (!armed) return;
+      cudaStreamSynchronize(p.in);
+      cudaStreamSynchronize(p.comp);
+      cudaStreamSynchronize(p.out);
+      for (int s = 0; s < RING; ++s) p.used[s] = false;
+    }
+  } drain{p};
   // start after the work already queued on the caller's stream
   if (cudaEventRecord(p.entry, static_cast<cudaStream_t>(stream)) != cudaSuccess ||
       cudaStreamWaitEvent(p.in, p.entry, 0) != cudaSuccess)
@@ -155,5 +170,6 @@ extern "C" TF_API int tf_eval_host(int fn, int width, const void* x0, const void
   }
   // the results are on the host when the call returns
   if (cudaStreamSynchronize(p.out) != cudaSuccess) return cuda_check("tf_eval_host: drain");
+  drain.armed = false;
   return TF_OK;
 }

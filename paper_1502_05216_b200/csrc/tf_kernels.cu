@@ -14,6 +14,7 @@
 // status codes with a message in tf_last_error().
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include "tf_fast.cuh"
@@ -129,11 +130,17 @@ template <class T, int VW> struct KCfg {
 };
 
 // shared-memory layout of one k_eval CTA (dynamic: > 48 KB)
+// The rare queue holds each element's index AND its operands (qa, qb): the
+// drain never re-reads x0 / x1 from global memory, so z may alias x element
+// for element (in-place evaluation; the fast path has already overwritten
+// the element by the time it is drained).
 template <class T, int VW, int BLOCK, bool ASYNC, bool XCH, int STAGES> struct EvalSmem {
   static constexpr int WARPS = BLOCK / 32;
   static constexpr int QCAP = 32 + 32 * VW;
   STab<T> tb;
   uint32_t qs[WARPS][QCAP];
+  T qa[WARPS][QCAP];
+  T qb[WARPS][QCAP];
   __align__(16) T stg[ASYNC ? STAGES : 1][2][BLOCK][VW];
   Xch<VW> xch[XCH ? WARPS : 1];
 };
@@ -178,15 +185,15 @@ template <int N> TF_DEV void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// Evaluate the queued rare elements q[0..cnt) (cnt <= 32) with the exact path.
+// Evaluate the queued rare elements (q, qa, qb)[0..cnt) (cnt <= 32) with the
+// exact path; the operands come from the queue, not from x0 / x1.
 template <class T, int FN>
-TF_DEV void drain(const STab<T>& tb, const uint32_t* q, int cnt, const T* __restrict__ x0,
-                  const T* __restrict__ x1, T* __restrict__ z0, T* __restrict__ z1, int lane,
-                  bool count, bool mark, bool force) {
+TF_DEV void drain(const STab<T>& tb, const uint32_t* q, const T* qa, const T* qb, int cnt,
+                  T* z0, T* z1, int lane, bool count, bool mark, bool force) {
   bool exact = false;
   if (lane < cnt) {
     uint32_t i = q[lane];
-    T a = x0[i], b = dotted_fn(FN) ? T(0) : x1[i];
+    T a = qa[lane], b = dotted_fn(FN) ? T(0) : qb[lane];
     if (mark) {  // diagnostics: tag exact-path elements instead of evaluating them
       z0[i] = Lim<T>::qnan();
       z1[i] = T(-12345);
@@ -216,44 +223,44 @@ TF_DEV void drain(const STab<T>& tb, const uint32_t* q, int cnt, const T* __rest
 // binary64 tlog and -1..2% for the binary32 exponentials, so only the binary64
 // log1p family calls it.
 template <class T, int FN>
-__device__ __noinline__ void drain_call(const STab<T>& tb, const uint32_t* q, int cnt,
-                                        const T* __restrict__ x0, const T* __restrict__ x1,
-                                        T* __restrict__ z0, T* __restrict__ z1, int lane,
-                                        bool count, bool mark, bool force) {
-  drain<T, FN>(tb, q, cnt, x0, x1, z0, z1, lane, count, mark, force);
+__device__ __noinline__ void drain_call(const STab<T>& tb, const uint32_t* q, const T* qa,
+                                        const T* qb, int cnt, T* z0, T* z1, int lane, bool count,
+                                        bool mark, bool force) {
+  drain<T, FN>(tb, q, qa, qb, cnt, z0, z1, lane, count, mark, force);
 }
 template <class T, int FN>
-TF_DEV void drain_any(const STab<T>& tb, const uint32_t* q, int cnt, const T* __restrict__ x0,
-                      const T* __restrict__ x1, T* __restrict__ z0, T* __restrict__ z1,
-                      int lane, bool count, bool mark, bool force) {
+TF_DEV void drain_any(const STab<T>& tb, const uint32_t* q, const T* qa, const T* qb, int cnt,
+                      T* z0, T* z1, int lane, bool count, bool mark, bool force) {
   constexpr bool CALL = TF_DRAIN_CALL_LOG1P64 && sizeof(T) == 8 &&
                         (FN == FN_TLOG1P || FN == FN_TLOG1PP || FN == FN_PLOG1P ||
                          FN == FN_TLOG1P0 || FN == FN_PLOG1P0);
-  if constexpr (CALL) drain_call<T, FN>(tb, q, cnt, x0, x1, z0, z1, lane, count, mark, force);
-  else drain<T, FN>(tb, q, cnt, x0, x1, z0, z1, lane, count, mark, force);
+  if constexpr (CALL) drain_call<T, FN>(tb, q, qa, qb, cnt, z0, z1, lane, count, mark, force);
+  else drain<T, FN>(tb, q, qa, qb, cnt, z0, z1, lane, count, mark, force);
 }
 
 // Drop the first 32 entries of a warp's rare queue (entries [32, qn) move
-// down by 32): every lane reads its entries of all chunks, then writes.
-template <int QCAP>
-TF_DEV void queue_shift(uint32_t* q, int qn, int lane) {
+// down by 32, operands with them), one 32-entry chunk at a time: each lane
+// moves its entry of chunk k + 1 into chunk k (chunk k was read in the
+// previous pass), so only one entry per lane is live.
+template <int QCAP, class T>
+TF_DEV void queue_shift(uint32_t* q, T* qa, T* qb, int qn, int lane) {
   constexpr int NCH = (QCAP + 31) / 32 - 1;
-  uint32_t mv[NCH > 0 ? NCH : 1];
-#pragma unroll
-  for (int k = 0; k < NCH; ++k) {
+#pragma unroll 1
+  for (int k = 0; k < NCH && 32 * (k + 1) < qn; ++k) {
     const int src = lane + 32 * (k + 1);
-    mv[k] = src < qn ? q[src] : 0u;
+    const bool in = src < qn;
+    uint32_t mv = 0u;
+    T ma = T(0), mb = T(0);
+    if (in) { mv = q[src]; ma = qa[src]; mb = qb[src]; }
+    __syncwarp();
+    if (in) { q[src - 32] = mv; qa[src - 32] = ma; qb[src - 32] = mb; }
+    __syncwarp();
   }
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < NCH; ++k)
-    if (lane + 32 * (k + 1) < qn) q[lane + 32 * k] = mv[k];
 }
 
 template <class T, int FN, int VW>
 __global__ void __launch_bounds__((EvalCfg<T, FN, VW>::BLOCK), (EvalCfg<T, FN, VW>::MINB))
-k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
-       T* __restrict__ z1, uint32_t n, int flags) {
+k_eval(const T* x0, const T* x1, T* z0, T* z1, uint32_t n, int flags) {
   constexpr int BLOCK = EvalCfg<T, FN, VW>::BLOCK;
   constexpr int WARPS = BLOCK / 32;
   constexpr int QCAP = 32 + 32 * VW;
@@ -323,6 +330,7 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   }
   int cs = 0;
   while (base < nvec) {
+    int us = cs;  // the stage this iteration consumes (intact until the next prefetch)
     const uint32_t vi = base + lane;
     const bool valid = vi < nvec;
     T a[VW], b[VW], r0[VW], r1[VW];
@@ -368,7 +376,19 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
 #pragma unroll
       for (int e = 0; e < VW; ++e) {
         unsigned mask = __ballot_sync(0xffffffffu, rare[e]);
-        if (rare[e]) q[qn + __popc(mask & ((1u << lane) - 1u))] = vi * VW + e;
+        if (rare[e]) {
+          const int at = qn + __popc(mask & ((1u << lane) - 1u));
+          q[at] = vi * VW + e;
+          // operands from this thread's own staging slots (no live registers
+          // across the fast path); the direct-load path keeps them in a / b
+          if constexpr (ASYNC) {
+            S.qa[warp][at] = stg[us][0][threadIdx.x][e];
+            S.qb[warp][at] = DOT ? T(0) : stg[us][1][threadIdx.x][e];
+          } else {
+            S.qa[warp][at] = a[e];
+            S.qb[warp][at] = b[e];
+          }
+        }
         qn += __popc(mask);
       }
     }
@@ -377,9 +397,9 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
 #if TF_TIMELINE
       ++tl_drains;
 #endif
-      drain_any<T, FN>(tb, q, 32, x0, x1, z0, z1, lane, count, mark, force);
+      drain_any<T, FN>(tb, q, S.qa[warp], S.qb[warp], 32, z0, z1, lane, count, mark, force);
       __syncwarp();
-      queue_shift<QCAP>(q, qn, lane);
+      queue_shift<QCAP>(q, S.qa[warp], S.qb[warp], qn, lane);
       qn -= 32;
       __syncwarp();
     }
@@ -394,15 +414,20 @@ k_eval(const T* __restrict__ x0, const T* __restrict__ x1, T* __restrict__ z0,
   // ragged tail (n % VW elements): exact path, first warp of block 0
   const uint32_t tail = n - nvec * VW;
   if (blockIdx.x == 0 && warp == 0 && tail) {
-    if (lane < (int)tail) q[qn + lane] = (uint32_t)(nvec * VW + lane);
+    if (lane < (int)tail) {   // never touched by the main loop: x still holds them
+      const uint32_t i = nvec * VW + lane;
+      q[qn + lane] = i;
+      S.qa[warp][qn + lane] = x0[i];
+      S.qb[warp][qn + lane] = DOT ? T(0) : x1[i];
+    }
     qn += tail;
   }
   while (qn > 0) {
     __syncwarp();
     int c = qn < 32 ? qn : 32;
-    drain_any<T, FN>(tb, q, c, x0, x1, z0, z1, lane, count, mark, force);
+    drain_any<T, FN>(tb, q, S.qa[warp], S.qb[warp], c, z0, z1, lane, count, mark, force);
     __syncwarp();
-    queue_shift<QCAP>(q, qn, lane);
+    queue_shift<QCAP>(q, S.qa[warp], S.qb[warp], qn, lane);
     qn -= c;
   }
 #if TF_TIMELINE
@@ -608,17 +633,31 @@ using tfabi::g_const_ready;
 using tfabi::g_err;
 using tfabi::g_mu;
 
+std::mutex g_attr_mu;
+
 template <class T, int FN, int VW>
 int launch_one(const T* x0, const T* x1, T* z0, T* z1, int64_t n, cudaStream_t s, int flags) {
-  static int occ = 0;
   constexpr size_t SMEM = sizeof(typename tf::EvalCfg<T, FN, VW>::Smem);
+  static_assert(SMEM <= 227 * 1024, "k_eval shared memory exceeds the 227 KB per CTA");
+  // The dynamic-shared-memory attribute is per device (context): set it, and
+  // read the occupancy, once for each device this instantiation launches on.
+  static std::atomic<int> occ_dev[64];
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return cuda_check("cudaGetDevice");
+  int occ = occ_dev[d].load(std::memory_order_acquire);
   if (!occ) {
-    cudaFuncSetAttribute(tf::k_eval<T, FN, VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)SMEM);
-    int v = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, tf::k_eval<T, FN, VW>,
-                                                  tf::EvalCfg<T, FN, VW>::BLOCK, SMEM);
-    occ = v > 0 ? v : 1;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    occ = occ_dev[d].load(std::memory_order_relaxed);
+    if (!occ) {
+      if (cudaFuncSetAttribute(tf::k_eval<T, FN, VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)SMEM) != cudaSuccess)
+        return cuda_check("k_eval shared-memory attribute");
+      int v = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, tf::k_eval<T, FN, VW>,
+                                                    tf::EvalCfg<T, FN, VW>::BLOCK, SMEM);
+      occ = v > 0 ? v : 1;
+      occ_dev[d].store(occ, std::memory_order_release);
+    }
   }
   const int64_t CHUNK = (int64_t)1 << 31;  // queue indices are 32-bit
   for (int64_t off = 0; off < n; off += CHUNK) {
@@ -802,6 +841,28 @@ TF_API int tf_compare(int width, const void* z0, const void* z1, const void* r0,
   else
     return fail(TF_ERR_ARG, "unsupported width%s");
   return cuda_check("k_compare launch");
+}
+
+TF_API int tf_reduce_stats(const tf_stats* parts, int64_t nparts, tf_stats* out) {
+  if (!out || nparts < 0 || (nparts > 0 && !parts)) return fail(TF_ERR_ARG, "bad stats arguments%s");
+  tf_stats r;
+  memset(&r, 0, sizeof r);
+  r.err_max = -__builtin_inf();
+  for (int64_t i = 0; i < nparts; ++i) {
+    const tf_stats& p = parts[i];
+    r.n += p.n;
+    r.z0_mismatch += p.z0_mismatch;
+    r.z0_gt1ulp += p.z0_gt1ulp;
+    r.tol_violations += p.tol_violations;
+    r.class_mismatch += p.class_mismatch;
+    r.z1_mismatch += p.z1_mismatch;
+    r.included += p.included;
+    r.warnings += p.warnings;
+    r.err_sum += p.err_sum;
+    if (p.err_max > r.err_max) r.err_max = p.err_max;   // NaN compares false: ignored
+  }
+  *out = r;
+  return TF_OK;
 }
 
 TF_API int tf_fma_peak(int width, void* out_dev, int blocks, int iters, void* stream) {

@@ -13,9 +13,12 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-# counters summed across ranks / maxima taken across ranks
-SUM_KEYS = ("n", "z0_mismatch", "z0_gt1ulp", "tol_violations", "class_mismatch")
-MAX_KEYS = ("worst_rel_log2",)
+# stats-dict keys carried by the C record struct tf_stats (include/twofold_b200.h);
+# worst_rel_log2 travels in err_max
+RECORD_KEYS = {"n": "n", "z0_mismatch": "z0_mismatch", "z0_gt1ulp": "z0_gt1ulp",
+               "tol_violations": "tol_violations", "class_mismatch": "class_mismatch",
+               "z1_bit_mismatch": "z1_mismatch", "included": "included", "warnings": "warnings",
+               "err_sum": "err_sum", "worst_rel_log2": "err_max"}
 
 
 def shard_range(n_global: int, rank: int, world: int) -> tuple[int, int]:
@@ -31,22 +34,48 @@ def _active() -> bool:
     return dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
 
 
+def to_record(stats: dict):
+    """Pack a stats dict (oracle.compare / audit counters) into a tf_stats record."""
+    from ._lib import TfStats
+
+    r = TfStats()
+    r.err_max = float("-inf")
+    for k, f in RECORD_KEYS.items():
+        if k in stats and stats[k] is not None:
+            setattr(r, f, type(getattr(r, f))(stats[k]))
+    return r
+
+
 def reduce_stats(stats: dict, device=None) -> dict:
-    """Sum the counters and max the maxima of a per-rank stats dict (one
-    all-reduce each, a few dozen bytes)."""
+    """Merge a per-rank stats dict over all ranks: each rank contributes its
+    fixed-size tf_stats record (80 bytes) to one all-gather, and the records
+    merge with the C ABI's tf_reduce_stats (counts and sums add, maxima max).
+    Integer counters outside the record (e.g. *_given_z0_match) are summed
+    with one all-reduce; list-valued entries (diagnostic indices, histograms)
+    stay per-rank."""
     out = dict(stats)
     if not _active():
         return out
+    from ._lib import TfStats, reduce_stats_c
+
     dev = device if device is not None else torch.device("cpu")
-    s = torch.tensor([float(stats.get(k, 0)) for k in SUM_KEYS], dtype=torch.float64, device=dev)
-    m = torch.tensor([float(stats.get(k, float("-inf"))) for k in MAX_KEYS], dtype=torch.float64,
-                     device=dev)
-    dist.all_reduce(s, op=dist.ReduceOp.SUM)
-    dist.all_reduce(m, op=dist.ReduceOp.MAX)
-    for k, v in zip(SUM_KEYS, s.tolist()):
-        out[k] = int(v)
-    for k, v in zip(MAX_KEYS, m.tolist()):
-        out[k] = v
+    world = dist.get_world_size()
+    rec = bytes(to_record(stats))
+    mine = torch.frombuffer(bytearray(rec), dtype=torch.uint8).to(dev)
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    merged = reduce_stats_c([TfStats.from_buffer_copy(bytes(p.cpu().numpy())) for p in parts])
+    for k, f in RECORD_KEYS.items():
+        if k in stats:
+            v = getattr(merged, f)
+            out[k] = v if isinstance(v, float) else int(v)
+    extra = sorted(k for k, v in stats.items()
+                   if k not in RECORD_KEYS and isinstance(v, int) and not isinstance(v, bool))
+    if extra:
+        t = torch.tensor([float(stats[k]) for k in extra], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        for k, v in zip(extra, t.tolist()):
+            out[k] = int(v)
     return out
 
 

@@ -68,6 +68,22 @@ def _is_torch(x) -> bool:
     return isinstance(x, torch.Tensor)
 
 
+def _span(t):
+    lo = t.data_ptr()
+    return lo, lo + t.numel() * t.element_size()
+
+
+def _overlaps(a, b) -> bool:
+    if a.numel() == 0 or b.numel() == 0:
+        return False
+    (a0, a1), (b0, b1) = _span(a), _span(b)
+    return a0 < b1 and b0 < a1
+
+
+def _same_span(a, b) -> bool:
+    return _span(a) == _span(b)
+
+
 class ExpLog:
     """Twofold exponent and logarithm functions for one float width."""
 
@@ -233,6 +249,14 @@ class ExpLog:
             if (z0.shape != a0.shape or z1.shape != a0.shape or z0.dtype != dt or
                     z1.dtype != dt or not z0.is_contiguous() or not z1.is_contiguous()):
                 raise ValueError("out= tensors must be contiguous, same shape and dtype")
+            if z0.device != a0.device or z1.device != a0.device:
+                raise ValueError(f"out= tensors must live on the operands' device {a0.device}, "
+                                 f"got {z0.device}/{z1.device}")
+            # in place is supported element for element (z0 is x0 / z1 is x1: the
+            # kernel's rare queue keeps the operands); any other overlap is not
+            if _overlaps(z0, z1) or any(_overlaps(z, a) and not _same_span(z, a)
+                                        for z in (z0, z1) for a in (a0, a1)):
+                raise ValueError("out= tensors may alias the inputs only element for element")
         with torch.cuda.device(a0.device):
             stream = torch.cuda.current_stream(a0.device).cuda_stream
             self._launch(fn, a0, a1, z0, z1, a0.numel(), stream, flags)
