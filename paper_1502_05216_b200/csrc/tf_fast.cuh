@@ -441,17 +441,42 @@ template <int F> TF_DEV float cr32_lib(float x, bool& hard) {
 }
 
 // ================================================================ texp
+// Classes of x0 by raw bits (the sign-magnitude order of IEEE bit patterns):
+//   core   lo_bound <= x0 < hi_bound            pexp0_raw's table path
+//   below  -inf <= x0 < lo_bound                pexp0_raw = (0, 0)  (expcore.py:125-126)
+//   above  hi_bound <= x0 <= +inf               (inf, inf)          (expcore.py:127-128,
+//          x0 == hi_bound too: its product overflows and texp's guard returns (inf, inf))
+//   NaN                                         (NaN, NaN)          (expcore.py:123-124)
+// The fast path evaluates the core for tiny tails (|x1| < 2^-27, where t1 is the
+// polynomial) and resolves the saturated classes with selects, branch-free:
+// (inf, inf) and (NaN, NaN) whatever x1 is (explog.py:121-122, and NaN propagates
+// through z1), and for `below` z0 = exp(x0) in {2^-1074, 0} with the texp
+// epilogue on v = (0, 0).  Results in the subnormal range (x0 < -708.4) round
+// the 2^128-scaled twofold onto the subnormal grid (round_unscale128, the exact
+// path's own rounding), so the fast path covers every finite x0.
+constexpr uint64_t U64_HI = 0x40862e42fefa39f0ull;     // hi_bound
+constexpr uint64_t U64_LO_NEG = 0xc0874385446d71c4ull; // lo_bound (negative)
+constexpr uint64_t U64_UNF_NEG = 0xc0874910d52d3052ull; // EXP_UNF: exp(x) rounds to 0 below
+constexpr uint64_t U64_PINF = 0x7ff0000000000000ull, U64_NINF = 0xfff0000000000000ull;
+constexpr uint64_t U64_SIGN = 0x8000000000000000ull;
+
 // PM = true: pexp0 = renorm_fast(pexp0_raw(x0)) (explog.py:101-103), no libm value
 template <int VW, bool PM = false>
 TF_DEV void fast_texp(const STab<double>& tb, const double (&x0)[VW], const double (&x1)[VW],
                       double (&z0)[VW], double (&z1)[VW], bool (&ok)[VW]) {
   double y[VW];
   int m[VW], n[VW];
+  bool core[VW], below[VW], above[VW], nan0[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    ok[e] = ahi(x0[e]) <= (sgn(x0[e]) ? H64_TEXP_NEG : H64_TEXP_POS) &&
-            ahi(x1[e]) < H64_X1_TINY;
-    decomp_exp_u(ok[e] ? x0[e] : 0.0, m[e], n[e], y[e]);
+    const uint64_t b = ubits(x0[e]);
+    const bool tiny1 = ahi(x1[e]) < H64_X1_TINY;
+    core[e] = b < U64_HI || (b >= U64_SIGN && b <= U64_LO_NEG);
+    below[e] = b > U64_LO_NEG && b <= U64_NINF;
+    above[e] = b >= U64_HI && b <= U64_PINF;
+    nan0[e] = !(core[e] || below[e] || above[e]);
+    ok[e] = PM ? core[e] : (core[e] || below[e]) && tiny1 || above[e] || nan0[e];
+    decomp_exp_u(core[e] ? x0[e] : 0.0, m[e], n[e], y[e]);
   }
   TF<double> t[VW];
   taylor_exp_v<VW>(y, t);
@@ -468,12 +493,19 @@ TF_DEV void fast_texp(const STab<double>& tb, const double (&x0)[VW], const doub
     double zz = add(v.v, v.e);                                  // CR exp(x0)
     if (m[e] <= TF64_ESC_LO + TF64_ESC_COUNT - 1) {
       // e^x < 2^-987: the unscaled product's residuals underflow, so round the
-      // value part from the 2^128-scaled coarse entry (result normal: exact unscale)
+      // value part from the 2^128-scaled coarse entry (onto the subnormal grid
+      // where the result is subnormal)
       TF<double> vs = t_mul_u(tv<double>(tb.ESC[m[e] - TF64_ESC_LO]), ct);
-      zz = mul(add(vs.v, vs.e), 0x1p-128);
+      zz = round_unscale128(vs.v, vs.e);
+    }
+    if (below[e]) {                                             // pexp0_raw = (0, 0)
+      v = mk(0.0, 0.0);
+      zz = ubits(x0[e]) < U64_UNF_NEG ? 0x1p-1074 : 0.0;        // CR exp(x0)
     }
     z0[e] = zz;
     z1[e] = add(mul(zz, t1_tiny(x1[e])), add(v.e, sub(v.v, zz)));  // explog.py:125
+    if (above[e]) { z0[e] = Lim<double>::inf(); z1[e] = Lim<double>::inf(); }
+    if (nan0[e]) { z0[e] = Lim<double>::qnan(); z1[e] = Lim<double>::qnan(); }
   }
 }
 
@@ -652,6 +684,8 @@ template <> struct LogC<double> {
   // stay far below an ulp of |log y0| >= 2^-20 (coupled inputs have |d| <= 2^-53)
   static constexpr uint32_t DMAX = (1023u - 50u) << 20;
   static constexpr int SMALL = 50, EBIAS = 1022;
+  static constexpr int SUBSH = 54;
+  static constexpr double SUBSCALE = 0x1p54;
   static constexpr uint64_t HALF = B64_HALF, TWO = B64_TWO;
   static constexpr uint32_t NEAR1H = H64_NEAR1;
   TF_DEV static uint32_t eb(double x) { return (uint32_t)hi32(x) >> 20; }
@@ -671,6 +705,8 @@ template <> struct LogC<float> {
   static constexpr uint32_t NORM_SPAN = 254u;           // (2^-n may be subnormal: p2n = p2)
   static constexpr uint32_t DMAX = (127u - 21u) << 23;   // |d| < 2^-21
   static constexpr int SMALL = 21, EBIAS = 126;
+  static constexpr int SUBSH = 25;
+  static constexpr float SUBSCALE = 0x1p25f;
   static constexpr uint32_t HALF = B32_HALF, TWO = B32_TWO;
   static constexpr uint32_t NEAR1H = NEAR1_32 + 1u;
   TF_DEV static uint32_t eb(float x) { return ubits(x) >> 23; }
@@ -683,6 +719,34 @@ template <> struct LogC<float> {
   TF_DEV static float p2n(int k) { return p2f_bf(k); }
   TF_DEV static float rcp(float x) { return rcp_approx(x); }
 };
+
+// tlog / tlog0 / tlogp inputs whose result is a constant (_correct, explog.py:
+// 216-223, with the library value log(y0)): y0 NaN or negative (not -0) ->
+// log(y0) = NaN -> (NaN, NaN) whatever y1; y0 = +-0 and y1 = +-0 -> the core is
+// (-inf, NaN) and log(0) = -inf -> (-inf, -inf); y0 = +inf, y1 finite -> the
+// core's value part is +inf -> (inf, inf).  Resolved by selects in the fast
+// epilogue instead of the exact path.
+enum LogConst { LC_NONE = 0, LC_NAN = 1, LC_NINF = 2, LC_PINF = 3 };
+TF_DEV int log_const_class(double y0, double y1) {
+  const uint64_t b0 = ubits(y0), b1 = ubits(y1);
+  if (b0 > U64_PINF && b0 != U64_SIGN) return LC_NAN;
+  if ((b0 << 1) == 0 && (b1 << 1) == 0) return LC_NINF;
+  if (b0 == U64_PINF && is_finite(y1)) return LC_PINF;
+  return LC_NONE;
+}
+TF_DEV int log_const_class(float y0, float y1) {
+  const uint32_t b0 = ubits(y0), b1 = ubits(y1);
+  if (b0 > 0x7f800000u && b0 != 0x80000000u) return LC_NAN;
+  if ((b0 << 1) == 0 && (b1 << 1) == 0) return LC_NINF;
+  if (b0 == 0x7f800000u && is_finite(y1)) return LC_PINF;
+  return LC_NONE;
+}
+template <class T> TF_DEV void log_const_apply(int c, T& z0, T& z1, bool& ok) {
+  if (c == LC_NAN) { z0 = Lim<T>::qnan(); z1 = Lim<T>::qnan(); }
+  if (c == LC_NINF) { z0 = -Lim<T>::inf(); z1 = -Lim<T>::inf(); }
+  if (c == LC_PINF) { z0 = Lim<T>::inf(); z1 = Lim<T>::inf(); }
+  ok = ok || c != LC_NONE;
+}
 
 // Variants (explog.py:225-258): RENORM = false evaluates the core on (y0, y1)
 // as given (tlogp, plog; tlog0 / plog0 have y1 = 0, where renorm is the
@@ -700,21 +764,29 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
   T y0[VW], y1[VW], zc0[VW], zc1[VW], r0[VW], mr0[VW];
   int n[VW];
   TF<T> v[VW];
+  int nsc[VW];  // exponent of the tail scaling 2^-n (0 for pre-scaled subnormals)
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
+    // FULLR (drain): a positive subnormal y0 with y1 = 0 is scaled by 2^SUBSH
+    // first (exact), so frexp's exponent is n_of(y0 2^SUBSH) - SUBSH
+    bool subn = false;
+    if constexpr (FULLR)
+      subn = C::eb(y0i[e]) == 0u && !sgn(y0i[e]) && !zbits(y0i[e]) && zbits(y1i[e]);
+    const T y0s = subn ? mul(y0i[e], C::SUBSCALE) : y0i[e];
     // positive normal y0 (below 2^1022 / 2^126) and finite y1; how small y1 is
     // against y0 is checked on d = y1/y0 below, where it matters
-    ok[e] = C::eb(y0i[e]) - 1u < SPAN && is_finite(y1i[e]);
-    y0[e] = ok[e] ? y0i[e] : T(1);
+    ok[e] = C::eb(y0s) - 1u < SPAN && is_finite(y1i[e]);
+    y0[e] = ok[e] ? y0s : T(1);
     y1[e] = ok[e] ? y1i[e] : T(0);
     v[e] = RENORM ? renorm_u(mk(y0[e], y1[e])) : mk(y0[e], y1[e]);
     ok[e] = ok[e] && C::eb(v[e].v) - 1u < SPAN;
     if (!ok[e]) v[e] = mk(T(1), T(0));
     auto vb = ubits(v[e].v);
     bool band = vb >= C::HALF && vb <= C::TWO;
-    n[e] = band ? 0 : C::n_of(v[e].v);
+    n[e] = band ? 0 : C::n_of(v[e].v) - (subn ? C::SUBSH : 0);
+    nsc[e] = subn ? 0 : -n[e];
     zc0[e] = band ? v[e].v : C::mant(v[e].v);
-    zc1[e] = band ? v[e].e : (zbits(v[e].e) ? T(0) : mul(v[e].e, p2s(-n[e])));
+    zc1[e] = band ? v[e].e : (zbits(v[e].e) ? T(0) : mul(v[e].e, p2s(nsc[e])));
     r0[e] = seed_log1p_t(add(sub(zc0[e], T(1)), zc1[e]),      // explog.py:196-199
                          [&](int i) { return seed_entry(tb, i); });
     ok[e] = ok[e] && C::in_ln2(r0[e]);
@@ -744,7 +816,7 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     // to d = y1/y0 (|d| <= 2^-50 |log y0|, 2^-17 in binary32), so
     // log(y0) = core - d to well below an ulp with d known to ~2^-22:
     // y1 * 2^-n over zc0 (= v0 * 2^-n, within an ulp of y0 * 2^-n).
-    T d0 = mul(mul(y1[e], p2s(-n[e])), C::rcp(zc0[e]));
+    T d0 = mul(mul(y1[e], p2s(nsc[e])), C::rcp(zc0[e]));
     ok[e] = ok[e] && ahi(d0) < C::DMAX;
     // binary64: d carries the reciprocal's 2^-40 relative error, which must
     // stay ~2^-30 below an ulp of log(y0): |d| <= 2^-42 |core| away from the
@@ -783,7 +855,11 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
   }
   if constexpr (!PM) {
 #pragma unroll
-    for (int e = 0; e < VW; ++e) z1[e] = add(ce[e], sub(cv[e], z0[e]));  // _correct (222-223)
+    for (int e = 0; e < VW; ++e) {
+      z1[e] = add(ce[e], sub(cv[e], z0[e]));  // _correct (222-223)
+      if constexpr (sizeof(T) == 8 && !DBLV)
+        log_const_apply(log_const_class(y0i[e], y1i[e]), z0[e], z1[e], ok[e]);
+    }
   }
 }
 

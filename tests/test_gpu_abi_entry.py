@@ -120,9 +120,11 @@ def test_out_tensors_on_wrong_device_rejected(cuda):
     a1 = torch.zeros(8, dtype=torch.float64, device=cuda)
     with pytest.raises(ValueError):
         api(64).texp((a0, a1), out=(torch.empty(8, dtype=torch.float64), torch.empty_like(a0)))
-    big = torch.empty(9, dtype=torch.float64, device=cuda)
+    buf = torch.ones(16, dtype=torch.float64, device=cuda)
     with pytest.raises(ValueError):          # partial overlap with the input
-        api(64).texp((a0, a1), out=(big[1:], torch.empty_like(a0)))
+        api(64).texp((buf[:8], a1), out=(buf[4:12], torch.empty_like(a0)))
+    with pytest.raises(ValueError):          # the two outputs overlap
+        api(64).texp((a0, a1), out=(buf[:8], buf[2:10]))
 
 
 def test_two_devices_one_process():
