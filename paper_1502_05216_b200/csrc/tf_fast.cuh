@@ -1776,12 +1776,14 @@ TF_DEV void fast_eval(const STab<T>& tb, void* xch, const T (&x0)[VW], const T (
       fast_tlog1p<T, VW, RENORM, PM, INNER>(tb, x0, x1, z0, z1, ok);
   }
   if constexpr (FN == FN_PEXP || FN == FN_PEXPM1) {
-    // renorm_fast(texpp / texpm1p) (explog.py:131-133, 165-166)
+    // renorm_fast(texpp / texpm1p) (explog.py:131-133, 165-166); a non-finite
+    // sum takes the _special policy (eft.py:65-74): exact path
 #pragma unroll
     for (int e = 0; e < VW; ++e) {
       TF<T> r = fast_two_sum_u(z0[e], z1[e]);
       z0[e] = r.v;
       z1[e] = r.e;
+      ok[e] = ok[e] && is_finite(r.v);
     }
   }
 }

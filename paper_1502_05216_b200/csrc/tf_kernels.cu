@@ -262,7 +262,6 @@ template <class T, int FN, int VW>
 __global__ void __launch_bounds__((EvalCfg<T, FN, VW>::BLOCK), (EvalCfg<T, FN, VW>::MINB))
 k_eval(const T* x0, const T* x1, T* z0, T* z1, uint32_t n, int flags) {
   constexpr int BLOCK = EvalCfg<T, FN, VW>::BLOCK;
-  constexpr int WARPS = BLOCK / 32;
   constexpr int QCAP = 32 + 32 * VW;
 
   static_assert(VW == 1 || VW * sizeof(T) % 16 == 0, "vector lanes must fill 16-byte chunks");
@@ -284,7 +283,15 @@ k_eval(const T* x0, const T* x1, T* z0, T* z1, uint32_t n, int flags) {
   unsigned long long tl0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl0));
 #endif
+  // Programmatic dependent launch: the next launch on this stream may start
+  // (its CTAs take SMs as ours retire and stage their tables) right away; its
+  // griddepcontrol.wait still waits for this whole grid to complete and its
+  // memory to be visible, so triggering early is always safe.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // tables come from constant __device__ arrays no kernel writes: staged
+  // before waiting on the previous grid, overlapping its tail
   load_tables(tb, EvalCfg<T, FN, VW>::LOGF);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -633,6 +640,10 @@ using tfabi::g_const_ready;
 using tfabi::g_err;
 using tfabi::g_mu;
 
+// programmatic dependent launch of k_eval (TF_PDL=0: plain stream order)
+#ifndef TF_PDL
+#define TF_PDL 1
+#endif
 std::mutex g_attr_mu;
 
 template <class T, int FN, int VW>
@@ -666,8 +677,18 @@ int launch_one(const T* x0, const T* x1, T* z0, T* z1, int64_t n, cudaStream_t s
     int64_t vecs = (m / VW + BLK - 1) / BLK;
     int64_t grid = (int64_t)device_sms() * occ;
     if (vecs < grid) grid = vecs > 0 ? vecs : 1;
-    tf::k_eval<T, FN, VW><<<(unsigned)grid, BLK, SMEM, s>>>(
-        x0 + off, x1 + off, z0 + off, z1 + off, (uint32_t)m, flags);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(BLK);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = TF_PDL;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, tf::k_eval<T, FN, VW>, x0 + off, x1 + off, z0 + off, z1 + off,
+                       (uint32_t)m, flags);
   }
   return cuda_check("k_eval launch");
 }

@@ -27,8 +27,9 @@ def rate(fn, w, dist, n, reps=10):
     return round(n * reps / (e0.elapsed_time(e1) * 1e-3) / 1e9, 1)
 
 
-order = [("texp", 64, "exp64", 1 << 26), ("texpm1", 64, "pow10_64", 1 << 24), ("tlog", 64, "log64", 1 << 26),
+order = [("texp", 64, "exp64s", 1 << 28), ("tlog", 64, "logu64s", 1 << 28),
+         ("texp", 64, "exp64", 1 << 26), ("texpm1", 64, "pow10_64", 1 << 24), ("tlog", 64, "log64", 1 << 26),
          ("tlog1p", 64, "pow10c_64", 1 << 24), ("texp", 32, "exp32", 1 << 28), ("texpm1", 32, "exp32", 1 << 28),
          ("tlog", 32, "log32", 1 << 28), ("tlog1p", 32, "log32", 1 << 28)]
-for rnd in range(2):
-    print({f"{fn}_f{w}": rate(fn, w, d, n) for fn, w, d, n in order})
+for rnd in range(int(os.environ.get("ROUNDS", "2"))):
+    print({f"{fn}_f{w}_{d}": rate(fn, w, d, n) for fn, w, d, n in order}, flush=True)
