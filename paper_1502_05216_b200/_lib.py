@@ -114,8 +114,9 @@ def load() -> ctypes.CDLL:
         L.tf_eft.restype = i32
         L.tf_eval_host.argtypes = [i32, i32, vp, vp, vp, vp, i64, i64, vp, i32]
         L.tf_eval_host.restype = i32
-        L.tf_reduce_stats.argtypes = [ctypes.POINTER(TfStats), i64, ctypes.POINTER(TfStats)]
-        L.tf_reduce_stats.restype = i32
+        if hasattr(L, "tf_reduce_stats"):      # (older diagnostic builds lack it)
+            L.tf_reduce_stats.argtypes = [ctypes.POINTER(TfStats), i64, ctypes.POINTER(TfStats)]
+            L.tf_reduce_stats.restype = i32
         _lib = L
         return L
 

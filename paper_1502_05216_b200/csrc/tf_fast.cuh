@@ -447,13 +447,11 @@ template <int F> TF_DEV float cr32_lib(float x, bool& hard) {
 //   above  hi_bound <= x0 <= +inf               (inf, inf)          (expcore.py:127-128,
 //          x0 == hi_bound too: its product overflows and texp's guard returns (inf, inf))
 //   NaN                                         (NaN, NaN)          (expcore.py:123-124)
-// The fast path evaluates the core for tiny tails (|x1| < 2^-27, where t1 is the
-// polynomial) and resolves the saturated classes with selects, branch-free:
-// (inf, inf) and (NaN, NaN) whatever x1 is (explog.py:121-122, and NaN propagates
-// through z1), and for `below` z0 = exp(x0) in {2^-1074, 0} with the texp
-// epilogue on v = (0, 0).  Results in the subnormal range (x0 < -708.4) round
-// the 2^128-scaled twofold onto the subnormal grid (round_unscale128, the exact
-// path's own rounding), so the fast path covers every finite x0.
+// The main kernels run the core on the band where the result is normal and
+// below 2^1023 (cheap high-word tests); the rare-element drain resolves the
+// saturated classes with selects (texp_special) and evaluates the rest of the
+// core -- subnormal results, x0 up to hi_bound -- with WIDE = true (fast_alt),
+// so the exact path sees no finite x0 with a tiny tail at all.
 constexpr uint64_t U64_HI = 0x40862e42fefa39f0ull;     // hi_bound
 constexpr uint64_t U64_LO_NEG = 0xc0874385446d71c4ull; // lo_bound (negative)
 constexpr uint64_t U64_UNF_NEG = 0xc0874910d52d3052ull; // EXP_UNF: exp(x) rounds to 0 below
@@ -461,22 +459,21 @@ constexpr uint64_t U64_PINF = 0x7ff0000000000000ull, U64_NINF = 0xfff00000000000
 constexpr uint64_t U64_SIGN = 0x8000000000000000ull;
 
 // PM = true: pexp0 = renorm_fast(pexp0_raw(x0)) (explog.py:101-103), no libm value
-template <int VW, bool PM = false>
+template <int VW, bool PM = false, bool WIDE = false>
 TF_DEV void fast_texp(const STab<double>& tb, const double (&x0)[VW], const double (&x1)[VW],
                       double (&z0)[VW], double (&z1)[VW], bool (&ok)[VW]) {
   double y[VW];
   int m[VW], n[VW];
-  bool core[VW], below[VW], above[VW], nan0[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    const uint64_t b = ubits(x0[e]);
-    const bool tiny1 = ahi(x1[e]) < H64_X1_TINY;
-    core[e] = b < U64_HI || (b >= U64_SIGN && b <= U64_LO_NEG);
-    below[e] = b > U64_LO_NEG && b <= U64_NINF;
-    above[e] = b >= U64_HI && b <= U64_PINF;
-    nan0[e] = !(core[e] || below[e] || above[e]);
-    ok[e] = PM ? core[e] : (core[e] || below[e]) && tiny1 || above[e] || nan0[e];
-    decomp_exp_u(core[e] ? x0[e] : 0.0, m[e], n[e], y[e]);
+    if constexpr (WIDE) {
+      const uint64_t b = ubits(x0[e]);
+      ok[e] = (b < U64_HI || (b >= U64_SIGN && b <= U64_LO_NEG)) && ahi(x1[e]) < H64_X1_TINY;
+    } else {
+      ok[e] = ahi(x0[e]) <= (sgn(x0[e]) ? H64_TEXP_NEG : H64_TEXP_POS) &&
+              ahi(x1[e]) < H64_X1_TINY;
+    }
+    decomp_exp_u(ok[e] ? x0[e] : 0.0, m[e], n[e], y[e]);
   }
   TF<double> t[VW];
   taylor_exp_v<VW>(y, t);
@@ -493,20 +490,37 @@ TF_DEV void fast_texp(const STab<double>& tb, const double (&x0)[VW], const doub
     double zz = add(v.v, v.e);                                  // CR exp(x0)
     if (m[e] <= TF64_ESC_LO + TF64_ESC_COUNT - 1) {
       // e^x < 2^-987: the unscaled product's residuals underflow, so round the
-      // value part from the 2^128-scaled coarse entry (onto the subnormal grid
-      // where the result is subnormal)
+      // value part from the 2^128-scaled coarse entry (result normal: exact
+      // unscale; WIDE: onto the subnormal grid, the exact path's rounding)
       TF<double> vs = t_mul_u(tv<double>(tb.ESC[m[e] - TF64_ESC_LO]), ct);
-      zz = round_unscale128(vs.v, vs.e);
-    }
-    if (below[e]) {                                             // pexp0_raw = (0, 0)
-      v = mk(0.0, 0.0);
-      zz = ubits(x0[e]) < U64_UNF_NEG ? 0x1p-1074 : 0.0;        // CR exp(x0)
+      zz = WIDE ? round_unscale128(vs.v, vs.e) : mul(add(vs.v, vs.e), 0x1p-128);
     }
     z0[e] = zz;
     z1[e] = add(mul(zz, t1_tiny(x1[e])), add(v.e, sub(v.v, zz)));  // explog.py:125
-    if (above[e]) { z0[e] = Lim<double>::inf(); z1[e] = Lim<double>::inf(); }
-    if (nan0[e]) { z0[e] = Lim<double>::qnan(); z1[e] = Lim<double>::qnan(); }
   }
+}
+
+// texp's saturated classes (drain): (NaN, NaN) for NaN x0 and (inf, inf) for
+// x0 >= hi_bound whatever x1 (explog.py:119-122: the guard returns before t1;
+// NaN propagates through z1), and for x0 < lo_bound with a tiny tail
+// pexp0_raw = (0, 0), z0 = exp(x0) in {2^-1074, 0}, z1 by the texp epilogue.
+TF_DEV bool texp_special(double x0, double x1, double& z0, double& z1) {
+  const uint64_t b = ubits(x0);
+  if (b > U64_PINF && b != U64_SIGN && !(b >= U64_SIGN && b <= U64_NINF)) {
+    z0 = z1 = Lim<double>::qnan();
+    return true;
+  }
+  if (b >= U64_HI && b <= U64_PINF) {
+    z0 = z1 = Lim<double>::inf();
+    return true;
+  }
+  if (b > U64_LO_NEG && b <= U64_NINF && ahi(x1) < H64_X1_TINY) {
+    const double zz = b < U64_UNF_NEG ? 0x1p-1074 : 0.0;
+    z0 = zz;
+    z1 = add(mul(zz, t1_tiny(x1)), add(0.0, sub(0.0, zz)));
+    return true;
+  }
+  return false;
 }
 
 // DBLV: value part from the binary64 library (cr32_lib), rare-element drain
@@ -724,8 +738,8 @@ template <> struct LogC<float> {
 // 216-223, with the library value log(y0)): y0 NaN or negative (not -0) ->
 // log(y0) = NaN -> (NaN, NaN) whatever y1; y0 = +-0 and y1 = +-0 -> the core is
 // (-inf, NaN) and log(0) = -inf -> (-inf, -inf); y0 = +inf, y1 finite -> the
-// core's value part is +inf -> (inf, inf).  Resolved by selects in the fast
-// epilogue instead of the exact path.
+// core's value part is +inf -> (inf, inf).  Resolved in the rare-element drain
+// (special_const) instead of the exact path.
 enum LogConst { LC_NONE = 0, LC_NAN = 1, LC_NINF = 2, LC_PINF = 3 };
 TF_DEV int log_const_class(double y0, double y1) {
   const uint64_t b0 = ubits(y0), b1 = ubits(y1);
@@ -741,11 +755,11 @@ TF_DEV int log_const_class(float y0, float y1) {
   if (b0 == 0x7f800000u && is_finite(y1)) return LC_PINF;
   return LC_NONE;
 }
-template <class T> TF_DEV void log_const_apply(int c, T& z0, T& z1, bool& ok) {
+template <class T> TF_DEV bool log_const_apply(int c, T& z0, T& z1) {
   if (c == LC_NAN) { z0 = Lim<T>::qnan(); z1 = Lim<T>::qnan(); }
   if (c == LC_NINF) { z0 = -Lim<T>::inf(); z1 = -Lim<T>::inf(); }
   if (c == LC_PINF) { z0 = Lim<T>::inf(); z1 = Lim<T>::inf(); }
-  ok = ok || c != LC_NONE;
+  return c != LC_NONE;
 }
 
 // Variants (explog.py:225-258): RENORM = false evaluates the core on (y0, y1)
@@ -857,8 +871,6 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
 #pragma unroll
     for (int e = 0; e < VW; ++e) {
       z1[e] = add(ce[e], sub(cv[e], z0[e]));  // _correct (222-223)
-      if constexpr (sizeof(T) == 8 && !DBLV)
-        log_const_apply(log_const_class(y0i[e], y1i[e]), z0[e], z1[e], ok[e]);
     }
   }
 }
@@ -1557,7 +1569,8 @@ TF_DEV void tlog1p_sorted(const STab<float>& tb, Xch<VW>* xw, const float (&x0)[
 template <class T, int FN> struct HasAlt {
   static constexpr bool value =
       sizeof(T) == 4 ||
-      (FN == FN_TEXPM1 || FN == FN_TEXPM10 || FN == FN_PEXPM10 || FN == FN_PEXPM1 ||
+      (FN == FN_TEXP || FN == FN_TEXPP || FN == FN_TEXP0 || FN == FN_PEXP0 ||
+       FN == FN_TEXPM1 || FN == FN_TEXPM10 || FN == FN_PEXPM10 || FN == FN_PEXPM1 ||
        FN == FN_TLOG1P || FN == FN_TLOG1P0 || FN == FN_TLOG1PP || FN == FN_PLOG1P ||
        FN == FN_PLOG1P0 || FN == FN_TLOG || FN == FN_TLOG0 || FN == FN_TLOGP ||
        FN == FN_PLOG || FN == FN_PLOG0);
@@ -1658,7 +1671,11 @@ TF_DEV void fast_alt64_v(const STab<double>& tb, const double (&x0)[DR], const d
     }
   }
   T r0[DR], r1[DR];
-  if constexpr (FN == FN_TEXPM1 || FN == FN_TEXPM10 || FN == FN_PEXPM1) {
+  if constexpr (FN == FN_TEXP || FN == FN_TEXPP || FN == FN_TEXP0) {   // subnormal / near-overflow
+    fast_texp<DR, false, true>(tb, x0, x1, r0, r1, ok);
+  } else if constexpr (FN == FN_PEXP0) {
+    fast_texp<DR, true, true>(tb, x0, x1, r0, r1, ok);
+  } else if constexpr (FN == FN_TEXPM1 || FN == FN_TEXPM10 || FN == FN_PEXPM1) {
     fast_texpm1_fb<DR>(tb, x0, x1, r0, r1, ok);
     if constexpr (FN == FN_PEXPM1) {
 #pragma unroll
@@ -1706,6 +1723,20 @@ TF_DEV bool fast_alt64(const STab<double>& tb, double x0, double x1, double& z0,
   z0 = r0[0];
   z1 = r1[0];
   return ok[0];
+}
+
+// Constant-result classes of the rare elements (specials), resolved in the
+// drain with a few selects before any evaluation: texp / texpp / texp0
+// (texp_special) and tlog / tlog0 / tlogp (log_const_class).
+template <class T, int FN>
+TF_DEV bool special_const(T x0, T x1, T& z0, T& z1) {
+  if constexpr (sizeof(T) == 8 && (FN == FN_TEXP || FN == FN_TEXPP || FN == FN_TEXP0)) {
+    return texp_special(x0, x1, z0, z1);
+  } else if constexpr (FN == FN_TLOG || FN == FN_TLOG0 || FN == FN_TLOGP) {
+    return log_const_apply(log_const_class(x0, x1), z0, z1);
+  } else {
+    return false;
+  }
 }
 
 template <class T, int FN>

@@ -130,17 +130,20 @@ template <class T, int VW> struct KCfg {
 };
 
 // shared-memory layout of one k_eval CTA (dynamic: > 48 KB)
-// The rare queue holds each element's index AND its operands (qa, qb): the
-// drain never re-reads x0 / x1 from global memory, so z may alias x element
-// for element (in-place evaluation; the fast path has already overwritten
-// the element by the time it is drained).
+// In-place evaluation (z aliasing x element for element) needs the drain to
+// see each rare element's ORIGINAL operands.  TF_QOPS = 1: the rare queue
+// holds them next to the index (qa, qb); TF_QOPS = 0: the fast pass does not
+// store rare lanes, so x still holds them when the drain reads x0 / x1.
+#ifndef TF_QOPS
+#define TF_QOPS 0
+#endif
 template <class T, int VW, int BLOCK, bool ASYNC, bool XCH, int STAGES> struct EvalSmem {
   static constexpr int WARPS = BLOCK / 32;
   static constexpr int QCAP = 32 + 32 * VW;
   STab<T> tb;
   uint32_t qs[WARPS][QCAP];
-  T qa[WARPS][QCAP];
-  T qb[WARPS][QCAP];
+  T qa[TF_QOPS ? WARPS : 1][TF_QOPS ? QCAP : 1];
+  T qb[TF_QOPS ? WARPS : 1][TF_QOPS ? QCAP : 1];
   __align__(16) T stg[ASYNC ? STAGES : 1][2][BLOCK][VW];
   Xch<VW> xch[XCH ? WARPS : 1];
 };
@@ -189,18 +192,23 @@ template <int N> TF_DEV void cp_async_wait() {
 // exact path; the operands come from the queue, not from x0 / x1.
 template <class T, int FN>
 TF_DEV void drain(const STab<T>& tb, const uint32_t* q, const T* qa, const T* qb, int cnt,
-                  T* z0, T* z1, int lane, bool count, bool mark, bool force) {
+                  const T* x0, const T* x1, T* z0, T* z1, int lane, bool count, bool mark,
+                  bool force) {
   bool exact = false;
   if (lane < cnt) {
     uint32_t i = q[lane];
-    T a = qa[lane], b = dotted_fn(FN) ? T(0) : qb[lane];
+    T a = TF_QOPS ? qa[lane] : x0[i];
+    T b = dotted_fn(FN) ? T(0) : TF_QOPS ? qb[lane] : x1[i];
     if (mark) {  // diagnostics: tag exact-path elements instead of evaluating them
       z0[i] = Lim<T>::qnan();
       z1[i] = T(-12345);
     } else {
       T r0, r1;
-      bool done = false;
-      if constexpr (HasAlt<T, FN>::value) done = !force && fast_alt<T, FN>(tb, a, b, r0, r1);
+      // constant-result specials, then the second-chance fast evaluator, then
+      // the exact path (TF_FLAG_FORCE_EXACT: the exact path alone)
+      bool done = !force && special_const<T, FN>(a, b, r0, r1);
+      if constexpr (HasAlt<T, FN>::value)
+        if (!done) done = !force && fast_alt<T, FN>(tb, a, b, r0, r1);
       if (!done) {
         TF<T> r = eval_gen<T, FN>(a, b);
         r0 = r.v;
@@ -224,18 +232,20 @@ TF_DEV void drain(const STab<T>& tb, const uint32_t* q, const T* qa, const T* qb
 // log1p family calls it.
 template <class T, int FN>
 __device__ __noinline__ void drain_call(const STab<T>& tb, const uint32_t* q, const T* qa,
-                                        const T* qb, int cnt, T* z0, T* z1, int lane, bool count,
-                                        bool mark, bool force) {
-  drain<T, FN>(tb, q, qa, qb, cnt, z0, z1, lane, count, mark, force);
+                                        const T* qb, int cnt, const T* x0, const T* x1, T* z0,
+                                        T* z1, int lane, bool count, bool mark, bool force) {
+  drain<T, FN>(tb, q, qa, qb, cnt, x0, x1, z0, z1, lane, count, mark, force);
 }
 template <class T, int FN>
 TF_DEV void drain_any(const STab<T>& tb, const uint32_t* q, const T* qa, const T* qb, int cnt,
-                      T* z0, T* z1, int lane, bool count, bool mark, bool force) {
+                      const T* x0, const T* x1, T* z0, T* z1, int lane, bool count, bool mark,
+                      bool force) {
   constexpr bool CALL = TF_DRAIN_CALL_LOG1P64 && sizeof(T) == 8 &&
                         (FN == FN_TLOG1P || FN == FN_TLOG1PP || FN == FN_PLOG1P ||
                          FN == FN_TLOG1P0 || FN == FN_PLOG1P0);
-  if constexpr (CALL) drain_call<T, FN>(tb, q, qa, qb, cnt, z0, z1, lane, count, mark, force);
-  else drain<T, FN>(tb, q, qa, qb, cnt, z0, z1, lane, count, mark, force);
+  if constexpr (CALL)
+    drain_call<T, FN>(tb, q, qa, qb, cnt, x0, x1, z0, z1, lane, count, mark, force);
+  else drain<T, FN>(tb, q, qa, qb, cnt, x0, x1, z0, z1, lane, count, mark, force);
 }
 
 // Drop the first 32 entries of a warp's rare queue (entries [32, qn) move
@@ -251,9 +261,15 @@ TF_DEV void queue_shift(uint32_t* q, T* qa, T* qb, int qn, int lane) {
     const bool in = src < qn;
     uint32_t mv = 0u;
     T ma = T(0), mb = T(0);
-    if (in) { mv = q[src]; ma = qa[src]; mb = qb[src]; }
+    if (in) {
+      mv = q[src];
+      if (TF_QOPS) { ma = qa[src]; mb = qb[src]; }
+    }
     __syncwarp();
-    if (in) { q[src - 32] = mv; qa[src - 32] = ma; qb[src - 32] = mb; }
+    if (in) {
+      q[src - 32] = mv;
+      if (TF_QOPS) { qa[src - 32] = ma; qb[src - 32] = mb; }
+    }
     __syncwarp();
   }
 }
@@ -372,13 +388,24 @@ k_eval(const T* x0, const T* x1, T* z0, T* z1, uint32_t n, int flags) {
     fast_eval<T, FN, VW>(tb, &xch[XCH ? warp : 0], a, b, r0, r1, ok);
 #pragma unroll
     for (int e = 0; e < VW; ++e) rare[e] = valid && (!ok[e] || force);
-    if (valid) {
-      st<T, VW>(z0, vi, r0);
-      st<T, VW>(z1, vi, r1);
-    }
     bool anyrare = false;
 #pragma unroll
     for (int e = 0; e < VW; ++e) anyrare |= rare[e];
+    if (TF_QOPS || !anyrare) {
+      if (valid) {
+        st<T, VW>(z0, vi, r0);
+        st<T, VW>(z1, vi, r1);
+      }
+    } else {
+      // rare lanes keep x intact for the drain (in-place safety): per-lane
+      // stores of the admitted ones
+#pragma unroll
+      for (int e = 0; e < VW; ++e)
+        if (!rare[e]) {
+          __stcs(z0 + vi * VW + e, r0[e]);
+          __stcs(z1 + vi * VW + e, r1[e]);
+        }
+    }
     if (__any_sync(0xffffffffu, anyrare)) {  // one vote in the common all-fast case
 #pragma unroll
       for (int e = 0; e < VW; ++e) {
@@ -388,7 +415,8 @@ k_eval(const T* x0, const T* x1, T* z0, T* z1, uint32_t n, int flags) {
           q[at] = vi * VW + e;
           // operands from this thread's own staging slots (no live registers
           // across the fast path); the direct-load path keeps them in a / b
-          if constexpr (ASYNC) {
+          if constexpr (!TF_QOPS) {
+          } else if constexpr (ASYNC) {
             S.qa[warp][at] = stg[us][0][threadIdx.x][e];
             S.qb[warp][at] = DOT ? T(0) : stg[us][1][threadIdx.x][e];
           } else {
@@ -404,7 +432,8 @@ k_eval(const T* x0, const T* x1, T* z0, T* z1, uint32_t n, int flags) {
 #if TF_TIMELINE
       ++tl_drains;
 #endif
-      drain_any<T, FN>(tb, q, S.qa[warp], S.qb[warp], 32, z0, z1, lane, count, mark, force);
+      drain_any<T, FN>(tb, q, S.qa[warp], S.qb[warp], 32, x0, x1, z0, z1, lane, count, mark,
+                       force);
       __syncwarp();
       queue_shift<QCAP>(q, S.qa[warp], S.qb[warp], qn, lane);
       qn -= 32;
@@ -424,15 +453,18 @@ k_eval(const T* x0, const T* x1, T* z0, T* z1, uint32_t n, int flags) {
     if (lane < (int)tail) {   // never touched by the main loop: x still holds them
       const uint32_t i = nvec * VW + lane;
       q[qn + lane] = i;
-      S.qa[warp][qn + lane] = x0[i];
-      S.qb[warp][qn + lane] = DOT ? T(0) : x1[i];
+      if (TF_QOPS) {
+        S.qa[warp][qn + lane] = x0[i];
+        S.qb[warp][qn + lane] = DOT ? T(0) : x1[i];
+      }
     }
     qn += tail;
   }
   while (qn > 0) {
     __syncwarp();
     int c = qn < 32 ? qn : 32;
-    drain_any<T, FN>(tb, q, S.qa[warp], S.qb[warp], c, z0, z1, lane, count, mark, force);
+    drain_any<T, FN>(tb, q, S.qa[warp], S.qb[warp], c, x0, x1, z0, z1, lane, count, mark,
+                     force);
     __syncwarp();
     queue_shift<QCAP>(q, S.qa[warp], S.qb[warp], qn, lane);
     qn -= c;
