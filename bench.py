@@ -459,6 +459,25 @@ def run_ours(args):
                  "graph_gps": _r(ms_ * world / (graph_ms * 1e-3) / 1e9)}
         del a0, a1, z0, z1, g
 
+    # ---- the reference's own calling convention: one scalar twofold per call
+    # (audit.py:343-349), through api(64) on Python floats
+    scalar = None
+    if not args.headline_only:
+        from paper_1502_05216_b200 import workloads as W
+
+        scalar = {}
+        for fn, dname in HEADLINE:
+            x0s, x1s = W.generate(dname, 0, 512, seed=SEED)
+            pairs = list(zip(x0s.tolist(), x1s.tolist()))
+            f = getattr(f64, fn)
+            for p_ in pairs[:64]:
+                f(p_)
+            t = time.perf_counter()
+            for p_ in pairs:
+                f(p_)
+            scalar[fn] = _r((time.perf_counter() - t) / len(pairs) * 1e6)
+        scalar["unit"] = "us per call (api(64).fn((x0, x1)) on Python floats)"
+
     # ---- end to end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -558,6 +577,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "cfg1_small": small,
+            "scalar_call_us": scalar,
             "parity_legend": PARITY_LEGEND,
             "parity_cfg5": {fn: _compact(v) for fn, v in parity5.items()},
             "per_function_legend": "G elem/s, bound, frac of bound, fp frac, hbm frac (2^28)",

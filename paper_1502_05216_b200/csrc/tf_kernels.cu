@@ -135,7 +135,7 @@ template <class T, int VW> struct KCfg {
 // holds them next to the index (qa, qb); TF_QOPS = 0: the fast pass does not
 // store rare lanes, so x still holds them when the drain reads x0 / x1.
 #ifndef TF_QOPS
-#define TF_QOPS 0
+#define TF_QOPS 1
 #endif
 template <class T, int VW, int BLOCK, bool ASYNC, bool XCH, int STAGES> struct EvalSmem {
   static constexpr int WARPS = BLOCK / 32;

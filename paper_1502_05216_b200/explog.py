@@ -50,7 +50,7 @@ COUPLED_ARG = frozenset(("texpp", "pexp", "texpm1p", "pexpm1", "tlogp", "plog", 
                          "plog1p"))
 TWOFOLD_ARG = frozenset(("texp", "texpm1", "tlog", "tlog1p"))
 
-HOST_CHUNK = 1 << 20  # elements per pipelined host<->device chunk (tf_eval_host)
+HOST_CHUNK = 1 << 20  # tf_eval_host's default chunk (elements per pipelined transfer)
 
 
 def family_of(name: str) -> str:
@@ -204,10 +204,7 @@ class ExpLog:
             return self._host_torch(fn, x0, x1, out)
         if np.isscalar(x0) and np.isscalar(x1) or (isinstance(x0, (int, float)) and
                                                    isinstance(x1, (int, float))):
-            a0 = np.array([x0], dtype=self._np)
-            a1 = np.array([x1], dtype=self._np)
-            z0, z1 = self._host_numpy(fn, a0, a1)
-            return Twofold(float(z0[0]), float(z1[0]))
+            return self._scalar(fn, x0, x1)
         a0 = np.asarray(x0)
         a1 = np.asarray(x1)
         if a0.shape != a1.shape:
@@ -215,6 +212,28 @@ class ExpLog:
         z0, z1 = self._host_numpy(fn, a0.astype(self._np, copy=False),
                                   a1.astype(self._np, copy=False))
         return Twofold(z0, z1)
+
+    def _scalar(self, fn, x0, x1):
+        """One element, the reference's own calling convention (audit.py:343-349):
+        straight through tf_eval_host's small-call path (operands in a mapped
+        pinned buffer the kernel reads over PCIe; one launch, one sync)."""
+        import ctypes
+
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("no CUDA device visible: the twofold kernels need a B200 "
+                               "(sm_100a); there is no CPU fallback")
+        dev = torch.cuda.current_device()
+        L = _lib.ensure_device(dev)
+        ct = ctypes.c_double if self.width == 64 else ctypes.c_float
+        a0, a1, z0, z1 = ct(x0), ct(x1), ct(), ct()
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev).cuda_stream
+        rc = L.tf_eval_host(_lib.FN_CODES[fn], self.width, ctypes.byref(a0), ctypes.byref(a1),
+                            ctypes.byref(z0), ctypes.byref(z1), 1, 0, stream, 0)
+        _lib.check(rc, f"tf_eval_host({fn}, width={self.width})")
+        return Twofold(float(z0.value), float(z1.value))
 
     def _torch_dtype(self):
         import torch
@@ -289,7 +308,7 @@ class ExpLog:
         return z0.numpy().reshape(a0.shape), z1.numpy().reshape(a0.shape)
 
 
-def _pipeline(lib: ExpLog, fn: str, h0, h1, device=None, chunk: int = HOST_CHUNK, out=None):
+def _pipeline(lib: ExpLog, fn: str, h0, h1, device=None, chunk: int = 0, out=None):
     """Evaluate host tensors through tf_eval_host (csrc/tf_host.cu): a three-stage
     chunk pipeline -- H2D, kernel and D2H on three streams over a ring of device
     buffers -- so both PCIe directions stay busy at once.  `out` may supply

@@ -155,3 +155,37 @@ def test_host_pipeline_concurrent_callers(cuda):
         r0, r1 = _device_ref(j[0], j[1], *data[j])
         assert np.array_equal(z0.view(np.uint8), r0.view(np.uint8)), j
         assert np.array_equal(z1.view(np.uint8), r1.view(np.uint8)), j
+
+
+@pytest.mark.parametrize("width", (64, 32))
+@pytest.mark.parametrize("fn", FNS)
+def test_scalar_calls_equal_array_calls(fn, width, cuda):
+    """Python-float calls (the reference's convention) take tf_eval_host's
+    small-call path (mapped pinned buffer); results equal the device path."""
+    import numpy as np
+
+    from paper_1502_05216_b200 import api
+
+    x0, x1 = _inputs(fn, width, 64)
+    z0, z1 = _device_ref(fn, width, x0, x1)
+    f = getattr(api(width), fn)
+    for i in range(64):
+        r = f((float(x0[i]), float(x1[i])))
+        assert np.array([r.value], dtype=x0.dtype).view(np.uint8).tobytes() == \
+            z0[i:i + 1].view(np.uint8).tobytes()
+        same1 = np.array([r.error], dtype=x0.dtype).view(np.uint8).tobytes() == \
+            z1[i:i + 1].view(np.uint8).tobytes()
+        assert same1 or (np.isnan(r.error) and np.isnan(z1[i]))
+
+
+def test_small_host_arrays_use_mapped_path(cuda):
+    """n <= 1024 host arrays go through the small-call path; results equal the
+    chunked pipeline's bit for bit."""
+    import numpy as np
+
+    for n in (1, 7, 1024):
+        x0, x1 = _inputs("tlog", 64, n)
+        a = _host("tlog", 64, x0, x1, chunk=0)
+        b = _host("tlog", 64, x0, x1, chunk=3)
+        assert np.array_equal(a[0].view(np.int64), b[0].view(np.int64))
+        assert np.array_equal(a[1].view(np.int64), b[1].view(np.int64))
