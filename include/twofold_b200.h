@@ -130,7 +130,7 @@ TF_API int tf_generate(int dist, uint64_t seed, int64_t start, int64_t n, void* 
 
 /* Accumulate parity statistics of (z0, z1) against (r0, r1) into the 6
  * counters at stats_dev (device memory, caller-zeroed):
- * [elements, z0 bit mismatches, z0 mismatches > 1 ulp, |dz| > max(rel|r|, abs_guard),
+ * [elements, z0 bit mismatches, z0 mismatches > 1 ulp, |dz| > max(rel|r|, abs_guard, 2 ulp(r1)),
  *  non-finite class mismatches, z1 bit mismatches]. */
 TF_API int tf_compare(int width, const void* z0, const void* z1, const void* r0, const void* r1,
                       int64_t n, double rel, double abs_guard, unsigned long long* stats_dev,

@@ -906,11 +906,17 @@ TF_DEV TF<f2> taylor_expm1_p(f2 yp) {
 #ifndef TF_SPLIT_LDS
 #define TF_SPLIT_LDS 1
 #endif
-TF_DEV float lds32(const float* p) {
+// 32-bit shared-window address of a shared-memory object; the table bases are
+// loop invariant, so each lookup costs one index scaling (the (v, e) halves
+// share it through the load's immediate offset) instead of a generic-to-shared
+// conversion per load (which ptxas emits as IMADs on the busy FMA pipe)
+TF_DEV uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+TF_DEV float lds32a(uint32_t a) {
   float r;
-  asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(r) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(r) : "r"(a));
   return r;
 }
+TF_DEV float lds32(const float* p) { return lds32a(saddr(p)); }
 // TF_BOUNDS_CHECK (diagnostic builds, tools/sanitize_target.py): trap on a table
 // index outside the staged table; the pool has no compute-sanitizer
 #ifndef TF_BOUNDS_CHECK
@@ -923,8 +929,11 @@ template <int N>
 TF_DEV TF<f2> ldpair(const float2 (&t)[N], int i0, int i1) {
   bounds(i0, N);
   bounds(i1, N);
-  if (TF_SPLIT_LDS)
-    return mk(pk(lds32(&t[i0].x), lds32(&t[i1].x)), pk(lds32(&t[i0].y), lds32(&t[i1].y)));
+  if (TF_SPLIT_LDS) {
+    const uint32_t b = saddr(&t[0]);
+    const uint32_t a0 = b + (uint32_t)i0 * 8u, a1 = b + (uint32_t)i1 * 8u;
+    return mk(pk(lds32a(a0), lds32a(a1)), pk(lds32a(a0 + 4u), lds32a(a1 + 4u)));
+  }
   const float2 a = t[i0], b = t[i1];
   return mk(pk(a.x, b.x), pk(a.y, b.y));
 }
@@ -936,14 +945,17 @@ TF_DEV f2 seed_log1p_p(const STab<float>& tb, f2 a) {
   const float ax[2] = {lo(a), hi(a)}, fx[2] = {lo(f), hi(f)};
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const uint32_t fb = ubits(fx[h]);
-    const int i = (((int)(fb >> 23) - 126) << B) | (int)((fb >> (23 - B)) & (NB - 1u));
-    idx[h] = fabsf(ax[h]) < 0x1p-8f ? 2 * NB + 1 : min(max(i, 0), 2 * NB);   // FP pipe test
+    // (exponent, leading B mantissa bits) of f in [1/2, 2] is one field:
+    // ((e - 126) << B) | m = (fb >> (23 - B)) - (126 << B), in [0, 2 NB]; the
+    // unsigned clamp keeps rejected lanes' garbage in range
+    const uint32_t i = (ubits(fx[h]) >> (23 - B)) - (126u << B);
+    idx[h] = fabsf(ax[h]) < 0x1p-8f ? 2 * NB + 1 : (int)min(i, 2u * NB);   // FP pipe test
   }
   const TF<f2> t = ldpair(tb.SEED, idx[0], idx[1]);       // (invc, logc)
   bounds(idx[0], TF32_SEED_COUNT + 1);
   bounds(idx[1], TF32_SEED_COUNT + 1);
-  const f2 m1 = TF_SPLIT_LDS ? pk(lds32(&tb.SEEDM1[idx[0]]), lds32(&tb.SEEDM1[idx[1]]))
+  const uint32_t bm = saddr(&tb.SEEDM1[0]);
+  const f2 m1 = TF_SPLIT_LDS ? pk(lds32a(bm + (uint32_t)idx[0] * 4u), lds32a(bm + (uint32_t)idx[1] * 4u))
                              : pk(tb.SEEDM1[idx[0]], tb.SEEDM1[idx[1]]);
   const f2 r = fmaop(a, t.v, m1);                          // (1 + a) invc - 1, one rounding
   const f2 q = mul(r, r);                                  // seed_poly<float>
@@ -1011,8 +1023,7 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
     if (RENORM) v = renorm_u(v);
     // per-lane classification and frexp on the integer pipe
     float vv[2] = {lo(v.v), hi(v.v)}, ve[2] = {lo(v.e), hi(v.e)};
-    float c0[2], p2[2];
-    bool zero1[2];
+    float c0[2], p2[2], z1a[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = 2 * p + h;
@@ -1021,11 +1032,13 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
       n[e] = band ? 0 : C::n_of(vv[h]);
       c0[h] = band ? vv[h] : C::mant(vv[h]);
       p2[h] = band ? 1.0f : C::p2n(-n[e]);            // band: v.e * 1 == v.e exactly
-      zero1[h] = !band && ve[h] == 0.0f;
+      z1a[h] = band ? -0.0f : 0.0f;
     }
     const f2 zc0 = pk(c0[0], c0[1]);
-    f2 zc1 = mul(pk(ve[0], ve[1]), pk(p2[0], p2[1]));     // v.e * 2^-n
-    zc1 = pk(zero1[0] ? 0.0f : lo(zc1), zero1[1] ? 0.0f : hi(zc1));
+    // v.e 2^-n, and 0.0 for a zero v.e out of band (explog.py:190, "if y1 != 0.0
+    // else 0.0"): one FFMA2 whose +0 addend turns -0 into +0 and leaves every
+    // other product unchanged (the band keeps v.e as is: addend -0)
+    const f2 zc1 = fmaop(pk(ve[0], ve[1]), pk(p2[0], p2[1]), pk(z1a[0], z1a[1]));
     const f2 rs = seed_log1p_p(tb, add(sub(zc0, splat(1.0f)), zc1));   // explog.py:196-199
     float rr[2] = {lo(rs), hi(rs)};
     float mr[2];
@@ -1058,12 +1071,13 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
     bool hard[2];
     const f2 zs = rn_guard_p(core.v, sub(core.e, d0), hard);   // |z| >= 2^-8 away from 1
     float zx[2] = {lo(zs), hi(zs)}, dx[2] = {lo(d0), hi(d0)};
+    const f2 dlp = sub(pk(y0[2 * p], y0[2 * p + 1]), splat(1.0f));   // exact near 1
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = 2 * p + h;
       ok[e] = ok[e] && fabsf(dx[h]) < 0x1p-21f;             // C::DMAX
       z0[e] = zx[h];
-      dl[e] = sub(y0[e], 1.0f);
+      dl[e] = h ? hi(dlp) : lo(dlp);
       if (fabsf(dl[e]) <= 0x1p-7f) near |= 1u << e;          // C::NEAR1H
       else ok[e] = ok[e] && !hard[h];
     }
@@ -1297,9 +1311,9 @@ TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const f
     const TF<f2> w = renorm_u(t_add_d_u(v, splat(1.0f)));
     const float vv[2] = {lo(v.v), hi(v.v)}, ve[2] = {lo(v.e), hi(v.e)};
     const float wv[2] = {lo(w.v), hi(w.v)}, we[2] = {lo(w.e), hi(w.e)};
-    bool k[2], inb[2], zero1[2];
+    bool k[2], inb[2];
     int n[2];
-    float xv[2], xe[2], p2[2], one[2];
+    float xv[2], xe[2], p2[2], one[2], z1a[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       // finite operands; with RENORM implied by the tests on v below (an
@@ -1316,12 +1330,11 @@ TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const f
       xv[h] = inb[h] ? vv[h] : band ? wv[h] : C::mant(wv[h]);
       xe[h] = inb[h] ? ve[h] : we[h];
       p2[h] = (inb[h] | band) ? 1.0f : C::p2(-nn);         // x1 * 1 == x1 exactly
-      zero1[h] = !(inb[h] | band) & (we[h] == 0.0f);
+      z1a[h] = (inb[h] | band) ? -0.0f : 0.0f;             // see fast_tlog_p
       one[h] = inb[h] ? 0.0f : 1.0f;
     }
     const f2 xm_v = pk(xv[0], xv[1]);
-    f2 xm_e = mul(pk(xe[0], xe[1]), pk(p2[0], p2[1]));
-    xm_e = pk(zero1[0] ? 0.0f : lo(xm_e), zero1[1] ? 0.0f : hi(xm_e));
+    const f2 xm_e = fmaop(pk(xe[0], xe[1]), pk(p2[0], p2[1]), pk(z1a[0], z1a[1]));
     const f2 pa = sub(xm_v, pk(one[0], one[1]));           // v0 in band, zc0 - 1 out (exact)
     f2 arg;
     TF<f2> yw;

@@ -324,10 +324,12 @@ struct SeedE64 { double invc, invcm1, logc; };
 template <class Get> TF_DEV double seed_log1p_t(double a, Get get) {
   constexpr int B = TF64_SEED_BITS, NB = 1 << B;
   double f = add(1.0, a);
-  uint32_t h = (uint32_t)hi32(f);
-  int idx = (((int)(h >> 20) - 1022) << B) | (int)((h >> (20 - B)) & (NB - 1u));
+  // (exponent, leading B mantissa bits) of f in [1/2, 2] as one field,
+  // ((e - 1022) << B) | m, in [0, 2 NB]; the unsigned clamp keeps any other
+  // argument's index in range
+  const uint32_t u = ((uint32_t)hi32(f) >> (20 - B)) - (1022u << B);
   bool small = ahi(a) < 0x3f400000u;                  // |a| < 2^-11
-  idx = small ? 2 * NB + 1 : min(max(idx, 0), 2 * NB);
+  const int idx = small ? 2 * NB + 1 : (int)min(u, 2u * NB);
   const SeedE64 t = get(idx);
   double r = fmaop(a, t.invc, t.invcm1);
   double p = seed_poly(r);
@@ -337,10 +339,9 @@ struct SeedE32 { float invc, invcm1, logc; };
 template <class Get> TF_DEV float seed_log1p_t(float a, Get get) {   // as binary64
   constexpr int B = TF32_SEED_BITS, NB = 1 << B;
   float f = add(1.0f, a);
-  uint32_t h = ubits(f);
-  int idx = (((int)(h >> 23) - 126) << B) | (int)((h >> (23 - B)) & (NB - 1u));
+  const uint32_t u = (ubits(f) >> (23 - B)) - (126u << B);
   bool small = fabsf(a) < 0x1p-8f;                    // |a| < 2^-8
-  idx = small ? 2 * NB + 1 : min(max(idx, 0), 2 * NB);
+  const int idx = small ? 2 * NB + 1 : (int)min(u, 2u * NB);
   const SeedE32 t = get(idx);
   float r = fmaop(a, t.invc, t.invcm1);
   float p = seed_poly(r);
