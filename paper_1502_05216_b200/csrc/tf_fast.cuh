@@ -687,7 +687,7 @@ TF_DEV void fast_texpm1_inb32(const STab<float>& tb, float x0, float x1, float& 
 }
 
 // ================================================================= tlog
-// explog.py:244-249 -> _log_core (338-358) -> _newton_log_z (320-336),
+// explog.py:244-249 -> _log_core (188-208) -> _newton_log_z (170-186),
 // with the value part replaced by a correctly rounded log(y0):
 //   log(y0) = log(v) - log1p(d),  d = y1 / y0  (renorm is error-free: v - y0 == y1),
 // and near 1 by the exact-d series (log_near1).
@@ -1113,10 +1113,10 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
 // =============================================================== tlog1p
 // _plog1p_raw (explog.py:290-294) with both branches sharing ONE in-band
 // pexpm10 evaluation (the Taylor core is ~3/4 of the work):
-//   in-band  (-1/2 <= v0 <= 1): _log1p_core (426-432) -> _newton_log1p_in_band
-//            (410-424), seed log1p(v0);
+//   in-band  (-1/2 <= v0 <= 1): _log1p_core (276-282) -> _newton_log1p_in_band
+//            (260-274), seed log1p(v0);
 //   out-of-band: w = renorm(v + 1), tlogp(w) = _correct(_log_core(w), log(w0))
-//            (389-392, 338-358), seed log1p((z0 - 1) + z1) after frexp.
+//            (239-242, 188-208), seed log1p((z0 - 1) + z1) after frexp.
 // UNIFIED=false (binary64, cfg 2: 0.45% out-of-band) sends the out-of-band
 // lanes to the exact path instead; UNIFIED=true (binary32, cfg 4: 50/50)
 // evaluates them here with a lane-selected prologue/epilogue.
@@ -1235,9 +1235,9 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
       else zz = rn_guard<TF_TOL32_LOG>(sd[e], sub(x1, d), hard);
       z0[e] = tiny ? y0[e] : zz;
       ok[e] = ok[e] && (tiny || !hard);
-      z1[e] = add(x1, sub(sd[e], z0[e]));               // _correct (372-373)
+      z1[e] = add(x1, sub(sd[e], z0[e]));               // _correct (222-223)
     } else if (UNIFIED) {
-      // _newton_log_z (320-336) on (zc0, zc1), then + n ln2 (355-358)
+      // _newton_log_z (170-186) on (zc0, zc1), then + n ln2 (206-208)
       TF<T> wz = fast_two_sum_u(sub(zc0[e], T(1)), zc1[e]);
       TF<T> u = t_add_u(t_mul_u(mk(zc0[e], zc1[e]), s[e]), wz);
       T r1 = add(u.v, u.e);
@@ -1250,7 +1250,7 @@ TF_DEV void fast_tlog1p(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW
         z1[e] = r.e;
         continue;
       }
-      // tlogp's value part log(w0) (correct, 366-373): w1/w0 = zc1/zc0
+      // tlogp's value part log(w0) (_correct, 216-223): w1/w0 = zc1/zc0
       // (out-of-band: |log w0| >= ln 2 - tiny, |w1/w0| <= 2^-24)
       T rc = rcp_nr(zc0[e]);
       bool hard0;
@@ -1373,7 +1373,7 @@ TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const f
     const float xx[2] = {lo(x1), hi(x1)}, lm[2] = {lo(lim), hi(lim)};
 #pragma unroll
     for (int h = 0; h < 2; ++h) k[h] &= fabsf(xx[h]) < lm[h];
-    // + n ln2 (explog.py:355-358).  In band n = 0 and core == (sd, x1) (up to
+    // + n ln2 (explog.py:206-208).  In band n = 0 and core == (sd, x1) (up to
     // the sign of a zero x1, which no result below can see)
     const TF<f2> nl = t_mul_d_u(mk(splat(P<float>::LN2_V), splat(P<float>::LN2_E)),
                                 pk((float)n[0], (float)n[1]));
@@ -1382,7 +1382,7 @@ TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const f
     const f2 q = sel2(inb[0], inb[1], add(splat(1.0f), y0), xm_v);
     const f2 r = pk(rcp_approx(lo(q)), rcp_approx(hi(q)));
     const f2 rc = fmaop(r, fmaop(-q, r, splat(1.0f)), r);   // rcp_nr
-    // tlogp's value part t0 = log(w0) (_correct, explog.py:366-373); in band
+    // tlogp's value part t0 = log(w0) (_correct, explog.py:216-223); in band
     // t0 = RN(sd - 0) = sd, so that the final _correct below is x1 + (sd - z0)
     bool hard0[2], hard[2];
     const f2 t0 = rn_guard_p(core.v, sel2(inb[0], inb[1], splat(-0.0f), sub(core.e, mul(xm_e, rc))),
@@ -1402,7 +1402,7 @@ TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const f
       k[h] &= inb[h] ? okin : !(hard0[h] | hard[h]);
       zx[h] = tiny ? yy0[h] : zx[h];
     }
-    const f2 zr = add(t1, sub(t0, pk(zx[0], zx[1])));      // _correct (222-223, 372-373)
+    const f2 zr = add(t1, sub(t0, pk(zx[0], zx[1])));      // _correct (222-223)
     z0[a] = zx[0];
     z0[b] = zx[1];
     z1[a] = lo(zr);

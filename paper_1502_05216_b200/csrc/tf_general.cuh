@@ -578,7 +578,7 @@ template <class T> TF_DEV TF<T> tlog1p_gen(T y0, T y1) {
     } else {
       lw0 = log_cr(w.v);
     }
-    core = correct_c(raw, lw0);                                  // tlogp (389-392)
+    core = correct_c(raw, lw0);                                  // tlogp (239-242)
   } else {
     core = log1p_core_c(v.v, v.e);
     raw = core;
