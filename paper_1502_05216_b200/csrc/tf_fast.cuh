@@ -1738,15 +1738,65 @@ TF_DEV bool fast_alt64(const STab<double>& tb, double x0, double x1, double& z0,
   return ok[0];
 }
 
+// texpm1 / texpm1p / texpm10 saturated classes (explog.py:149-160 with
+// pexpm10_raw's fallback t_add_d(pexp0_raw(x0), -1), expcore.py:138-147):
+// NaN -> (NaN, NaN); x0 >= hi_bound -> (inf, inf) (the guard, explog.py:155);
+// x0 < lo_bound with a tiny tail -> w = (-1, +0), z0 = expm1(x0) = -1 and z1 by
+// the texpm1 epilogue (+0 for finite tiny x1).
+template <class T> TF_DEV bool texpm1_special(T x0, T x1, T& z0, T& z1) {
+  if (is_nan(x0)) {
+    z0 = z1 = Lim<T>::qnan();
+    return true;
+  }
+  if (x0 >= P<T>::HI) {
+    z0 = z1 = Lim<T>::inf();
+    return true;
+  }
+  const bool tiny1 = sizeof(T) == 8 ? ahi(x1) < H64_X1_TINY : (uint32_t)ahi(x1) < B32_X1_TINY;
+  if (x0 < P<T>::LO && tiny1) {
+    const T w0 = T(-1), w1 = T(0);
+    z0 = T(-1);
+    const T tail = add(w1, sub(w0, z0));
+    z1 = add(mul(add(z0, T(1)), t1_tiny(x1)), tail);
+    return true;
+  }
+  return false;
+}
+
+// tlog1p / tlog1pp / tlog1p0 constant classes (_correct with log1p(y0),
+// explog.py:216-223, 305-317): y0 NaN or below -1 -> log1p(y0) = NaN ->
+// (NaN, NaN); y0 = -1 with y1 = +-0 -> the core is tlogp(0, 0) = (-inf, -inf)
+// and log1p(-1) = -inf -> (-inf, -inf); y0 = +inf, y1 finite -> (inf, inf).
+template <class T> TF_DEV bool log1p_special(T y0, T y1, T& z0, T& z1) {
+  if (is_nan(y0) || y0 < T(-1)) {
+    z0 = z1 = Lim<T>::qnan();
+    return true;
+  }
+  if (y0 == T(-1) && y1 == T(0)) {
+    z0 = z1 = -Lim<T>::inf();
+    return true;
+  }
+  if (is_inf(y0) && y0 > T(0) && is_finite(y1)) {
+    z0 = z1 = Lim<T>::inf();
+    return true;
+  }
+  return false;
+}
+
 // Constant-result classes of the rare elements (specials), resolved in the
 // drain with a few selects before any evaluation: texp / texpp / texp0
-// (texp_special) and tlog / tlog0 / tlogp (log_const_class).
+// (texp_special), texpm1 / texpm1p / texpm10, tlog / tlog0 / tlogp
+// (log_const_class) and tlog1p / tlog1pp / tlog1p0.
 template <class T, int FN>
 TF_DEV bool special_const(T x0, T x1, T& z0, T& z1) {
   if constexpr (sizeof(T) == 8 && (FN == FN_TEXP || FN == FN_TEXPP || FN == FN_TEXP0)) {
     return texp_special(x0, x1, z0, z1);
+  } else if constexpr (FN == FN_TEXPM1 || FN == FN_TEXPM1P || FN == FN_TEXPM10) {
+    return texpm1_special(x0, x1, z0, z1);
   } else if constexpr (FN == FN_TLOG || FN == FN_TLOG0 || FN == FN_TLOGP) {
     return log_const_apply(log_const_class(x0, x1), z0, z1);
+  } else if constexpr (FN == FN_TLOG1P || FN == FN_TLOG1PP || FN == FN_TLOG1P0) {
+    return log1p_special(x0, x1, z0, z1);
   } else {
     return false;
   }

@@ -22,6 +22,13 @@ template <int CH, int MIX> __global__ void __launch_bounds__(1024, 1) k(float* o
         f[i] = lo > f[i] ? f[i] + 0.f : lo;
       }
       if (MIX == 2) q[i] = q[i] * 3u + (unsigned)p[i];   // IMAD
+      if (MIX == 3) {  // the same compare + select on the bit patterns (ISETP + SEL)
+        unsigned lo = (unsigned)p[i], fb = __float_as_uint(f[i]);
+        unsigned r;
+        asm("{ .reg .pred q; setp.gt.s32 q, %1, %2; selp.b32 %0, %2, %1, q; }" : "=r"(r) : "r"(lo), "r"(fb));
+        f[i] = __uint_as_float(r);
+      }
+      if (MIX == 4) q[i] = (q[i] ^ (unsigned)p[i]) + 3u;  // LOP3 + IADD (ALU)
     }
   }
   float s = 0;
@@ -45,5 +52,7 @@ int main() {
   run<1, 0>("FADD2", d, sms); run<2, 0>("FADD2", d, sms); run<4, 0>("FADD2", d, sms);
   run<1, 1>("+FSETP/FSEL", d, sms); run<2, 1>("+FSETP/FSEL", d, sms); run<4, 1>("+FSETP/FSEL", d, sms);
   run<1, 2>("+IMAD", d, sms); run<2, 2>("+IMAD", d, sms); run<4, 2>("+IMAD", d, sms);
+  run<2, 3>("+ISETP/SEL", d, sms); run<4, 3>("+ISETP/SEL", d, sms);
+  run<2, 4>("+LOP3/IADD", d, sms); run<4, 4>("+LOP3/IADD", d, sms);
   return 0;
 }
