@@ -917,28 +917,6 @@ TF_DEV float lds32a(uint32_t a) {
   return r;
 }
 TF_DEV float lds32(const float* p) { return lds32a(saddr(p)); }
-
-// ---- binary32 predicates and selects on the bit patterns (ALU pipe).  On
-// sm_100 a scalar FSETP / FSEL takes a slot of the FMA pipe, which the packed
-// FADD2 / FFMA2 keep busy in the binary32 kernels: one FSETP + FSEL per two
-// FADD2 cut the packed rate by a third, the same work on the bit patterns
-// (ISETP / SEL / LOP3) costs the FMA pipe nothing (tools/micro/chain_micro.cu).
-TF_DEV uint32_t fb(float x) { return __float_as_uint(x); }
-TF_DEV uint32_t fab(float x) { return __float_as_uint(x) & 0x7fffffffu; }   // |x|
-TF_DEV float bsel(bool c, float a, float b) { return __uint_as_float(c ? fb(a) : fb(b)); }
-// 0 < x <= FLT_MAX normal: (x bits - min normal) below the finite span
-TF_DEV bool pos_normal(float x) { return fb(x) - 0x00800000u < 0x7f000000u; }
-// a <= x <= b for 0 < a <= b (positive bounds as bit patterns)
-TF_DEV bool in_pos(float x, uint32_t a, uint32_t b) { return fb(x) - a <= b - a; }
-// |y| <= 2^-k |x| for normal x (conservative for a subnormal y: its bits plus
-// k << 23 read as a larger number); false for a non-finite y
-TF_DEV bool small_vs(float y, float x, int k) { return fab(y) + ((uint32_t)k << 23) <= fab(x); }
-// conservative |r1| < 2^-21 max(|r0|, 1) on the exponent fields (the binary64
-// newton_quiet's form): 2^(e1 - 126) > |r1| and max(|r0|, 1) >= 2^(e0 - 127)
-TF_DEV bool newton_quiet_b(float r1, float r0) {
-  const int e1 = (int)(fab(r1) >> 23), e0 = (int)(fab(r0) >> 23);
-  return e1 + 22 <= max(e0, 127);
-}
 // TF_BOUNDS_CHECK (diagnostic builds, tools/sanitize_target.py): trap on a table
 // index outside the staged table; the pool has no compute-sanitizer
 #ifndef TF_BOUNDS_CHECK
@@ -971,7 +949,7 @@ TF_DEV f2 seed_log1p_p(const STab<float>& tb, f2 a) {
     // ((e - 126) << B) | m = (fb >> (23 - B)) - (126 << B), in [0, 2 NB]; the
     // unsigned clamp keeps rejected lanes' garbage in range
     const uint32_t i = (ubits(fx[h]) >> (23 - B)) - (126u << B);
-    idx[h] = fab(ax[h]) < 0x3b800000u ? 2 * NB + 1 : (int)min(i, 2u * NB);   // |a| < 2^-8
+    idx[h] = fabsf(ax[h]) < 0x1p-8f ? 2 * NB + 1 : (int)min(i, 2u * NB);   // FP pipe test
   }
   const TF<f2> t = ldpair(tb.SEED, idx[0], idx[1]);       // (invc, logc)
   bounds(idx[0], TF32_SEED_COUNT + 1);
@@ -1005,14 +983,14 @@ TF_DEV f2 rn_guard_p(f2 h, f2 l, bool (&hard)[2]) {
   const f2 zs = add(h, l);
   const f2 rho = add(sub(h, zs), l);
   const f2 cr = fmaop(rho, splat(kguard<TOL>()), zs);
-  hard[0] = fb(lo(cr)) != fb(lo(zs));     // bit compare (ALU); conservative at +-0
-  hard[1] = fb(hi(cr)) != fb(hi(zs));
+  hard[0] = lo(cr) != lo(zs);
+  hard[1] = hi(cr) != hi(zs);
   return zs;
 }
 
 // per-lane select of two lane pairs: (c0 ? a.lo : b.lo, c1 ? a.hi : b.hi)
 TF_DEV f2 sel2(bool c0, bool c1, f2 a, f2 b) {
-  return pk(bsel(c0, lo(a), lo(b)), bsel(c1, hi(a), hi(b)));
+  return pk(c0 ? lo(a) : lo(b), c1 ? hi(a) : hi(b));
 }
 
 template <int VW, bool RENORM>
@@ -1030,8 +1008,9 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
     // the ALU pipe: positive normal y0, finite y1.  With RENORM the finiteness
     // tests are implied by the positive-normal test of v = renorm(y) below (an
     // infinite or NaN operand, or an overflowing sum, makes v0 NaN)
-    ok[e] = RENORM ? (int)fb(y0i[e]) >= 0x00800000
-                   : pos_normal(y0i[e]) && fab(y1i[e]) <= 0x7f7fffffu;
+    ok[e] = RENORM ? y0i[e] >= 0x1p-126f
+                   : y0i[e] >= 0x1p-126f && y0i[e] <= 0x1.fffffep127f &&
+                         fabsf(y1i[e]) <= 0x1.fffffep127f;
     // rejected lanes compute on whatever they hold: every table index below is
     // clamped or derived from a masked value, and their results are discarded
     y0[e] = y0i[e];
@@ -1048,12 +1027,12 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = 2 * p + h;
-      ok[e] = ok[e] && pos_normal(vv[h]);
-      bool band = in_pos(vv[h], B32_HALF, B32_TWO);
+      ok[e] = ok[e] && vv[h] >= 0x1p-126f && vv[h] <= 0x1.fffffep127f;
+      bool band = vv[h] >= 0.5f && vv[h] <= 2.0f;
       n[e] = band ? 0 : C::n_of(vv[h]);
-      c0[h] = bsel(band, vv[h], C::mant(vv[h]));
-      p2[h] = bsel(band, 1.0f, C::p2n(-n[e]));        // band: v.e * 1 == v.e exactly
-      z1a[h] = __uint_as_float((uint32_t)band << 31);  // -0 in band, +0 out
+      c0[h] = band ? vv[h] : C::mant(vv[h]);
+      p2[h] = band ? 1.0f : C::p2n(-n[e]);            // band: v.e * 1 == v.e exactly
+      z1a[h] = band ? -0.0f : 0.0f;
     }
     const f2 zc0 = pk(c0[0], c0[1]);
     // v.e 2^-n, and 0.0 for a zero v.e out of band (explog.py:190, "if y1 != 0.0
@@ -1067,8 +1046,8 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
     for (int h = 0; h < 2; ++h) {
       const int e = 2 * p + h;
       r0[e] = rr[h];
-      ok[e] = ok[e] && fab(rr[h]) <= B32_LN2;
-      mr[h] = __uint_as_float(ok[e] ? fb(rr[h]) ^ 0x80000000u : 0u);  // keeps the CM1 index in range
+      ok[e] = ok[e] && fabsf(rr[h]) <= P<float>::LN2_V;
+      mr[h] = ok[e] ? -rr[h] : 0.0f;                     // keeps the CM1 index in range
     }
     // s = pexpm10_raw(-r0), in-band branch (expcore.py:142-146)
     const TF<f2> s = pexpm10_inband_p(tb, pk(mr[0], mr[1]));
@@ -1077,10 +1056,12 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
     const TF<f2> u = t_add_u(t_mul_u(mk(zc0, zc1), s), w);
     const f2 r1 = add(u.v, u.e);
     const f2 r0p = pk(r0[2 * p], r0[2 * p + 1]);
-    // newton_quiet: |r1| < 2^-21 max(|r0|, 1), on the exponent fields
+    // newton_quiet on the FP pipe: |r1| < 2^-21 max(|r0|, 1) (exact scaling)
+    const f2 lim = mul(pk(fmaxf(fabsf(r0[2 * p]), 1.0f), fmaxf(fabsf(r0[2 * p + 1]), 1.0f)),
+                       splat(0x1p-21f));
 #pragma unroll
     for (int h = 0; h < 2; ++h)
-      ok[2 * p + h] = ok[2 * p + h] && newton_quiet_b(h ? hi(r1) : lo(r1), r0[2 * p + h]);
+      ok[2 * p + h] = ok[2 * p + h] && fabsf(h ? hi(r1) : lo(r1)) < (h ? hi(lim) : lo(lim));
     const TF<f2> nl = t_mul_d_u(mk(splat(P<float>::LN2_V), splat(P<float>::LN2_E)),
                                 pk((float)n[2 * p], (float)n[2 * p + 1]));
     const TF<f2> core = t_add_u(mk(r0p, r1), nl);
@@ -1094,10 +1075,10 @@ TF_DEV void fast_tlog_p(const STab<float>& tb, const float (&y0i)[VW], const flo
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = 2 * p + h;
-      ok[e] = ok[e] && fab(dx[h]) < 0x35000000u;            // |d| < 2^-21 (C::DMAX)
+      ok[e] = ok[e] && fabsf(dx[h]) < 0x1p-21f;             // C::DMAX
       z0[e] = zx[h];
       dl[e] = h ? hi(dlp) : lo(dlp);
-      if (fab(dl[e]) <= 0x3c000000u) near |= 1u << e;        // |y0 - 1| <= 2^-7 (C::NEAR1H)
+      if (fabsf(dl[e]) <= 0x1p-7f) near |= 1u << e;          // C::NEAR1H
       else ok[e] = ok[e] && !hard[h];
     }
     // z1 = core.e + (core.v - z0) (_correct, explog.py:222-223), after near-1 fix-ups
@@ -1338,23 +1319,19 @@ TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const f
       // finite operands; with RENORM implied by the tests on v below (an
       // infinite or NaN operand or an overflowing sum makes v0 NaN, which is
       // neither in band nor > -1)
-      // (all tests on the bit patterns: ALU, not the FMA pipe)
-      k[h] = RENORM || ((fab(yy0[h]) <= 0x7f7fffffu) & (fab(yy1[h]) <= 0x7f7fffffu));
-      const bool neg = (int)fb(vv[h]) < 0;
-      inb[h] = fab(vv[h]) <= (neg ? B32_HALF : B32_ONE);  // -1/2 <= v0 <= 1 (explog.py:291)
-      // out of band: v0 > -1 and |y1 / (1 + y0)| <= 2^-14 (log1p(d) = d - d^2/2),
-      // with w0 finite
-      const bool gt_m1 = neg ? fab(vv[h]) < B32_ONE : fb(vv[h]) <= 0x7f800000u;
-      k[h] &= inb[h] | (gt_m1 & (fab(wv[h]) <= 0x7f7fffffu) & small_vs(yy1[h], wv[h], 14));
-      const bool band = in_pos(wv[h], B32_HALF, B32_TWO);
+      k[h] = RENORM || ((fabsf(yy0[h]) <= 0x1.fffffep127f) & (fabsf(yy1[h]) <= 0x1.fffffep127f));
+      inb[h] = (vv[h] >= -0.5f) & (vv[h] <= 1.0f);         // explog.py:291
+      // out of band: v0 > -1 and |y1 / (1 + y0)| <= 2^-14 (log1p(d) = d - d^2/2)
+      k[h] &= inb[h] | ((vv[h] > -1.0f) & (fabsf(yy1[h]) * 0x1p14f <= fabsf(wv[h])));
+      const bool band = (wv[h] >= 0.5f) & (wv[h] <= 2.0f);
       const int nn = band ? 0 : C::n_of(wv[h]);
       n[h] = inb[h] ? 0 : nn;
       // the Newton product's left operand x: v in band, zc = (zc0, w1 2^-n) out
-      xv[h] = bsel(inb[h], vv[h], bsel(band, wv[h], C::mant(wv[h])));
-      xe[h] = bsel(inb[h], ve[h], we[h]);
-      p2[h] = bsel(inb[h] | band, 1.0f, C::p2(-nn));       // x1 * 1 == x1 exactly
-      z1a[h] = __uint_as_float((uint32_t)(inb[h] | band) << 31);   // see fast_tlog_p
-      one[h] = __uint_as_float(inb[h] ? 0u : B32_ONE);
+      xv[h] = inb[h] ? vv[h] : band ? wv[h] : C::mant(wv[h]);
+      xe[h] = inb[h] ? ve[h] : we[h];
+      p2[h] = (inb[h] | band) ? 1.0f : C::p2(-nn);         // x1 * 1 == x1 exactly
+      z1a[h] = (inb[h] | band) ? -0.0f : 0.0f;             // see fast_tlog_p
+      one[h] = inb[h] ? 0.0f : 1.0f;
     }
     const f2 xm_v = pk(xv[0], xv[1]);
     const f2 xm_e = fmaop(pk(xe[0], xe[1]), pk(p2[0], p2[1]), pk(z1a[0], z1a[1]));
@@ -1376,26 +1353,26 @@ TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const f
     float ms[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      k[h] &= fab(sx[h]) <= B32_LN2;
-      ms[h] = __uint_as_float(k[h] ? fb(sx[h]) ^ 0x80000000u : 0u);  // keeps the CM1 index in range
+      k[h] &= fabsf(sx[h]) <= P<float>::LN2_V;
+      ms[h] = k[h] ? -sx[h] : 0.0f;                         // keeps the CM1 index in range
     }
     const TF<f2> s = pexpm10_inband_p(tb, pk(ms[0], ms[1]));
     // Newton step: one product x s, then + v + s in band, + wz out of band
     const TF<f2> u1 = t_add_u(t_mul_u(mk(xm_v, xm_e), s), yw);
     const TF<f2> u2 = t_add_u(u1, s);
     TF<f2> u = mk(sel2(inb[0], inb[1], u2.v, u1.v), sel2(inb[0], inb[1], u2.e, u1.e));
-    const bool dot[2] = {bool(inb[0] & ((fb(ve[0]) << 1) == 0u)),
-                         bool(inb[1] & ((fb(ve[1]) << 1) == 0u))};
+    const bool dot[2] = {bool(inb[0] & (ve[0] == 0.0f)), bool(inb[1] & (ve[1] == 0.0f))};
     if (__any_sync(0xffffffffu, dot[0] | dot[1])) {       // explog.py:268-270
       const TF<f2> w1 = fast_two_sum_u(splat(1.0f), v.v);
       const TF<f2> u0 = t_add_d_u(t_mul_u(w1, s), v.v);
       u = mk(sel2(dot[0], dot[1], u0.v, u.v), sel2(dot[0], dot[1], u0.e, u.e));
     }
     const f2 x1 = add(u.v, u.e);
-    // newton_quiet: |x1| < 2^-21 max(|sd|, 1), on the exponent fields
-    const float xx[2] = {lo(x1), hi(x1)};
+    // newton_quiet: |x1| < 2^-21 max(|sd|, 1)
+    const f2 lim = mul(pk(fmaxf(fabsf(sx[0]), 1.0f), fmaxf(fabsf(sx[1]), 1.0f)), splat(0x1p-21f));
+    const float xx[2] = {lo(x1), hi(x1)}, lm[2] = {lo(lim), hi(lim)};
 #pragma unroll
-    for (int h = 0; h < 2; ++h) k[h] &= newton_quiet_b(xx[h], sx[h]);
+    for (int h = 0; h < 2; ++h) k[h] &= fabsf(xx[h]) < lm[h];
     // + n ln2 (explog.py:206-208).  In band n = 0 and core == (sd, x1) (up to
     // the sign of a zero x1, which no result below can see)
     const TF<f2> nl = t_mul_d_u(mk(splat(P<float>::LN2_V), splat(P<float>::LN2_E)),
@@ -1420,10 +1397,10 @@ TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const f
     float zx[2] = {lo(zz), hi(zz)};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const bool tiny = inb[h] & (fab(yy0[h]) < 0x33000000u);            // |y0| < 2^-25
-      const bool okin = tiny | (small_vs(dx[h], sx[h], 21) & !hard[h]);  // |d| <= 2^-21 |sd|
+      const bool tiny = inb[h] & (fabsf(yy0[h]) < 0x1p-25f);
+      const bool okin = tiny | ((fabsf(dx[h]) * 0x1p21f <= fabsf(sx[h])) & !hard[h]);
       k[h] &= inb[h] ? okin : !(hard0[h] | hard[h]);
-      zx[h] = bsel(tiny, yy0[h], zx[h]);
+      zx[h] = tiny ? yy0[h] : zx[h];
     }
     const f2 zr = add(t1, sub(t0, pk(zx[0], zx[1])));      // _correct (222-223)
     z0[a] = zx[0];
@@ -1458,10 +1435,9 @@ TF_DEV void fast_texp_p(const STab<float>& tb, const float (&x0)[VW], const floa
   int m[VW], n[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    // band tests on the bit patterns (ALU; the FMA pipe is the busy one)
-    ok[e] = fab(x0[e]) <= ((int)fb(x0[e]) < 0 ? B32_TEXP_NEG : B32_TEXP_POS) &&
-            fab(x1[e]) < B32_X1_TINY;
-    decomp_exp_u(bsel(ok[e], x0[e], 0.0f), m[e], n[e], y[e]);
+    ok[e] = x0[e] >= -__uint_as_float(B32_TEXP_NEG) && x0[e] <= __uint_as_float(B32_TEXP_POS) &&
+            fabsf(x1[e]) < __uint_as_float(B32_X1_TINY);
+    decomp_exp_u(ok[e] ? x0[e] : 0.0f, m[e], n[e], y[e]);
   }
 #pragma unroll
   for (int p = 0; p < VW / 2; ++p) {
@@ -1500,9 +1476,9 @@ TF_DEV void fast_texpm1_p(const STab<float>& tb, const float (&x0)[VW], const fl
   int m[VW], n[VW];
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
-    ok[e] = fab(x0[e]) > B32_LN2 && fab(x0[e]) <= ((int)fb(x0[e]) < 0 ? B32_LO : B32_TEXP_POS) &&
-            fab(x1[e]) < B32_X1_TINY;
-    decomp_exp_u(bsel(ok[e], x0[e], 1.0f), m[e], n[e], y[e]);
+    ok[e] = fabsf(x0[e]) > __uint_as_float(B32_LN2) && x0[e] >= -__uint_as_float(B32_LO) &&
+            x0[e] <= __uint_as_float(B32_TEXP_POS) && fabsf(x1[e]) < __uint_as_float(B32_X1_TINY);
+    decomp_exp_u(ok[e] ? x0[e] : 1.0f, m[e], n[e], y[e]);
   }
 #pragma unroll
   for (int p = 0; p < VW / 2; ++p) {

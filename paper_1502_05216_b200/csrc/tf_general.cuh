@@ -238,7 +238,7 @@ TF_DEV double t1_tiny(double x) {
 TF_DEV float t1_tiny(float x) {
   double d = (double)x;
   double r = fmaop(mul(d, d), fmaop(d, 0x1.5555555555555p-3, 0.5), d);
-  return (__float_as_uint(x) << 1) == 0u ? x : __double2float_rn(r);   // +-0 (bit test: ALU)
+  return x == 0.0f ? x : __double2float_rn(r);
 }
 
 TF_DEV double expm1_cr(double x) {
