@@ -139,6 +139,25 @@ def check(rc: int, what: str) -> None:
         raise RuntimeError(f"{what}: {msg}")
 
 
+_scalar_dev = None
+
+
+def scalar_device() -> ctypes.CDLL:
+    """The library, initialised on torch's current device (scalar-call fast path:
+    checked once per process and device)."""
+    global _scalar_dev
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device visible: the twofold kernels need a B200 "
+                           "(sm_100a); there is no CPU fallback")
+    d = torch.cuda.current_device()
+    if _scalar_dev != d:
+        ensure_device(d)
+        _scalar_dev = d
+    return _lib
+
+
 def ensure_device(device_index: int) -> ctypes.CDLL:
     L = load()
     if device_index not in _inited:

@@ -97,6 +97,7 @@ struct SmallBuf {
   bool ready = false;
   void* host = nullptr;  // 4 x SMALL_N doubles, cudaHostAllocMapped
   void* dev = nullptr;   // its device alias
+  cudaStream_t own = nullptr;  // used when the caller passes no stream
   std::mutex mu;
 };
 SmallBuf g_small[MAX_DEV];
@@ -107,10 +108,14 @@ int eval_small(int dev, int fn, int width, const void* x0, const void* x1, void*
   std::lock_guard<std::mutex> lk(b.mu);
   if (!b.ready) {
     if (cudaHostAlloc(&b.host, 4 * SMALL_N * sizeof(double), cudaHostAllocMapped) != cudaSuccess ||
-        cudaHostGetDevicePointer(&b.dev, b.host, 0) != cudaSuccess)
+        cudaHostGetDevicePointer(&b.dev, b.host, 0) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&b.own, cudaStreamNonBlocking) != cudaSuccess)
       return cuda_check("tf_eval_host: mapped staging buffer");
     b.ready = true;
   }
+  // no caller stream: a library stream that does not serialise with the
+  // device's other work (the operands are host values, nothing to wait for)
+  if (!stream) stream = b.own;
   const size_t sz = width / 8, bytes = (size_t)n * sz, slot = SMALL_N * sizeof(double);
   char* h = static_cast<char*>(b.host);
   char* d = static_cast<char*>(b.dev);

@@ -27,6 +27,7 @@ where the reference raises OverflowError for a non-coupled argument
 
 from __future__ import annotations
 
+import ctypes
 from functools import lru_cache
 
 import numpy as np
@@ -99,6 +100,7 @@ class ExpLog:
         self.backend = backend
         self.params = params
         self._np = np.float64 if width == 64 else np.float32
+        self._ct = ctypes.c_double if width == 64 else ctypes.c_float
 
     # ---- the four twofold-argument functions (explog.py:115, 149, 244, 314)
     def texp(self, x, out=None):
@@ -217,23 +219,16 @@ class ExpLog:
         """One element, the reference's own calling convention (audit.py:343-349):
         straight through tf_eval_host's small-call path (operands in a mapped
         pinned buffer the kernel reads over PCIe; one launch, one sync)."""
-        import ctypes
-
-        import torch
-
-        if not torch.cuda.is_available():
-            raise RuntimeError("no CUDA device visible: the twofold kernels need a B200 "
-                               "(sm_100a); there is no CPU fallback")
-        dev = torch.cuda.current_device()
-        L = _lib.ensure_device(dev)
-        ct = ctypes.c_double if self.width == 64 else ctypes.c_float
+        L = _lib.scalar_device()
+        ct = self._ct
         a0, a1, z0, z1 = ct(x0), ct(x1), ct(), ct()
-        with torch.cuda.device(dev):
-            stream = torch.cuda.current_stream(dev).cuda_stream
+        # stream NULL: the library's own non-blocking stream (host operands,
+        # nothing on the device to order after)
         rc = L.tf_eval_host(_lib.FN_CODES[fn], self.width, ctypes.byref(a0), ctypes.byref(a1),
-                            ctypes.byref(z0), ctypes.byref(z1), 1, 0, stream, 0)
-        _lib.check(rc, f"tf_eval_host({fn}, width={self.width})")
-        return Twofold(float(z0.value), float(z1.value))
+                            ctypes.byref(z0), ctypes.byref(z1), 1, 0, None, 0)
+        if rc:
+            _lib.check(rc, f"tf_eval_host({fn}, width={self.width})")
+        return Twofold(z0.value, z1.value)
 
     def _torch_dtype(self):
         import torch

@@ -164,3 +164,27 @@ def test_named_entry_point_scalar_c_form(cuda):
     r0, r1 = O.evaluate("texp", 64, np.array([1.0]), np.array([2.0 ** -60]), backend="fma",
                         libm64="cr")
     assert z0.item() == r0[0] and z1.item() == r1[0]
+
+
+@pytest.mark.parametrize("width", (64, 32))
+@pytest.mark.parametrize("fn", ALL_FNS)
+def test_tiny_launch_equals_full_kernel(fn, width, golden, cuda):
+    """n <= 32 runs the one-warp k_tiny (exact path, global tables); every
+    32-element window of the golden vectors must equal the admission-band
+    kernel's result on the whole array bit for bit."""
+    from paper_1502_05216_b200 import api
+
+    g = golden(fn, width)
+    x0, x1 = g["x0"], g["x1"]
+    if fn.endswith("0"):
+        x1 = np.zeros_like(x0)
+    lib = api(width)
+    a0, a1 = _dev_arrays(x0, x1, cuda)
+    full = lib._device(fn, a0, a1)
+    f0, f1 = full.value.cpu().numpy(), full.error.cpu().numpy()
+    for lo_ in range(0, min(x0.size, 32 * 24), 32):
+        t0, t1 = _dev_arrays(x0[lo_:lo_ + 32], x1[lo_:lo_ + 32], cuda)
+        z = lib._device(fn, t0, t1)
+        r = compare(z.value.cpu().numpy(), z.error.cpu().numpy(), f0[lo_:lo_ + 32],
+                    f1[lo_:lo_ + 32], width)
+        assert r["z0_mismatch"] == 0 and r["z1_bit_mismatch"] == 0, (lo_, r)

@@ -7,6 +7,7 @@ import subprocess
 import sys
 
 ROUND = sys.argv[1] if len(sys.argv) > 1 else "r01"
+N = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 24     # elements per captured launch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G, P = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
 
@@ -16,8 +17,10 @@ def last_json(path):
 
 
 # each part is optional: a capture-only call (tools/ncu_full.sh) has no bench logs
-if os.path.exists(f"{G}/bench_full.log"):
-    json.dump(last_json(f"{G}/bench_full.log"), open(f"{P}/{ROUND}_bench.json", "w"), indent=1)
+for bl in ("bench_full.log", "bench.log"):
+    if os.path.exists(f"{G}/{bl}"):
+        json.dump(last_json(f"{G}/{bl}"), open(f"{P}/{ROUND}_bench.json", "w"), indent=1)
+        break
 if os.path.exists(f"{G}/bench_ref.log"):
     json.dump(last_json(f"{G}/bench_ref.log"), open(f"{P}/{ROUND}_bench_reference.json", "w"), indent=1)
 if os.path.exists(f"{G}/launches.csv"):
@@ -30,7 +33,7 @@ for name in sorted(os.listdir(G)):
         continue
     tag = name[len("full_"):-len(".ncu-rep")]
     fn, width, dist = tag.split("_", 2)
-    n = 1 << 24
+    n = N
     summ = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"),
                            os.path.join(G, name), str(n)], capture_output=True, text=True).stdout
     open(f"{P}/{ROUND}_ncu_full_{tag}.txt", "w").write(summ)
@@ -47,7 +50,8 @@ for name in sorted(os.listdir(G)):
     rd = float(val[hdr.index("dram__bytes_read.sum")].replace(",", "")) * scale[unit[hdr.index("dram__bytes_read.sum")]]
     wr = float(val[hdr.index("dram__bytes_write.sum")].replace(",", "")) * scale[unit[hdr.index("dram__bytes_write.sum")]]
     ty = "double" if width == "64" else "float"
-    traffic[f"k_eval<{ty},{fn}>"] = {
+    key = f"cfg5_{fn}_f64" if dist in ("exp64s", "logu64s") else f"k_eval<{ty},{fn}>"
+    traffic[key] = {
         "dram_read_bytes": rd, "dram_write_bytes": wr, "elements": n,
         "algorithmic_bytes": n * (32 if width == "64" else 16),
         "source": f"profiles/{ROUND}_ncu_full_{tag}.txt (ncu --set full)",
