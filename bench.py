@@ -561,6 +561,9 @@ def run_ours(args):
             par32[fn] = {"ref": _compact(_reduce(_host_compare(z0, z1, *ref, 32), dev)),
                          "crsim": _compact(_reduce(_host_compare(z0, z1, *crs, 32), dev))}
 
+    if args.extended and rank == 0:
+        _extended(args, L, dev, stream, sp, gen, peaks)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
@@ -591,6 +594,64 @@ def run_ours(args):
 
         dist.destroy_process_group()
     return 0
+
+
+def _extended(args, L, dev, stream, sp, gen, peaks):
+    """--extended PATH: the sixteen sibling kernels on their family's 2^28-element
+    inputs and the element-wise EFT / twofold-arithmetic ops at 2^25, written to
+    PATH as JSON (kept out of the driver's bench line)."""
+    import torch
+
+    from paper_1502_05216_b200 import DOTTED_ARG, FAMILIES, _lib, api, family_of
+
+    def timed(go, reps):
+        for _ in range(3):
+            go()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            go()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    out = {"siblings": {}, "eft_ops": {}}
+    for fn, width, dname in PER_FN:
+        m = N_PER_FN
+        dt = torch.float64 if width == 64 else torch.float32
+        a0, a1 = gen(dname, m, dt, 0)
+        z0, z1 = torch.empty_like(a0), torch.empty_like(a1)
+        lib = api(width)
+        base = timed(lambda: lib._launch(fn, a0, a1, z0, z1, m, sp), 5)
+        for name in FAMILIES[family_of(fn)]:
+            if name == fn:
+                continue
+            b1 = a0 if name in DOTTED_ARG else a1
+            ms = timed(lambda: lib._launch(name, a0, b1, z0, z1, m, sp), 5)
+            out["siblings"][f"{name}_f{width}"] = {
+                "config_dist": dname, "elements": m, "ms": ms,
+                "elements_per_s": m / (ms * 1e-3), "vs_" + fn: base / ms}
+        del a0, a1, z0, z1
+    m = 1 << 25
+    for width in (64, 32):
+        dt = torch.float64 if width == 64 else torch.float32
+        sz = 8 if width == 64 else 4
+        ops_in = [torch.empty(m, dtype=dt, device=dev).uniform_(1.0, 2.0) for _ in range(4)]
+        z0, z1 = torch.empty_like(ops_in[0]), torch.empty_like(ops_in[0])
+        ptrs = [a.data_ptr() for a in ops_in]
+        for op, code in _lib.OP_CODES.items():
+            for backend in ((0, 1) if op in EFT_BACKEND_OPS else (0,)):
+                def go(code=code, backend=backend):
+                    _lib.check(L.tf_eft(code, width, backend, *ptrs, z0.data_ptr(), z1.data_ptr(),
+                                        m, sp), "tf_eft")
+                ms = timed(go, 10)
+                gbs = (EFT_ARRAYS_IN[op] + 2) * sz * m / (ms * 1e-3) / 1e9
+                out["eft_ops"][f"{op}{'_dv' if backend else ''}_f{width}"] = {
+                    "elements_per_s": m / (ms * 1e-3), "ms": ms, "hbm_gbs": gbs,
+                    "hbm_frac": gbs / peaks["hbm_gbs"]}
+        del ops_in, z0, z1
+    with open(args.extended, "w") as f:
+        json.dump(out, f, indent=1)
 
 
 def shard(total: int, rank: int, world: int) -> tuple[int, int]:
@@ -706,6 +767,8 @@ def main():
     ap.add_argument("--parity32-sample", type=int, default=1 << 22)
     ap.add_argument("--e2e-steps", type=int, default=1 << 30)
     ap.add_argument("--headline-only", action="store_true")
+    ap.add_argument("--extended", default=None, metavar="PATH",
+                    help="also time the sibling kernels and the EFT ops, JSON to PATH")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--streams", type=int, default=2, choices=(1, 2),
