@@ -1427,22 +1427,41 @@ TF_DEV TF<f2> taylor_exp_p(f2 yp) {                 // taylor_exp_v<float>'s pac
   return tp;
 }
 
+// decompose_exp (expcore.py:35-48) of a lane pair: M = RNE(32 x) by the magic
+// constant and the exact y = x - M/32 as two packed FMAs and one FADD2 (the
+// same IEEE ops per lane as decomp_exp_u), then m, n = sign(M) (|M| div/mod 64)
+// as (M + (M < 0 ? 63 : 0)) >> 6 and M - 64 m.  Rejected lanes take M = 0 (the
+// table indices stay in range; their y is discarded with their result).
+TF_DEV f2 decomp_exp_p(f2 x, const bool (&okp)[2], int (&m)[2], int (&n)[2]) {
+  const f2 mg = splat(12582912.0f);                     // 1.5 * 2^23
+  const f2 t = fmaop(x, splat(32.0f), mg);
+  const f2 y = fmaop(sub(t, mg), splat(-0.03125f), x);
+  const float tl[2] = {lo(t), hi(t)};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int M = okp[h] ? (int)ubits(tl[h]) - 0x4b400000 : 0;
+    m[h] = (M + ((M >> 31) & 63)) >> 6;
+    n[h] = M - (m[h] << 6);
+  }
+  return y;
+}
+
 template <int VW, bool PM = false>
 TF_DEV void fast_texp_p(const STab<float>& tb, const float (&x0)[VW], const float (&x1)[VW],
                         float (&z0)[VW], float (&z1)[VW], bool (&ok)[VW]) {
   static_assert(VW % 2 == 0, "lane pairs");
-  float y[VW];
   int m[VW], n[VW];
 #pragma unroll
-  for (int e = 0; e < VW; ++e) {
+  for (int e = 0; e < VW; ++e)
     ok[e] = x0[e] >= -__uint_as_float(B32_TEXP_NEG) && x0[e] <= __uint_as_float(B32_TEXP_POS) &&
             fabsf(x1[e]) < __uint_as_float(B32_X1_TINY);
-    decomp_exp_u(ok[e] ? x0[e] : 0.0f, m[e], n[e], y[e]);
-  }
 #pragma unroll
   for (int p = 0; p < VW / 2; ++p) {
     const int a = 2 * p, b = 2 * p + 1;
-    const TF<f2> t = taylor_exp_p(pk(y[a], y[b]));
+    int mm[2], nn[2];
+    const f2 yp = decomp_exp_p(pk(x0[a], x0[b]), {ok[a], ok[b]}, mm, nn);
+    m[a] = mm[0]; m[b] = mm[1]; n[a] = nn[0]; n[b] = nn[1];
+    const TF<f2> t = taylor_exp_p(yp);
     const TF<f2> ct = t_mul_u(ldpair(tb.C, n[a] - P<float>::C_LO, n[b] - P<float>::C_LO), t);
     const TF<f2> ev = ldpair(tb.E, m[a] - P<float>::E_LO, m[b] - P<float>::E_LO);
     const TF<f2> v = t_mul_u(ev, ct);
@@ -1472,18 +1491,18 @@ template <int VW, bool PM = false>
 TF_DEV void fast_texpm1_p(const STab<float>& tb, const float (&x0)[VW], const float (&x1)[VW],
                           float (&z0)[VW], float (&z1)[VW], bool (&ok)[VW]) {
   static_assert(VW % 2 == 0, "lane pairs");
-  float y[VW];
   int m[VW], n[VW];
 #pragma unroll
-  for (int e = 0; e < VW; ++e) {
+  for (int e = 0; e < VW; ++e)
     ok[e] = fabsf(x0[e]) > __uint_as_float(B32_LN2) && x0[e] >= -__uint_as_float(B32_LO) &&
             x0[e] <= __uint_as_float(B32_TEXP_POS) && fabsf(x1[e]) < __uint_as_float(B32_X1_TINY);
-    decomp_exp_u(ok[e] ? x0[e] : 1.0f, m[e], n[e], y[e]);
-  }
 #pragma unroll
   for (int p = 0; p < VW / 2; ++p) {
     const int a = 2 * p, b = 2 * p + 1;
-    const TF<f2> t = taylor_exp_p(pk(y[a], y[b]));
+    int mm[2], nn[2];
+    const f2 yp = decomp_exp_p(pk(x0[a], x0[b]), {ok[a], ok[b]}, mm, nn);
+    m[a] = mm[0]; m[b] = mm[1]; n[a] = nn[0]; n[b] = nn[1];
+    const TF<f2> t = taylor_exp_p(yp);
     const TF<f2> v = t_mul_u(ldpair(tb.E, m[a] - P<float>::E_LO, m[b] - P<float>::E_LO),
                              t_mul_u(ldpair(tb.C, n[a] - P<float>::C_LO, n[b] - P<float>::C_LO), t));
     const TF<f2> w = t_add_d_u(v, splat(-1.0f));             // expcore.py:147
