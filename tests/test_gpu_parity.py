@@ -504,3 +504,30 @@ def test_random_bit_patterns(fn, width, cuda):
     rk = compare(a0[keep], a1[keep], *[v[keep] for v in _crsim(fn, width, x0, x1, "fma")], width)
     assert r["class_mismatch"] == 0, r
     assert rk["tol_violations"] == 0, rk
+
+
+@pytest.mark.parametrize("cfg", ("cfg5_texp_f64", "cfg5_tlog_f64"))
+def test_cfg5_full_default_path_equals_exact_path(cfg, cuda):
+    """Every one of the 2^30 config-5 elements (1% specials): the default path
+    (admission band, constant-class drain, second-chance evaluators) equals the
+    forced exact-path restatement bit for bit -- the size-independent form of
+    the oracle gate at the BASELINE size."""
+    import torch
+
+    from paper_1502_05216_b200 import _lib, api, workloads
+
+    fn, width, dist, n = workloads.CONFIGS[cfg]
+    L = _lib.ensure_device(cuda.index)
+    x0 = torch.empty(n, dtype=torch.float64, device=cuda)
+    x1 = torch.empty(n, dtype=torch.float64, device=cuda)
+    _lib.check(L.tf_generate(_lib.DIST_CODES[dist], 2024, 0, n, x0.data_ptr(), x1.data_ptr(),
+                             None), "gen")
+    lib = api(64)
+    a = lib._device(fn, x0, x1)
+    b = lib._device(fn, x0, x1, flags=_lib.FLAG_FORCE_EXACT)
+    torch.cuda.synchronize()
+    for u, v in ((a.value, b.value), (a.error, b.error)):
+        same = (u.view(torch.int64) == v.view(torch.int64)) | (torch.isnan(u) & torch.isnan(v))
+        assert bool(same.all()), int((~same).sum())
+    del x0, x1, a, b
+    torch.cuda.empty_cache()
