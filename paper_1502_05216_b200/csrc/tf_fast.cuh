@@ -790,11 +790,18 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     // positive normal y0 (below 2^1022 / 2^126) and finite y1; how small y1 is
     // against y0 is checked on d = y1/y0 below, where it matters
     ok[e] = C::eb(y0s) - 1u < SPAN && is_finite(y1i[e]);
-    y0[e] = ok[e] ? y0s : T(1);
-    y1[e] = ok[e] ? y1i[e] : T(0);
+    if constexpr (sizeof(T) == 8) {
+      // binary64: rejected lanes compute on whatever they hold (no selects
+      // here): the seed index is clamped and the CM1 index masked below
+      y0[e] = y0s;
+      y1[e] = y1i[e];
+    } else {
+      y0[e] = ok[e] ? y0s : T(1);
+      y1[e] = ok[e] ? y1i[e] : T(0);
+    }
     v[e] = RENORM ? renorm_u(mk(y0[e], y1[e])) : mk(y0[e], y1[e]);
     ok[e] = ok[e] && C::eb(v[e].v) - 1u < SPAN;
-    if (!ok[e]) v[e] = mk(T(1), T(0));
+    if (sizeof(T) == 4 && !ok[e]) v[e] = mk(T(1), T(0));
     auto vb = ubits(v[e].v);
     bool band = vb >= C::HALF && vb <= C::TWO;
     n[e] = band ? 0 : C::n_of(v[e].v) - (subn ? C::SUBSH : 0);
@@ -837,11 +844,20 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     // near-1 series (only |log y0| < ~2^-11 is sent away)
     const bool dsmall = sizeof(T) == 4 || ahi(d0) + (42u << 20) <= ahi(core.v);
     bool hard;
-    dl[e] = sub(y0[e], T(1));                         // exact near 1
-    if constexpr (DBLV && sizeof(T) == 4) {
+    if constexpr (sizeof(T) == 8) {
+      // |y0 - 1| < 2^-20 on the bit pattern (no DADD); y0 - 1 (exact there) is
+      // formed in the near-1 pass only
+      dl[e] = y0[e];
+      z0[e] = rn_guard<TF_TOL32_LOG>(core.v, sub(core.e, d0), hard);
+      if (ubits(y0[e]) - 0x3FEFFFFE00000001ull < 0x3FF0000010000000ull - 0x3FEFFFFE00000001ull)
+        near |= 1u << e;
+      else ok[e] = ok[e] && !hard && dsmall;
+    } else if constexpr (DBLV) {
+      dl[e] = sub(y0[e], T(1));
       z0[e] = cr32_lib<DF_LOG>(y0[e], hard);
       ok[e] = ok[e] && !hard;
     } else {
+      dl[e] = sub(y0[e], T(1));                       // exact near 1
       z0[e] = rn_guard<TF_TOL32_LOG>(core.v, sub(core.e, d0), hard);
       if (ahi(dl[e]) < C::NEAR1H) near |= 1u << e;
       else ok[e] = ok[e] && !hard && dsmall;
@@ -861,7 +877,7 @@ TF_DEV void fast_tlog(const STab<T>& tb, const T (&y0i)[VW], const T (&y1i)[VW],
     bool hn = false;
     T r;
     if constexpr (sizeof(T) == 4) r = log_near1_g(d, hn);
-    else r = log_near1(d);
+    else r = log_near1(sub(d, T(1)));                 // dl holds y0 (binary64)
 #pragma unroll
     for (int e = 0; e < VW; ++e)
       if (low == 1u << e) { z0[e] = r; ok[e] = ok[e] && !hn; }
