@@ -14,6 +14,8 @@
 // kernel time per chunk is ~2% of the copy time.
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <chrono>
 #include <cstring>
 #include <mutex>
 
@@ -90,14 +92,19 @@ int setup(HostPipe& p, int64_t bytes) {
 
 // Small calls (the reference's own scalar convention, audit.py:343-349: one
 // element per call) skip the chunk pipeline: the operands go into a mapped
-// pinned buffer the kernel reads and writes directly over PCIe (zero-copy),
-// so a call costs one kernel launch and one stream synchronisation.
+// pinned buffer the kernel reads and writes directly over PCIe (zero-copy).
+// Up to 32 elements take the tiny kernel: operands by value with the launch,
+// results into the mapped buffer, then a sequence number into a mapped flag: the caller spins on that flag instead of
+// synchronising the stream (a kernel that never stores it -- a launch or
+// device fault -- is caught by the bounded spin, then the stream status).
 constexpr int64_t SMALL_N = 1024;
+constexpr int64_t TINY_N = 32;
 struct SmallBuf {
   bool ready = false;
-  void* host = nullptr;  // 4 x SMALL_N doubles, cudaHostAllocMapped
+  void* host = nullptr;  // 4 x SMALL_N doubles + the completion flag, cudaHostAllocMapped
   void* dev = nullptr;   // its device alias
   cudaStream_t own = nullptr;  // used when the caller passes no stream
+  unsigned seq = 0;
   std::mutex mu;
 };
 SmallBuf g_small[MAX_DEV];
@@ -106,25 +113,48 @@ int eval_small(int dev, int fn, int width, const void* x0, const void* x1, void*
                int64_t n, bool dotted, void* stream, int flags) {
   SmallBuf& b = g_small[dev];
   std::lock_guard<std::mutex> lk(b.mu);
+  const size_t slot = SMALL_N * sizeof(double);
   if (!b.ready) {
-    if (cudaHostAlloc(&b.host, 4 * SMALL_N * sizeof(double), cudaHostAllocMapped) != cudaSuccess ||
+    if (cudaHostAlloc(&b.host, 4 * slot + 64, cudaHostAllocMapped) != cudaSuccess ||
         cudaHostGetDevicePointer(&b.dev, b.host, 0) != cudaSuccess ||
         cudaStreamCreateWithFlags(&b.own, cudaStreamNonBlocking) != cudaSuccess)
       return cuda_check("tf_eval_host: mapped staging buffer");
+    *static_cast<volatile unsigned*>(static_cast<void*>(static_cast<char*>(b.host) + 4 * slot)) = 0;
     b.ready = true;
   }
   // no caller stream: a library stream that does not serialise with the
   // device's other work (the operands are host values, nothing to wait for)
   if (!stream) stream = b.own;
-  const size_t sz = width / 8, bytes = (size_t)n * sz, slot = SMALL_N * sizeof(double);
+  const size_t sz = width / 8, bytes = (size_t)n * sz;
   char* h = static_cast<char*>(b.host);
   char* d = static_cast<char*>(b.dev);
-  memcpy(h, x0, bytes);
-  if (!dotted) memcpy(h + slot, x1, bytes);
-  int rc = tf_eval(fn, width, d, dotted ? d : d + slot, d + 2 * slot, d + 3 * slot, n, stream, flags);
-  if (rc) return rc;
-  if (cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) != cudaSuccess)
-    return cuda_check("tf_eval_host: small-call synchronisation");
+  if (n <= TINY_N && flags == 0) {
+    volatile unsigned* flag = reinterpret_cast<volatile unsigned*>(h + 4 * slot);
+    const unsigned seq = ++b.seq ? b.seq : ++b.seq;   // never 0 (the initial value)
+    int rc = tfabi::tiny_eval(fn, width, x0, dotted ? x0 : x1, d + 2 * slot, d + 3 * slot, n,
+                              stream, reinterpret_cast<unsigned*>(d + 4 * slot), seq);
+    if (rc) return rc;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned k = 0; *flag != seq; ++k) {
+      if ((k & 1023) == 1023 &&
+          std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(50)) {
+        // slow (a busy device) or failed: the stream decides
+        if (cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) != cudaSuccess)
+          return cuda_check("tf_eval_host: small-call synchronisation");
+        if (*flag != seq) return fail(TF_ERR_CUDA, "tf_eval_host: tiny kernel did not complete%s");
+        break;
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+  } else {
+    memcpy(h, x0, bytes);
+    if (!dotted) memcpy(h + slot, x1, bytes);
+    int rc = tf_eval(fn, width, d, dotted ? d : d + slot, d + 2 * slot, d + 3 * slot, n, stream,
+                     flags);
+    if (rc) return rc;
+    if (cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) != cudaSuccess)
+      return cuda_check("tf_eval_host: small-call synchronisation");
+  }
   memcpy(z0, h + 2 * slot, bytes);
   memcpy(z1, h + 3 * slot, bytes);
   return TF_OK;

@@ -187,6 +187,21 @@ template <int N> TF_DEV void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// One element the admission band rejected: the constant-result specials, then
+// the second-chance fast evaluator, then the exact path (force: the exact path
+// alone).  Returns true when the exact path ran.
+template <class T, int FN>
+TF_DEV bool rare_eval(const STab<T>& tb, T a, T b, bool force, T& r0, T& r1) {
+  bool done = !force && special_const<T, FN>(a, b, r0, r1);
+  if constexpr (HasAlt<T, FN>::value)
+    if (!done) done = !force && fast_alt<T, FN>(tb, a, b, r0, r1);
+  if (done) return false;
+  TF<T> r = eval_gen<T, FN>(a, b);
+  r0 = r.v;
+  r1 = r.e;
+  return true;
+}
+
 // Evaluate the queued rare elements (q, qa, qb)[0..cnt) (cnt <= 32) with the
 // exact path; the operands come from the queue, not from x0 / x1.
 template <class T, int FN>
@@ -203,17 +218,7 @@ TF_DEV void drain(const STab<T>& tb, const uint32_t* q, const T* qa, const T* qb
       z1[i] = T(-12345);
     } else {
       T r0, r1;
-      // constant-result specials, then the second-chance fast evaluator, then
-      // the exact path (TF_FLAG_FORCE_EXACT: the exact path alone)
-      bool done = !force && special_const<T, FN>(a, b, r0, r1);
-      if constexpr (HasAlt<T, FN>::value)
-        if (!done) done = !force && fast_alt<T, FN>(tb, a, b, r0, r1);
-      if (!done) {
-        TF<T> r = eval_gen<T, FN>(a, b);
-        r0 = r.v;
-        r1 = r.e;
-        exact = true;
-      }
+      exact = rare_eval<T, FN>(tb, a, b, force, r0, r1);
       z0[i] = r0;
       z1[i] = r1;
     }
@@ -488,17 +493,48 @@ k_eval(const T* x0, const T* x1, T* z0, T* z1, uint32_t n, int flags) {
 }
 
 // Tiny launches (n <= 32, e.g. the reference's one-element calls): one warp
-// runs the exact path straight from the global tables, with no table staging
-// -- bit-identical to the admission-band kernels (tests/test_gpu_parity.py
-// fast == exact), and a fraction of their fixed launch cost.
+// runs the main kernel's per-element sequence -- the admission-band fast path
+// (VW = 1), and for a rejected element rare_eval -- on tables held in global
+// memory (staged once per device by k_gtab_init, L2-resident between calls),
+// so there is no per-launch table staging.  Bit-identical to the main kernel
+// (tests/test_gpu_abi_entry.py checks every 32-element window of the golden
+// files).  `done` (small host calls): after the results, the lane-0 store of
+// `seq` to mapped host memory tells the spinning caller they are visible.
+__device__ STab<double> g_gt64;
+__device__ STab<float> g_gt32;
+template <class T> TF_DEV const STab<T>& gtab();
+template <> TF_DEV const STab<double>& gtab<double>() { return g_gt64; }
+template <> TF_DEV const STab<float>& gtab<float>() { return g_gt32; }
+
+__global__ void __launch_bounds__(1024) k_gtab_init() {
+  load_tables(g_gt64, true);
+  load_tables(g_gt32, true);
+}
+
+// operands by value (small host calls): they arrive with the launch instead of
+// being read back over PCIe from mapped host memory
+template <class T> struct TinyArgs { T x0[32], x1[32]; };
+
 template <class T, int FN>
-__global__ void __launch_bounds__(32) k_tiny(const T* x0, const T* x1, T* z0, T* z1, int n) {
+__global__ void __launch_bounds__(32) k_tiny(const T* x0, const T* x1, T* z0, T* z1, int n,
+                                             unsigned* done, unsigned seq,
+                                             const __grid_constant__ TinyArgs<T> v) {
   const int i = threadIdx.x;
   if (i < n) {
-    const T a = x0[i], b = dotted_fn(FN) ? T(0) : x1[i];
-    const TF<T> r = eval_gen<T, FN>(a, b);
-    z0[i] = r.v;
-    z1[i] = r.e;
+    const T a = x0 ? x0[i] : v.x0[i];
+    const T b = dotted_fn(FN) ? T(0) : x0 ? x1[i] : v.x1[i];
+    const STab<T>& tb = gtab<T>();
+    T aa[1] = {a}, bb[1] = {b}, r0[1], r1[1];
+    bool ok[1];
+    fast_eval<T, FN, 1>(tb, nullptr, aa, bb, r0, r1, ok);
+    if (!ok[0]) rare_eval<T, FN>(tb, a, b, false, r0[0], r1[0]);
+    z0[i] = r0[0];
+    z1[i] = r1[0];
+  }
+  if (done) {
+    __threadfence_system();
+    __syncwarp();
+    if (i == 0) *reinterpret_cast<volatile unsigned*>(done) = seq;
   }
 }
 
@@ -744,15 +780,51 @@ int launch_one(const T* x0, const T* x1, T* z0, T* z1, int64_t n, cudaStream_t s
   return cuda_check("k_eval launch");
 }
 
+// The tiny kernels' global-memory tables: staged once per device, on a private
+// stream, synchronously (so no launch on any stream can see them half-written).
+std::atomic<bool> g_gtab_ready[64];
+std::mutex g_gtab_mu;
+int ensure_gtab() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return cuda_check("cudaGetDevice");
+  if (g_gtab_ready[d].load(std::memory_order_acquire)) return TF_OK;
+  std::lock_guard<std::mutex> lk(g_gtab_mu);
+  if (g_gtab_ready[d].load(std::memory_order_relaxed)) return TF_OK;
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+    return cuda_check("tiny-kernel tables: stream");
+  tf::k_gtab_init<<<1, 1024, 0, st>>>();
+  const cudaError_t e = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess) return cuda_check("tiny-kernel tables: staging");
+  g_gtab_ready[d].store(true, std::memory_order_release);
+  return TF_OK;
+}
+
+// done / seq: completion flag of a small host call (tf_host.cu), tiny launches only
 template <class T, int FN>
-int launch(const T* x0, const T* x1, T* z0, T* z1, int64_t n, void* stream, int flags) {
+int launch(const T* x0, const T* x1, T* z0, T* z1, int64_t n, void* stream, int flags,
+           unsigned* done = nullptr, unsigned seq = 0) {
   if (n < 0) return fail(TF_ERR_ARG, "negative element count%s");
   if (n == 0) return TF_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (done) {
+    // small host call: x0 / x1 are HOST operands, passed by value
+    if (n > 32 || flags) return fail(TF_ERR_ARG, "completion flag on a launch that is not tiny%s");
+    const int rc = ensure_gtab();
+    if (rc) return rc;
+    tf::TinyArgs<T> v;
+    memcpy(v.x0, x0, (size_t)n * sizeof(T));
+    if (!tf::dotted_fn(FN)) memcpy(v.x1, x1, (size_t)n * sizeof(T));
+    tf::k_tiny<T, FN><<<1, 32, 0, s>>>(nullptr, nullptr, z0, z1, (int)n, done, seq, v);
+    return cuda_check("k_tiny launch");
+  }
   if (tf::dotted_fn(FN) && !x1) x1 = x0;  // plain-argument functions never read x1
   if (!x0 || !x1 || !z0 || !z1) return fail(TF_ERR_ARG, "null pointer%s");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n <= 32 && flags == 0) {
-    tf::k_tiny<T, FN><<<1, 32, 0, s>>>(x0, x1, z0, z1, (int)n);
+    const int rc = ensure_gtab();
+    if (rc) return rc;
+    tf::k_tiny<T, FN><<<1, 32, 0, s>>>(x0, x1, z0, z1, (int)n, nullptr, 0u, tf::TinyArgs<T>{});
     return cuda_check("k_tiny launch");
   }
   uintptr_t al = (uintptr_t)x0 | (uintptr_t)x1 | (uintptr_t)z0 | (uintptr_t)z1;
@@ -815,29 +887,46 @@ uint64_t mix64h(uint64_t z) {
 }  // namespace
 
 template <class T>
-int eval_dispatch(int fn, const T* a, const T* b, T* c, T* d, int64_t n, void* st, int fl) {
+int eval_dispatch(int fn, const T* a, const T* b, T* c, T* d, int64_t n, void* st, int fl,
+                  unsigned* dn = nullptr, unsigned sq = 0) {
   switch (fn) {
     // texpp / texpm1p are texp / texpm1 (explog.py:127-129, 162-163)
-    case TF_FN_TEXP: case TF_FN_TEXPP: return launch<T, tf::FN_TEXP>(a, b, c, d, n, st, fl);
-    case TF_FN_TEXPM1: case TF_FN_TEXPM1P: return launch<T, tf::FN_TEXPM1>(a, b, c, d, n, st, fl);
-    case TF_FN_TLOG: return launch<T, tf::FN_TLOG>(a, b, c, d, n, st, fl);
-    case TF_FN_TLOG1P: return launch<T, tf::FN_TLOG1P>(a, b, c, d, n, st, fl);
-    case TF_FN_PEXP: return launch<T, tf::FN_PEXP>(a, b, c, d, n, st, fl);
-    case TF_FN_PEXPM1: return launch<T, tf::FN_PEXPM1>(a, b, c, d, n, st, fl);
-    case TF_FN_PEXP0: return launch<T, tf::FN_PEXP0>(a, b, c, d, n, st, fl);
-    case TF_FN_TEXP0: return launch<T, tf::FN_TEXP0>(a, b, c, d, n, st, fl);
-    case TF_FN_PEXPM10: return launch<T, tf::FN_PEXPM10>(a, b, c, d, n, st, fl);
-    case TF_FN_TEXPM10: return launch<T, tf::FN_TEXPM10>(a, b, c, d, n, st, fl);
-    case TF_FN_PLOG0: return launch<T, tf::FN_PLOG0>(a, b, c, d, n, st, fl);
-    case TF_FN_TLOG0: return launch<T, tf::FN_TLOG0>(a, b, c, d, n, st, fl);
-    case TF_FN_TLOGP: return launch<T, tf::FN_TLOGP>(a, b, c, d, n, st, fl);
-    case TF_FN_PLOG: return launch<T, tf::FN_PLOG>(a, b, c, d, n, st, fl);
-    case TF_FN_PLOG1P0: return launch<T, tf::FN_PLOG1P0>(a, b, c, d, n, st, fl);
-    case TF_FN_TLOG1P0: return launch<T, tf::FN_TLOG1P0>(a, b, c, d, n, st, fl);
-    case TF_FN_TLOG1PP: return launch<T, tf::FN_TLOG1PP>(a, b, c, d, n, st, fl);
-    case TF_FN_PLOG1P: return launch<T, tf::FN_PLOG1P>(a, b, c, d, n, st, fl);
+    case TF_FN_TEXP: case TF_FN_TEXPP: return launch<T, tf::FN_TEXP>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_TEXPM1: case TF_FN_TEXPM1P: return launch<T, tf::FN_TEXPM1>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_TLOG: return launch<T, tf::FN_TLOG>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_TLOG1P: return launch<T, tf::FN_TLOG1P>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_PEXP: return launch<T, tf::FN_PEXP>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_PEXPM1: return launch<T, tf::FN_PEXPM1>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_PEXP0: return launch<T, tf::FN_PEXP0>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_TEXP0: return launch<T, tf::FN_TEXP0>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_PEXPM10: return launch<T, tf::FN_PEXPM10>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_TEXPM10: return launch<T, tf::FN_TEXPM10>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_PLOG0: return launch<T, tf::FN_PLOG0>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_TLOG0: return launch<T, tf::FN_TLOG0>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_TLOGP: return launch<T, tf::FN_TLOGP>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_PLOG: return launch<T, tf::FN_PLOG>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_PLOG1P0: return launch<T, tf::FN_PLOG1P0>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_TLOG1P0: return launch<T, tf::FN_TLOG1P0>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_TLOG1PP: return launch<T, tf::FN_TLOG1PP>(a, b, c, d, n, st, fl, dn, sq);
+    case TF_FN_PLOG1P: return launch<T, tf::FN_PLOG1P>(a, b, c, d, n, st, fl, dn, sq);
   }
   return fail(TF_ERR_ARG, "unknown function code%s");
+}
+
+// small host calls (tf_host.cu): a tiny launch that signals completion through
+// a flag in mapped host memory
+int tfabi::tiny_eval(int fn, int width, const void* x0, const void* x1, void* z0, void* z1,
+                     int64_t n, void* stream, unsigned* done, unsigned seq) {
+  if (n < 1 || n > 32) return fail(TF_ERR_ARG, "tiny launch size out of range%s");
+  if (width == 64)
+    return eval_dispatch<double>(fn, static_cast<const double*>(x0), static_cast<const double*>(x1),
+                                 static_cast<double*>(z0), static_cast<double*>(z1), n, stream, 0,
+                                 done, seq);
+  if (width == 32)
+    return eval_dispatch<float>(fn, static_cast<const float*>(x0), static_cast<const float*>(x1),
+                                static_cast<float*>(z0), static_cast<float*>(z1), n, stream, 0,
+                                done, seq);
+  return fail(TF_ERR_ARG, "unsupported width (expected 32 or 64)%s");
 }
 
 extern "C" {
@@ -849,7 +938,8 @@ TF_API const char* tf_last_error(void) { return g_err; }
 TF_API int tf_init(int device) {
   if (device >= 0 && cudaSetDevice(device) != cudaSuccess) return cuda_check("cudaSetDevice");
   device_sms();
-  return ensure_constants();
+  const int rc = ensure_gtab();
+  return rc ? rc : ensure_constants();
 }
 
 #define TF_DEF(NAME, T, FN)                                                                \

@@ -28,6 +28,7 @@ where the reference raises OverflowError for a non-coupled argument
 from __future__ import annotations
 
 import ctypes
+from ctypes import byref
 from functools import lru_cache
 
 import numpy as np
@@ -191,6 +192,15 @@ class ExpLog:
 
     # ---- dispatch
     def _call(self, fn: str, x, out=None):
+        # one element on Python floats, the reference's own calling convention
+        # (audit.py:343-349): straight to the small-call path
+        tx = type(x)
+        if tx is Twofold or tx is tuple:
+            if (out is None and len(x) == 2 and type(x[0]) is float and type(x[1]) is float
+                    and fn not in DOTTED_ARG):
+                return self._scalar(fn, x[0], x[1])
+        elif tx is float and out is None and fn in DOTTED_ARG:
+            return self._scalar(fn, x, x)
         if fn in DOTTED_ARG:
             # plain argument: the kernel never reads x1, so alias it to x0
             if isinstance(x, Twofold) or isinstance(x, tuple):
@@ -218,14 +228,17 @@ class ExpLog:
     def _scalar(self, fn, x0, x1):
         """One element, the reference's own calling convention (audit.py:343-349):
         straight through tf_eval_host's small-call path (operands in a mapped
-        pinned buffer the kernel reads over PCIe; one launch, one sync)."""
-        L = _lib.scalar_device()
+        pinned buffer the tiny kernel reads over PCIe; one launch, then a spin on
+        the completion flag the kernel stores after its results)."""
+        L = _lib._lib or _lib.scalar_device()
         ct = self._ct
-        a0, a1, z0, z1 = ct(x0), ct(x1), ct(), ct()
+        z0, z1 = ct(), ct()
+        # the device is the calling thread's current one (the library reads it
+        # from the driver's current context, which torch.cuda.set_device sets);
         # stream NULL: the library's own non-blocking stream (host operands,
-        # nothing on the device to order after)
-        rc = L.tf_eval_host(_lib.FN_CODES[fn], self.width, ctypes.byref(a0), ctypes.byref(a1),
-                            ctypes.byref(z0), ctypes.byref(z1), 1, 0, None, 0)
+        # nothing on the device to order after).  No GPU: rc reports it.
+        rc = L.tf_eval_host(_lib.FN_CODES[fn], self.width, byref(ct(x0)), byref(ct(x1)),
+                            byref(z0), byref(z1), 1, 0, None, 0)
         if rc:
             _lib.check(rc, f"tf_eval_host({fn}, width={self.width})")
         return Twofold(z0.value, z1.value)

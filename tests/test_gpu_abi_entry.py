@@ -169,8 +169,9 @@ def test_named_entry_point_scalar_c_form(cuda):
 @pytest.mark.parametrize("width", (64, 32))
 @pytest.mark.parametrize("fn", ALL_FNS)
 def test_tiny_launch_equals_full_kernel(fn, width, golden, cuda):
-    """n <= 32 runs the one-warp k_tiny (exact path, global tables); every
-    32-element window of the golden vectors must equal the admission-band
+    """n <= 32 runs the one-warp k_tiny (the same fast path and rare-element
+    sequence at one lane per thread, tables in global memory); every 32-element
+    window of the golden vectors must equal the admission-band
     kernel's result on the whole array bit for bit."""
     from paper_1502_05216_b200 import api
 

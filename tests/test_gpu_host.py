@@ -178,6 +178,39 @@ def test_scalar_calls_equal_array_calls(fn, width, cuda):
         assert same1 or (np.isnan(r.error) and np.isnan(z1[i]))
 
 
+@pytest.mark.parametrize("width", (64, 32))
+def test_scalar_twofold_dotted_and_thread_calls(width, cuda):
+    """The reference's own scalar forms -- a Twofold of Python floats, a plain
+    float for the dotted functions (audit.py:334-349) -- and calls from a
+    second host thread all equal the device path bit for bit."""
+    import threading
+
+    import numpy as np
+
+    from paper_1502_05216_b200 import Twofold, api
+
+    lib = api(width)
+    x0, x1 = _inputs("texp", width, 16)
+    z0, z1 = _device_ref("texp", width, x0, x1)
+    d0, d1 = _device_ref("texp0", width, x0, np.zeros_like(x0))
+    got = {}
+
+    def run(key):
+        got[key] = [(lib.texp(Twofold(float(x0[i]), float(x1[i]))), lib.texp0(float(x0[i])))
+                    for i in range(16)]
+
+    run("main")
+    t = threading.Thread(target=run, args=("thread",))
+    t.start()
+    t.join()
+    for key, res in got.items():
+        for i, (r, r0) in enumerate(res):
+            assert np.array([r.value, r.error], dtype=x0.dtype).tobytes() == \
+                np.array([z0[i], z1[i]], dtype=x0.dtype).tobytes(), (key, i)
+            assert np.array([r0.value, r0.error], dtype=x0.dtype).tobytes() == \
+                np.array([d0[i], d1[i]], dtype=x0.dtype).tobytes(), (key, i)
+
+
 def test_small_host_arrays_use_mapped_path(cuda):
     """n <= 1024 host arrays go through the small-call path; results equal the
     chunked pipeline's bit for bit."""
