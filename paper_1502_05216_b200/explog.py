@@ -240,6 +240,7 @@ class ExpLog:
         rc = L.tf_eval_host(_lib.FN_CODES[fn], self.width, byref(ct(x0)), byref(ct(x1)),
                             byref(z0), byref(z1), 1, 0, None, 0)
         if rc:
+            _lib.scalar_device()          # raises "no CUDA device visible" first
             _lib.check(rc, f"tf_eval_host({fn}, width={self.width})")
         return Twofold(z0.value, z1.value)
 
