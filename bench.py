@@ -263,12 +263,20 @@ def run_ours(args):
     from paper_1502_05216_b200 import Twofold, _lib, api, workloads
 
     rank, world, local = dist_env()
+    if args.dist_backend == "gloo":
+        # code-path check of the N > 1 arm on a box with fewer GPUs: ranks may
+        # share a device (their kernels never wait on one another; the timings
+        # of such a run mean nothing)
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     L = _lib.ensure_device(local)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
@@ -771,6 +779,8 @@ def main():
                     help="also time the sibling kernels and the EFT ops, JSON to PATH")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
+                    help="gloo: exercise the N > 1 code path with ranks sharing GPUs (tests)")
     ap.add_argument("--streams", type=int, default=2, choices=(1, 2),
                     help="run the step's two functions on 1 or 2 streams")
     args = ap.parse_args()

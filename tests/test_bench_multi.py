@@ -15,6 +15,7 @@ import subprocess
 import sys
 
 import numpy as np
+import pytest
 import torch.multiprocessing as mp
 
 from conftest import ROOT
@@ -48,6 +49,30 @@ def test_bench_gpus2_relaunches_reference_arm():
     assert rec["config"] == bench.config_for(2)
     assert rec["e2e"]["h2d_bytes_per_step"] == 0 and rec["value"] > 0
     assert rec["cpu_baseline"]["kind"] == "port"
+
+
+@pytest.mark.gpu
+def test_bench_gpu_arm_two_ranks_code_path():
+    """The GPU arm's N > 1 path -- relaunch, contiguous shards, max-over-ranks
+    timing, the parity merge -- with two ranks over gloo.  On a one-GPU box both
+    ranks share the device (independent kernels, nothing waits across ranks),
+    so this checks the code path, not the scaling."""
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dist-backend", "gloo",
+           "--steps", "3", "--warmup", "3", "--headline-only", "--no-e2e", "--no-cpu",
+           "--parity-sample", "65536", "--parity-host", "4096"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["value"] > 0
+    assert rec["config"]["elements_per_function_per_gpu"] == (1 << 29)
+    for fn in ("texp", "tlog"):
+        n, z0mm, gt1, tol, tolz, cls = rec["parity_cfg5"][fn][:6]
+        assert n == 2 * 65536 and gt1 == 0 and tol == 0 and tolz == 0 and cls == 0
 
 
 def test_bench_world_mismatch_fails_loudly():
