@@ -161,6 +161,17 @@ TF_DEV TF<float> taylor_expm1_u(float y) {    // N_m1=5
 // chains interleave while the hot code stays a few hundred bytes (a fully
 // unrolled 2-lane tlog1p was ~24 KB of SASS and stalled on instruction fetch).
 // Coefficients N!/k! come from constant memory with a warp-uniform index.
+// t_mul_d (eft.py:214-219) of a twofold whose error part is +0 -- the first
+// Horner step of every Taylor core, t = (s, 0): the reference's x1 * b + e
+// rounds the product 0 * b, which is exact (+-0 for finite b), so the single
+// FMA RN(x1 * b + e) is the same IEEE operation, signed zeros included (the
+// sign of an exact-zero sum follows the addition rules in both).  One FP op
+// fewer per lane and core.
+template <class T> TF_DEV TF<T> t_mul_d_z(TF<T> x, T b) {
+  T v = mul(x.v, b);
+  T e = fmaop(x.v, b, -v);
+  return mk(v, fmaop(x.e, b, e));
+}
 template <int VW> TF_DEV void taylor_exp_v(const double (&y)[VW], TF<double> (&t)[VW]) {
 #pragma unroll
   for (int e = 0; e < VW; ++e) {
@@ -170,7 +181,9 @@ template <int VW> TF_DEV void taylor_exp_v(const double (&y)[VW], TF<double> (&t
     t[e] = mk(s, 0.0);
   }
 #pragma unroll
-  for (int k = 0; k < 9; ++k) {
+  for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_z(t[e], y[e]), c_texp64[0]);
+#pragma unroll
+  for (int k = 1; k < 9; ++k) {
     const double c = c_texp64[k];
 #pragma unroll
     for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_u(t[e], y[e]), c);
@@ -183,6 +196,12 @@ TF_DEV TF<f2> t_mul_d_p(TF<f2> x, f2 b, f2 nb) {
   f2 v = mul(x.v, b);
   f2 ne = fmaop(x.v, nb, v);
   return mk(v, sub(mul(x.e, b), ne));
+}
+// the same with x.e = +0 (t_mul_d_z): RN(x1 b - ne) as one FFMA2
+TF_DEV TF<f2> t_mul_d_pz(TF<f2> x, f2 b, f2 nb) {
+  f2 v = mul(x.v, b);
+  f2 ne = fmaop(x.v, nb, v);
+  return mk(v, fmaop(x.e, b, -ne));
 }
 
 template <int VW> TF_DEV void taylor_exp_v(const float (&y)[VW], TF<float> (&t)[VW]) {
@@ -199,7 +218,10 @@ template <int VW> TF_DEV void taylor_exp_v(const float (&y)[VW], TF<float> (&t)[
       tp[p] = mk(s, splat(0.0f));
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int p = 0; p < NP; ++p)
+      tp[p] = t_add_d_u(t_mul_d_pz(tp[p], yp[p], nyp[p]), splat(c_texp32[0]));
+#pragma unroll
+    for (int k = 1; k < 4; ++k) {
       const f2 c = splat(c_texp32[k]);
 #pragma unroll
       for (int p = 0; p < NP; ++p) tp[p] = t_add_d_u(t_mul_d_p(tp[p], yp[p], nyp[p]), c);
@@ -217,7 +239,9 @@ template <int VW> TF_DEV void taylor_exp_v(const float (&y)[VW], TF<float> (&t)[
     t[e] = mk(s, 0.0f);
   }
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_z(t[e], y[e]), c_texp32[0]);
+#pragma unroll
+  for (int k = 1; k < 4; ++k) {
     const float c = c_texp32[k];
 #pragma unroll
     for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_u(t[e], y[e]), c);
@@ -233,7 +257,9 @@ template <int VW> TF_DEV void taylor_expm1_v(const double (&y)[VW], TF<double> (
     t[e] = mk(s, 0.0);
   }
 #pragma unroll
-  for (int k = 0; k < 6; ++k) {
+  for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_z(t[e], y[e]), c_texpm1_64[0]);
+#pragma unroll
+  for (int k = 1; k < 6; ++k) {
     const double c = c_texpm1_64[k];
 #pragma unroll
     for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_u(t[e], y[e]), c);
@@ -256,7 +282,10 @@ template <int VW> TF_DEV void taylor_expm1_v(const float (&y)[VW], TF<float> (&t
       tp[p] = mk(s, splat(0.0f));
     }
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int p = 0; p < NP; ++p)
+      tp[p] = t_add_d_u(t_mul_d_pz(tp[p], yp[p], nyp[p]), splat(c_texpm1_32[0]));
+#pragma unroll
+    for (int k = 1; k < 2; ++k) {
       const f2 c = splat(c_texpm1_32[k]);
 #pragma unroll
       for (int p = 0; p < NP; ++p) tp[p] = t_add_d_u(t_mul_d_p(tp[p], yp[p], nyp[p]), c);
@@ -275,7 +304,9 @@ template <int VW> TF_DEV void taylor_expm1_v(const float (&y)[VW], TF<float> (&t
     t[e] = mk(s, 0.0f);
   }
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_z(t[e], y[e]), c_texpm1_32[0]);
+#pragma unroll
+  for (int k = 1; k < 2; ++k) {
     const float c = c_texpm1_32[k];
 #pragma unroll
     for (int e = 0; e < VW; ++e) t[e] = t_add_d_u(t_mul_d_u(t[e], y[e]), c);
@@ -907,8 +938,8 @@ TF_DEV TF<f2> taylor_expm1_p(f2 yp) {
   f2 s = add(yp, splat(5.0f));
   s = add(mul(s, yp), splat(20.0f));
   TF<f2> tp = mk(s, splat(0.0f));
-#pragma unroll
-  for (int k = 0; k < 2; ++k) tp = t_add_d_u(t_mul_d_p(tp, yp, nyp), splat(c_texpm1_32[k]));
+  tp = t_add_d_u(t_mul_d_pz(tp, yp, nyp), splat(c_texpm1_32[0]));
+  tp = t_add_d_u(t_mul_d_p(tp, yp, nyp), splat(c_texpm1_32[1]));
   return t_mul_u(t_mul_d_p(tp, yp, nyp), mk(splat(P<float>::INVF_V), splat(P<float>::INVF_E)));
 }
 
@@ -1005,6 +1036,8 @@ TF_DEV f2 rn_guard_p(f2 h, f2 l, bool (&hard)[2]) {
 }
 
 // per-lane select of two lane pairs: (c0 ? a.lo : b.lo, c1 ? a.hi : b.hi)
+// (a select on the bit patterns compiles to the same FSEL / SEL mix: ptxas
+// picks the pipe)
 TF_DEV f2 sel2(bool c0, bool c1, f2 a, f2 b) {
   return pk(c0 ? lo(a) : lo(b), c1 ? hi(a) : hi(b));
 }
@@ -1438,8 +1471,9 @@ TF_DEV TF<f2> taylor_exp_p(f2 yp) {                 // taylor_exp_v<float>'s pac
   f2 s = add(yp, splat(6.0f));
   s = add(mul(s, yp), splat(30.0f));
   TF<f2> tp = mk(s, splat(0.0f));
+  tp = t_add_d_u(t_mul_d_pz(tp, yp, nyp), splat(c_texp32[0]));
 #pragma unroll
-  for (int k = 0; k < 4; ++k) tp = t_add_d_u(t_mul_d_p(tp, yp, nyp), splat(c_texp32[k]));
+  for (int k = 1; k < 4; ++k) tp = t_add_d_u(t_mul_d_p(tp, yp, nyp), splat(c_texp32[k]));
   return tp;
 }
 
