@@ -4,9 +4,10 @@
 // methods); this entry point takes HOST arrays and streams them through a
 // three-stage chunk pipeline on the device:
 //
-//   copy-in stream   H2D of chunk k into ring slot k % RING
-//   compute stream   tf_eval of chunk k           (waits for its H2D)
-//   copy-out stream  D2H of chunk k's results     (waits for its kernel)
+//   copy-in streams  H2D of chunk k into ring slot k % RING (x0 and x1 on two
+//                    streams: 95 vs 93 GB/s both directions, tools/pcie_streams_probe.py)
+//   compute stream   tf_eval of chunk k           (waits for both H2D)
+//   copy-out streams D2H of chunk k's results z0 / z1 (wait for its kernel)
 //
 // A slot is refilled only after its previous copy-out completed.  The copy
 // engines therefore run both PCIe directions at once (measured 55 GB/s H2D,
@@ -40,8 +41,9 @@ constexpr int64_t DEFAULT_CHUNK = 1 << 20;
 struct HostPipe {
   bool ready = false;
   int64_t cap_bytes = 0;  // bytes per ring buffer
-  cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
-  cudaEvent_t loaded[RING], done[RING], freed[RING], entry;
+  // two copy streams per direction: x0 / z0 on in / out, x1 / z1 on in2 / out2
+  cudaStream_t in = nullptr, in2 = nullptr, comp = nullptr, out = nullptr, out2 = nullptr;
+  cudaEvent_t loaded[RING], loaded2[RING], done[RING], freed[RING], freed2[RING], entry;
   bool used[RING] = {};
   void* buf[RING][4] = {};
 };
@@ -61,12 +63,16 @@ bool dotted_fn(int fn) {
 int setup(HostPipe& p, int64_t bytes) {
   if (!p.ready) {
     if (cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&p.in2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&p.out2, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&p.comp, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&p.out, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&p.entry, cudaEventDisableTiming) != cudaSuccess)
       return cuda_check("tf_eval_host: stream/event creation");
     for (int s = 0; s < RING; ++s)
       if (cudaEventCreateWithFlags(&p.loaded[s], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&p.loaded2[s], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&p.freed2[s], cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&p.done[s], cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&p.freed[s], cudaEventDisableTiming) != cudaSuccess)
         return cuda_check("tf_eval_host: event creation");
@@ -206,6 +212,8 @@ extern "C" TF_API int tf_eval_host(int fn, int width, const void* x0, const void
     ~Drain() {
       if (!armed) return;
       cudaStreamSynchronize(p.in);
+      cudaStreamSynchronize(p.in2);
+      cudaStreamSynchronize(p.out2);
       cudaStreamSynchronize(p.comp);
       cudaStreamSynchronize(p.out);
       for (int s = 0; s < RING; ++s) p.used[s] = false;
@@ -213,7 +221,8 @@ extern "C" TF_API int tf_eval_host(int fn, int width, const void* x0, const void
   } drain{p};
   // start after the work already queued on the caller's stream
   if (cudaEventRecord(p.entry, static_cast<cudaStream_t>(stream)) != cudaSuccess ||
-      cudaStreamWaitEvent(p.in, p.entry, 0) != cudaSuccess)
+      cudaStreamWaitEvent(p.in, p.entry, 0) != cudaSuccess ||
+      cudaStreamWaitEvent(p.in2, p.entry, 0) != cudaSuccess)
     return cuda_check("tf_eval_host: stream ordering");
   const char* hx0 = static_cast<const char*>(x0);
   const char* hx1 = static_cast<const char*>(x1);
@@ -226,25 +235,34 @@ extern "C" TF_API int tf_eval_host(int fn, int width, const void* x0, const void
     const int s = (int)(k % RING);
     void *d0 = p.buf[s][0], *d1 = copy_x1 ? p.buf[s][1] : p.buf[s][0];
     void *e0 = p.buf[s][2], *e1 = p.buf[s][3];
-    if (p.used[s] && cudaStreamWaitEvent(p.in, p.freed[s], 0) != cudaSuccess)
+    // a slot is refilled after BOTH of its copy-outs (z0 and z1) are done
+    if (p.used[s] && (cudaStreamWaitEvent(p.in, p.freed[s], 0) != cudaSuccess ||
+                      cudaStreamWaitEvent(p.in, p.freed2[s], 0) != cudaSuccess ||
+                      cudaStreamWaitEvent(p.in2, p.freed[s], 0) != cudaSuccess ||
+                      cudaStreamWaitEvent(p.in2, p.freed2[s], 0) != cudaSuccess))
       return cuda_check("tf_eval_host: ring wait");
     if (cudaMemcpyAsync(d0, hx0 + at, bytes, cudaMemcpyHostToDevice, p.in) != cudaSuccess ||
-        (copy_x1 && cudaMemcpyAsync(d1, hx1 + at, bytes, cudaMemcpyHostToDevice, p.in) != cudaSuccess) ||
         cudaEventRecord(p.loaded[s], p.in) != cudaSuccess ||
-        cudaStreamWaitEvent(p.comp, p.loaded[s], 0) != cudaSuccess)
+        cudaStreamWaitEvent(p.comp, p.loaded[s], 0) != cudaSuccess ||
+        (copy_x1 && (cudaMemcpyAsync(d1, hx1 + at, bytes, cudaMemcpyHostToDevice, p.in2) != cudaSuccess ||
+                     cudaEventRecord(p.loaded2[s], p.in2) != cudaSuccess ||
+                     cudaStreamWaitEvent(p.comp, p.loaded2[s], 0) != cudaSuccess)))
       return cuda_check("tf_eval_host: copy-in");
     rc = tf_eval(fn, width, d0, d1, e0, e1, m, p.comp, flags);
     if (rc) return rc;
     if (cudaEventRecord(p.done[s], p.comp) != cudaSuccess ||
         cudaStreamWaitEvent(p.out, p.done[s], 0) != cudaSuccess ||
+        cudaStreamWaitEvent(p.out2, p.done[s], 0) != cudaSuccess ||
         cudaMemcpyAsync(hz0 + at, e0, bytes, cudaMemcpyDeviceToHost, p.out) != cudaSuccess ||
-        cudaMemcpyAsync(hz1 + at, e1, bytes, cudaMemcpyDeviceToHost, p.out) != cudaSuccess ||
-        cudaEventRecord(p.freed[s], p.out) != cudaSuccess)
+        cudaMemcpyAsync(hz1 + at, e1, bytes, cudaMemcpyDeviceToHost, p.out2) != cudaSuccess ||
+        cudaEventRecord(p.freed[s], p.out) != cudaSuccess ||
+        cudaEventRecord(p.freed2[s], p.out2) != cudaSuccess)
       return cuda_check("tf_eval_host: copy-out");
     p.used[s] = true;
   }
   // the results are on the host when the call returns
-  if (cudaStreamSynchronize(p.out) != cudaSuccess) return cuda_check("tf_eval_host: drain");
+  if (cudaStreamSynchronize(p.out) != cudaSuccess || cudaStreamSynchronize(p.out2) != cudaSuccess)
+    return cuda_check("tf_eval_host: drain");
   drain.armed = false;
   return TF_OK;
 }
