@@ -114,10 +114,13 @@ TF_API int tf_eval(int fn, int width, const void* x0, const void* x1, void* z0, 
  * methods on host numpy arrays, explog.py:333-349).  x0, x1, z0, z1 are HOST
  * arrays -- pinned (cudaHostAlloc / torch pin_memory) for full PCIe speed,
  * pageable memory works at the driver's staged rate.  The n elements stream
- * through a three-stage chunk pipeline on the current device (H2D, kernel,
- * D2H on three streams over a ring of device buffers) that starts after the
- * work queued on `stream`; the call returns when z0, z1 hold the results.
- * chunk = elements per pipeline chunk, 0 = default (2^20).  Dotted functions
+ * through a three-stage chunk pipeline on the current device (H2D on two copy
+ * streams, the kernel, D2H on two copy streams, over a ring of device buffers)
+ * that starts after the work queued on `stream`; the call returns when z0, z1
+ * hold the results.  chunk = elements per pipeline chunk, 0 = default (2^20).
+ * Small calls (n <= 1024, chunk == 0) use a mapped pinned buffer instead; up to
+ * 32 elements travel by value with a one-warp launch whose completion the call
+ * detects from a mapped flag (no stream synchronisation).  Dotted functions
  * take x1 = NULL.  Thread-safe: each device has two pipelines, so two calls
  * from different host threads run concurrently; further calls queue. */
 TF_API int tf_eval_host(int fn, int width, const void* x0, const void* x1, void* z0, void* z1,
