@@ -124,10 +124,28 @@ _lib = None
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with its Makefile (gcc, -ffp-contract=off)."""
+    """Compile the oracle with its Makefile (gcc, -ffp-contract=off).  Several
+    processes may call this at once (bench.py's ranks): the build runs under a
+    file lock into a temporary name that is renamed into place, so no process
+    ever loads a half-written library."""
+    import fcntl
+
     src = os.path.join(HERE, "twofold_oracle.c")
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(src):
-        subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+    def stale():
+        return force or not os.path.exists(LIB_PATH) or \
+            os.path.getmtime(LIB_PATH) < os.path.getmtime(src)
+
+    if not stale():
+        return LIB_PATH
+    os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
+    with open(os.path.join(os.path.dirname(LIB_PATH), ".build.lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if stale():
+            tmp = f"{LIB_PATH}.{os.getpid()}.tmp"
+            subprocess.run(["make", "-s", "-B", "-C", HERE, f"OUT={tmp}"], check=True)
+            os.replace(tmp, LIB_PATH)
+            force = False
     return LIB_PATH
 
 
