@@ -80,10 +80,6 @@ def main():
     print(json.dumps({k: round(v, 2) for k, v in out.items()}))
 
 
-if __name__ == "__main__":
-    main()
-
-
 def launch_cost():
     """CPU cost of one tf_eval(n=1) launch (no synchronisation) and the tiny
     kernels' device time per launch (ncu: -k regex:k_tiny)."""
@@ -106,5 +102,7 @@ def launch_cost():
     print(json.dumps({k: round(v, 2) for k, v in res.items()}))
 
 
-if __name__ == "__main__" and os.environ.get("LAUNCH_COST"):
-    launch_cost()
+if __name__ == "__main__":
+    main()
+    if os.environ.get("LAUNCH_COST"):
+        launch_cost()
