@@ -410,7 +410,9 @@ def run_ours(args):
 
     O.build()
     nt = O.default_threads()
-    m = min(args.parity_sample, n)
+    # the sample is split over the ranks: the merged counts cover the same number
+    # of elements at every N, and the CPU port's time per rank shrinks with N
+    m = min(max(1, args.parity_sample // world), n)
     cpu = None
     parity5 = {}
     for fn, _ in HEADLINE:
@@ -555,7 +557,7 @@ def run_ours(args):
     # ---- binary32 parity (config 4 samples) vs the reference and CR-sim oracles
     par32 = {}
     if not args.headline_only and args.parity32_sample > 0:
-        m32 = args.parity32_sample
+        m32 = max(1, args.parity32_sample // world)
         for fn, width, dname in PER_FN:
             if width != 32:
                 continue
