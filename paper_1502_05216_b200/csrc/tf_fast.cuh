@@ -1370,6 +1370,12 @@ TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const f
       // neither in band nor > -1)
       k[h] = RENORM || ((fabsf(yy0[h]) <= 0x1.fffffep127f) & (fabsf(yy1[h]) <= 0x1.fffffep127f));
       inb[h] = (vv[h] >= -0.5f) & (vv[h] <= 1.0f);         // explog.py:291
+#ifdef TF_T1P32_PURE
+      // measurement builds only (tools/pure_probe.py): branch-pure
+      // code, 1 = in band only, 2 = out of band only; other lanes are rejected
+      k[h] &= (TF_T1P32_PURE == 1) == inb[h];
+      inb[h] = TF_T1P32_PURE == 1;
+#endif
       // out of band: v0 > -1 and |y1 / (1 + y0)| <= 2^-14 (log1p(d) = d - d^2/2)
       k[h] &= inb[h] | ((vv[h] > -1.0f) & (fabsf(yy1[h]) * 0x1p14f <= fabsf(wv[h])));
       const bool band = (wv[h] >= 0.5f) & (wv[h] <= 2.0f);

@@ -1,3 +1,9 @@
+"""tlog1p binary32 on config 4's mix, on all-in-band and on all-out-of-band inputs
+(the ceiling of class sorting).  Compare the default build with
+    bash tools/build_variant.sh pure1 -DTF_T1P32_PURE=1   (in-band-only pipeline)
+    bash tools/build_variant.sh pure2 -DTF_T1P32_PURE=2   (out-of-band-only pipeline)
+    TWOFOLD_B200_LIB=paper_1502_05216_b200/lib/var/pure1.so python tools/pure_probe.py
+"""
 import os, sys, torch
 sys.path.insert(0, os.getcwd())
 from paper_1502_05216_b200 import _lib, api
