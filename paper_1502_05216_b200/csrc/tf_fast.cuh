@@ -1412,16 +1412,24 @@ TF_DEV void fast_tlog1p_p(const STab<float>& tb, const float (&y0i)[VW], const f
       ms[h] = k[h] ? -sx[h] : 0.0f;                         // keeps the CM1 index in range
     }
     const TF<f2> s = pexpm10_inband_p(tb, pk(ms[0], ms[1]));
-    // Newton step: one product x s, then + v + s in band, + wz out of band
-    const TF<f2> u1 = t_add_u(t_mul_u(mk(xm_v, xm_e), s), yw);
-    const TF<f2> u2 = t_add_u(u1, s);
-    TF<f2> u = mk(sel2(inb[0], inb[1], u2.v, u1.v), sel2(inb[0], inb[1], u2.e, u1.e));
+    // Newton step: one product x s, then + v + s in band, + wz out of band.
+    // In band with v1 == 0 (explog.py:268-270) the reference computes
+    // t_add_d(t_mul(w, s), v0), w = fast_two_sum(1, v0): the same product and
+    // addition with x = w, since yw is (v0, +-0) there and adding a zero error
+    // part changes no bit for v0 != 0 (v0 = +-0 goes to the drain).
+    f2 xmv = xm_v, xme = xm_e;
     const bool dot[2] = {bool(inb[0] & (ve[0] == 0.0f)), bool(inb[1] & (ve[1] == 0.0f))};
-    if (__any_sync(0xffffffffu, dot[0] | dot[1])) {       // explog.py:268-270
+    if (__any_sync(0xffffffffu, dot[0] | dot[1])) {
       const TF<f2> w1 = fast_two_sum_u(splat(1.0f), v.v);
-      const TF<f2> u0 = t_add_d_u(t_mul_u(w1, s), v.v);
-      u = mk(sel2(dot[0], dot[1], u0.v, u.v), sel2(dot[0], dot[1], u0.e, u.e));
+      xmv = sel2(dot[0], dot[1], w1.v, xm_v);
+      xme = sel2(dot[0], dot[1], w1.e, xm_e);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) k[h] &= !(dot[h] & (vv[h] == 0.0f));
     }
+    const TF<f2> u1 = t_add_u(t_mul_u(mk(xmv, xme), s), yw);
+    const TF<f2> u2 = t_add_u(u1, s);
+    const bool two[2] = {bool(inb[0] & !dot[0]), bool(inb[1] & !dot[1])};
+    const TF<f2> u = mk(sel2(two[0], two[1], u2.v, u1.v), sel2(two[0], two[1], u2.e, u1.e));
     const f2 x1 = add(u.v, u.e);
     // newton_quiet: |x1| < 2^-21 max(|sd|, 1)
     const f2 lim = mul(pk(fmaxf(fabsf(sx[0]), 1.0f), fmaxf(fabsf(sx[1]), 1.0f)), splat(0x1p-21f));
