@@ -4,7 +4,7 @@ host in 2^24-element chunks).  binary64 against the reference-equivalent oracle
 ("dv" residuals, glibc value parts); binary32 against CR-sim (fma residuals,
 correctly rounded value parts).  Dotted functions get x1 = 0 (plain argument).
 
-    python tools/parity_device.py width [log2 n] [fn ...]      (GPU box)
+    python tools/parity_device.py width [log2 n] [fn[:dist] ...]      (GPU box)
 """
 import json
 import os
@@ -25,11 +25,12 @@ chunk = min(n, 1 << 24)
 dt = torch.float64 if width == 64 else torch.float32
 rel, guard = (2.0 ** -95, 2 * 2.0 ** -1074) if width == 64 else (2.0 ** -42, 2 * 2.0 ** -149)
 L = _lib.ensure_device(0)
-for fn in fns:
+for spec in fns:
+    fn, _, dist = spec.partition(":")
     x0 = torch.empty(n, dtype=dt, device="cuda")
     x1 = torch.empty_like(x0)
-    _lib.check(L.tf_generate(_lib.DIST_CODES[DIST[family_of(fn)]], 2024, 0, n, x0.data_ptr(),
-                             x1.data_ptr(), None), "gen")
+    _lib.check(L.tf_generate(_lib.DIST_CODES[dist or DIST[family_of(fn)]], 2024, 0, n,
+                             x0.data_ptr(), x1.data_ptr(), None), "gen")
     dotted = fn in DOTTED_ARG
     if dotted:
         x1.zero_()
@@ -46,7 +47,7 @@ for fn in fns:
                                 None), "tf_compare")
     torch.cuda.synchronize()
     c = st.tolist()
-    print(json.dumps({"fn": fn, "width": width, "n": c[0], "z0_mismatch": c[1], "z0_gt1ulp": c[2],
+    print(json.dumps({"fn": fn, "dist": dist or DIST[family_of(fn)], "width": width, "n": c[0], "z0_mismatch": c[1], "z0_gt1ulp": c[2],
                       "tol_violations": c[3], "class_mismatch": c[4], "z1_bit_mismatch": c[5]}),
           flush=True)
     del x0, x1, z
