@@ -23,9 +23,9 @@ path).  Inputs are generated on the device by the shard-invariant generator;
              the same run (tf_fma_peak; MEASURED_PEAKS.json has no FP64 figure);
              traffic = ncu dram bytes of the same kernel (profiles/);
   cpu_baseline = the CPU port of the reference algorithm (oracle/, "dv" backend,
-             bit-exact to the reference package) on all host threads, timed on a
-             bounded prefix of rank 0's slice; its outputs are also the parity
-             reference for that prefix (parity_cfg5);
+             bit-exact to the reference package) on all host threads, timed over
+             rank 0's whole slice in 2^24-element chunks (~20 s); its outputs are
+             also the parity reference of every element (parity_cfg5);
   per_function = the eight (function, width) kernels at the north-star size
              2^28 on their own configs' distributions;
   parity_f32 = config 4 samples vs the reference-equivalent oracle (numpy libm)
@@ -416,20 +416,15 @@ def run_ours(args):
     cpu = None
     parity5 = {}
     for fn, _ in HEADLINE:
-        x0 = ins[fn][0][:m].cpu().numpy()
-        x1 = ins[fn][1][:m].cpu().numpy()
-        tc = time.perf_counter()
-        r0, r1 = O.evaluate(fn, 64, x0, x1, backend="dv", nthreads=nt)
-        cpu_s = time.perf_counter() - tc
-        parity5[fn] = _parity_device(L, dev, sp, outs[fn][0][:m], outs[fn][1][:m], r0, r1, 64,
-                                     args.parity_host)
-        parity5[fn]["cpu_s"] = cpu_s
+        parity5[fn] = _parity_chunked(L, dev, sp, O, fn, ins[fn], outs[fn], m, args.parity_host,
+                                      nt)
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu_s = sum(parity5[fn].pop("cpu_s") for fn, _ in HEADLINE)
         cpu = {"value": _r(2 * m / cpu_s), "unit": "elements/s", "cores": nt, "kind": "port",
                "cpu": cpu_model(),
-               "sample": f"{m} elements of each function (prefix of the cfg-5 slice), C port "
-                         f"of the reference algorithm ('dv' backend), {nt} threads"}
+               "sample": f"{m} elements of each function ({'all' if m == n else 'a prefix'} "
+                         f"of the cfg-5 slice, in 2^24-element chunks), C port of the reference "
+                         f"algorithm ('dv' backend), {nt} threads"}
     for fn, _ in HEADLINE:
         parity5[fn].pop("cpu_s", None)
         parity5[fn] = _reduce(parity5[fn], dev)
@@ -687,33 +682,39 @@ def _traffic(fn, n):
     return None
 
 
-def _parity_device(L, dev, sp, z0, z1, r0, r1, width, host_n):
-    """Parity counters of GPU (z0, z1) against reference (r0, r1): the whole
-    sample on the device (tf_compare), plus the host comparator's finer
-    statistics (ulp histogram, given-z0-match counts, worst error) on the
-    first host_n elements."""
+def _parity_chunked(L, dev, sp, O, fn, xin, zout, m, host_n, nt, chunk=1 << 24):
+    """Parity of the first m elements of a binary64 slice against the CPU port
+    (the reference algorithm, "dv" backend), chunk by chunk: counters on the
+    device (tf_compare) over all m, the host comparator's finer statistics over
+    the first host_n.  Also returns the port's total time ("cpu_s")."""
     import torch
 
     from paper_1502_05216_b200 import _lib
 
-    rel, guard = (2.0 ** -95, 2 * 2.0 ** -1074) if width == 64 else (2.0 ** -42, 2 * 2.0 ** -149)
-    t0 = torch.from_numpy(r0).to(dev)
-    t1 = torch.from_numpy(r1).to(dev)
     st = torch.zeros(6, dtype=torch.int64, device=dev)
-    _lib.check(L.tf_compare(width, z0.data_ptr(), z1.data_ptr(), t0.data_ptr(), t1.data_ptr(),
-                            z0.numel(), rel, guard, st.data_ptr(), sp), "tf_compare")
+    cpu_s, fine = 0.0, {}
+    for lo in range(0, m, chunk):
+        k = min(chunk, m - lo)
+        x0 = xin[0][lo:lo + k].cpu().numpy()
+        x1 = xin[1][lo:lo + k].cpu().numpy()
+        tc = time.perf_counter()
+        r0, r1 = O.evaluate(fn, 64, x0, x1, backend="dv", nthreads=nt)
+        cpu_s += time.perf_counter() - tc
+        t0, t1 = torch.from_numpy(r0).to(dev), torch.from_numpy(r1).to(dev)
+        _lib.check(L.tf_compare(64, zout[0][lo:].data_ptr(), zout[1][lo:].data_ptr(),
+                                t0.data_ptr(), t1.data_ptr(), k, 2.0 ** -95, 2 * 2.0 ** -1074,
+                                st.data_ptr(), sp), "tf_compare")
+        if lo == 0 and host_n:
+            h = min(host_n, k)
+            fine = _host_compare(zout[0][:h].cpu().numpy(), zout[1][:h].cpu().numpy(), r0[:h],
+                                 r1[:h], 64)
+            fine = {"host_n": h} | {key: fine[key] for key in (
+                "tol_violations_given_z0_match", "z1_bit_mismatch_given_z0_match",
+                "worst_rel_log2", "z0_ulp_hist")}
     torch.cuda.synchronize()
     c = st.tolist()
-    out = {"n": c[0], "z0_mismatch": c[1], "z0_gt1ulp": c[2], "tol_violations": c[3],
-           "class_mismatch": c[4], "z1_bit_mismatch": c[5]}
-    k = min(host_n, z0.numel())
-    if k:
-        h = _host_compare(z0[:k].cpu().numpy(), z1[:k].cpu().numpy(), r0[:k], r1[:k], width)
-        out["host_n"] = k
-        for key in ("tol_violations_given_z0_match", "z1_bit_mismatch_given_z0_match",
-                    "worst_rel_log2", "z0_ulp_hist"):
-            out[key] = h[key]
-    return out
+    return {"n": c[0], "z0_mismatch": c[1], "z0_gt1ulp": c[2], "tol_violations": c[3],
+            "class_mismatch": c[4], "z1_bit_mismatch": c[5], **fine, "cpu_s": cpu_s}
 
 
 def _host_compare(z0, z1, r0, r1, width):
@@ -770,8 +771,9 @@ def main():
                     help="reference arm: elements per function per step (prefix of the stream)")
     ap.add_argument("--py-ref-sample", type=int, default=2048,
                     help="reference arm: elements per process per function for the Python package")
-    ap.add_argument("--parity-sample", type=int, default=1 << 26,
-                    help="cfg-5 elements per function checked against the CPU port")
+    ap.add_argument("--parity-sample", type=int, default=1 << 30,
+                    help="cfg-5 elements per function checked against the CPU port (default: "
+                         "all of them)")
     ap.add_argument("--parity-host", type=int, default=1 << 22,
                     help="of those, elements also run through the host comparator")
     ap.add_argument("--parity32-sample", type=int, default=1 << 22)
