@@ -100,9 +100,12 @@ int setup(HostPipe& p, int64_t bytes) {
 // element per call) skip the chunk pipeline: the operands go into a mapped
 // pinned buffer the kernel reads and writes directly over PCIe (zero-copy).
 // Up to 32 elements take the tiny kernel: operands by value with the launch,
-// results into the mapped buffer, then a sequence number into a mapped flag: the caller spins on that flag instead of
-// synchronising the stream (a kernel that never stores it -- a launch or
-// device fault -- is caught by the bounded spin, then the stream status).
+// results into the mapped buffer, then a sequence number into a mapped flag.
+// The caller spins on that flag instead of synchronising the stream (a kernel
+// that never stores it -- a launch or device fault -- is caught by the bounded
+// spin, then by the stream status).  Consecutive calls may use different
+// streams: a kernel's last access to the buffer is its flag store, which the
+// previous call waited for.
 constexpr int64_t SMALL_N = 1024;
 constexpr int64_t TINY_N = 32;
 struct SmallBuf {
